@@ -1,0 +1,331 @@
+#!/usr/bin/env python
+"""Benchmark of the sparse Sinkhorn-WMD hot path (BASELINE.json metric:
+"Sinkhorn nnz-updates/sec (nnz(c) x v_r x iters)").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config scaling] [--path auto|iter|fused]
+    python bench.py --impl reference ...   # the FP64 CPU oracle (this tier's reference arm)
+
+One step = one wmd_query: K~ build + all Sinkhorn iterations + final step + FP64 fallback
+(+ the NCCL all-gather of the distances when N > 1), on synthetic inputs already resident in
+HBM. Multi-GPU: launched by torch.distributed.run, one process per GPU, nnz-balanced document
+shards (strong scaling: the total workload is fixed). Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "Sinkhorn nnz-updates/sec (nnz(c) x v_r x iters)"
+UNIT = "nnz-updates/s"
+L2_BYTES = 126 * 2 ** 20
+# Measured on this pool's B200 (profiles/r01_gather_bw.jsonl): random 128-B row gathers from an
+# L2-resident table, all SMs. MEASURED_PEAKS.json has no L2 figure.
+L2_GATHER_GBS = 20112.2
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "MEASURED_PEAKS.json"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_oracle_rate(wl, q, w, target_s: float, seed: int = 0):
+    """Time the FP64 oracle (as it stands) on a bounded document sample; returns dict."""
+    import oracle
+    cfg = wl.cfg
+    rng = np.random.default_rng(seed)
+    # calibrate the sample: ~0.2 s probe, then scale to target_s
+    n = min(wl.N, 200)
+    docs = np.sort(rng.choice(wl.N, n, replace=False))
+    cp, ri, va = synth.subset_docs(wl.col_ptr, wl.row_idx, wl.val, docs)
+    t0 = time.perf_counter()
+    oracle.sinkhorn_wmd(wl.E, cp, ri, va, q, w, cfg.lam, cfg.iters)
+    dt = time.perf_counter() - t0
+    n2 = int(min(wl.N, max(n, n * target_s / max(dt, 1e-3))))
+    docs = np.sort(rng.choice(wl.N, n2, replace=False))
+    cp, ri, va = synth.subset_docs(wl.col_ptr, wl.row_idx, wl.val, docs)
+    t0 = time.perf_counter()
+    oracle.sinkhorn_wmd(wl.E, cp, ri, va, q, w, cfg.lam, cfg.iters)
+    dt = time.perf_counter() - t0
+    units = int(cp[-1]) * len(q) * cfg.iters
+    return {"value": units / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{n2} of {wl.N} docs ({int(cp[-1])} nnz), query 0, full build of M for the "
+                      f"sample's words + {cfg.iters} iterations + final, FP64 single thread, {dt:.2f} s"}
+
+
+def run_reference(args, wl):
+    """--impl reference: the FP64 CPU oracle, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    cfg = wl.cfg
+    q, w = wl.queries[0]
+    rng = np.random.default_rng(1)
+    per_step = float(os.environ.get("WMD_REF_STEP_S", "4.0"))
+    # size one step's doc sample so a step takes ~per_step seconds
+    probe = cpu_oracle_rate(wl, q, w, target_s=0.5)
+    nnz_per_s = probe["value"] / (len(q) * cfg.iters)
+    n_docs = int(min(wl.N, max(10, per_step * nnz_per_s / (wl.nnz / wl.N))))
+    times, units_tot = [], 0
+    for s in range(args.warmup + args.steps):
+        docs = np.sort(rng.choice(wl.N, n_docs, replace=False))
+        cp, ri, va = synth.subset_docs(wl.col_ptr, wl.row_idx, wl.val, docs)
+        t0 = time.perf_counter()
+        oracle.sinkhorn_wmd(wl.E, cp, ri, va, q, w, cfg.lam, cfg.iters)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+            units_tot += int(cp[-1]) * len(q) * cfg.iters
+    T = sum(times)
+    value = units_tot / T
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded Zipf bag-of-words, N(0,1) embeddings; BASELINE.json config)",
+        "config": config_dict(cfg, wl, args, sample_docs=n_docs),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"each step: {n_docs} random docs of {wl.N}, query 0, FP64 single thread"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(cfg, wl, args, **extra):
+    d = {"workload": cfg.name, "V": cfg.V, "d": cfg.d, "N": cfg.N, "nnz": wl.nnz,
+         "v_r": int(len(wl.queries[0][0])), "lambda": cfg.lam, "iters": cfg.iters,
+         "words_per_doc": f"{cfg.doc_lo}-{cfg.doc_hi}", "zipf_s": cfg.zipf_s,
+         "parallelism": f"doc-shard x{args.gpus}" if args.gpus > 1 else "1 GPU",
+         "l2": ("inputs larger than L2 (E %.0f MB + c %.0f MB > 126 MB)" % (cfg.V * cfg.d * 4 / 1e6, wl.nnz * 8 / 1e6))
+         if (cfg.V * cfg.d * 4 + wl.nnz * 8) > 2 * L2_BYTES else "L2 flushed (256 MB write) before every timed step"}
+    d.update(extra)
+    return d
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=os.environ.get("WMD_BENCH_CONFIG", "scaling"),
+                    choices=sorted(synth.CONFIGS))
+    ap.add_argument("--path", default="auto", choices=["auto", "iter", "fused"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    wl = synth.make_workload(args.config)
+    if args.impl == "reference":
+        return run_reference(args, wl)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2005_06727_b200 import wmd
+    from paper_2005_06727_b200.sharded import ShardedEngine, gather_distances
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    cfg = wl.cfg
+    q, w = wl.queries[0]
+    v_r = len(q)
+    path = {"auto": wmd.WMD_PATH_AUTO, "iter": wmd.WMD_PATH_PER_ITER, "fused": wmd.WMD_PATH_FUSED}[args.path]
+    E = torch.from_numpy(wl.E).cuda()
+    eng = ShardedEngine(E, wl.col_ptr, wl.row_idx, wl.val, rank, world, local_rank, path=path, timing=True)
+    h = eng.engine.h
+    stream = torch.cuda.current_stream()
+    small = (cfg.V * cfg.d * 4 + wl.nnz * 8) <= 2 * L2_BYTES
+    flush = torch.empty(256 * 2 ** 20 // 4, dtype=torch.float32, device="cuda") if small else None
+
+    # ---------------------------------------------------------------- device-resident timing
+    for _ in range(args.warmup):
+        eng.query(q, w, cfg.lam, cfg.iters)
+    torch.cuda.synchronize()
+    eng.engine.sync()
+    wmd.wmd_reset_stats(h)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local_rank) as clk:
+        for s in range(args.steps):
+            if flush is not None:
+                flush.fill_(float(s))
+            barrier()
+            torch.cuda.synchronize()
+            ev[s][0].record(stream)
+            out = eng.query(q, w, cfg.lam, cfg.iters)
+            ev[s][1].record(stream)
+            torch.cuda.synchronize()
+    barrier()
+    t_ms = sum(a.elapsed_time(b) for a, b in ev)
+    st = wmd.wmd_get_stats(h) if eng.n_local > 0 else None
+    eng.engine.sync()
+    st_sync = wmd.wmd_get_stats(h) if eng.n_local > 0 else None
+    t_max = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    T = float(t_max.item()) / 1e3
+    units = wl.nnz * v_r * cfg.iters * args.steps
+    value = units / T
+    check = out.float().cpu().numpy()
+    assert np.all(np.isfinite(check)), "non-finite distances"
+
+    # ---------------------------------------------------------------- end-to-end through the C ABI
+    # host query arrays -> wmd_query (H2D inside) -> [all-gather] -> D2H into pinned host memory
+    pin_out = torch.empty(wl.N, dtype=torch.float32, pin_memory=True)
+    q_pin = torch.from_numpy(q.copy()).pin_memory()
+    w_pin = torch.from_numpy(w.copy()).pin_memory()
+    e2e_ms = 0.0
+    for s in range(args.warmup + args.steps):
+        if flush is not None:
+            flush.fill_(float(s))
+        barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        if world == 1:
+            wmd.wmd_query(h, q_pin.numpy(), w_pin.numpy(), cfg.lam, cfg.iters, pin_out)  # host out
+        else:
+            res = eng.query(q_pin.numpy(), w_pin.numpy(), cfg.lam, cfg.iters)
+            pin_out.copy_(res, non_blocking=True)
+        b.record(stream)
+        torch.cuda.synchronize()
+        if s >= args.warmup:
+            e2e_ms += a.elapsed_time(b)
+    e2e_t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_value = units / (float(e2e_t.item()) / 1e3)
+    assert np.array_equal(pin_out.numpy(), check), "e2e result differs from the device-resident run"
+
+    if rank == 0:
+        peaks, peak_src = _peaks()
+        launches_per_query = st["kernel_launches"] / max(1, st["queries"]) if st else 0
+        nl, nnz_l = eng.n_local, eng.nnz_local
+        path_used = st["last_path"] if st else 0
+        if path_used == wmd.WMD_PATH_PER_ITER:
+            n_iter_launch = st["iter_launches"]
+            t_launch = st["iter_ms"] / 1e3 / max(1, n_iter_launch)
+            B_it = 8 * nnz_l + 4 * (nl + 1) + 8 * v_r * nl      # streamed (HBM) bytes per launch
+            G_it = 4 * v_r * nnz_l                              # K~ row gathers (L2) per launch
+            roofline = {
+                "kernel": "sddmm_spmm_iter", "bound": "l2",
+                "achieved": (B_it + G_it) / t_launch / 1e9, "peak": L2_GATHER_GBS, "unit": "GB/s",
+                "frac": (B_it + G_it) / t_launch / 1e9 / L2_GATHER_GBS,
+                "peak_source": "measured L2 row-gather bandwidth, profiles/r01_gather_bw.jsonl",
+                "algorithmic_bytes_per_launch": {"streamed": B_it, "gathered": G_it},
+                "launch_ms": t_launch * 1e3,
+                "hbm": {"achieved": B_it / t_launch / 1e9, "peak": peaks["hbm_gbs"],
+                        "frac": B_it / t_launch / 1e9 / peaks["hbm_gbs"], "peak_source": peak_src},
+                "roof_time_frac": max(B_it / (peaks["hbm_gbs"] * 1e9), (B_it + G_it) / (L2_GATHER_GBS * 1e9)) / t_launch,
+                "traffic": None,
+                "share_of_step": st["iter_ms"] / max(st["query_ms"], 1e-9),
+            }
+        else:
+            t_launch = st["iter_ms"] / 1e3 / max(1, st["iter_launches"])
+            flops = 4.0 * v_r * nnz_l * (cfg.iters + 1)           # 2 FMAs per nnz-update
+            clk = peaks.get("sm_max_mhz", 1965.0)
+            peak_tf = 148 * 128 * 2 * clk * 1e6 / 1e12
+            roofline = {
+                "kernel": "sinkhorn_fused", "bound": "alu",
+                "achieved": flops / t_launch / 1e12, "peak": peak_tf, "unit": "TFLOP/s",
+                "frac": flops / t_launch / 1e12 / peak_tf,
+                "peak_source": f"148 SMs x 128 FP32 FMA/clk x 2 x {clk:.0f} MHz (DESIGN.md §5)",
+                "launch_ms": t_launch * 1e3, "traffic": None,
+                "share_of_step": st["iter_ms"] / max(st["query_ms"], 1e-9),
+            }
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded Zipf bag-of-words, N(0,1) embeddings; BASELINE.json config)",
+            "config": config_dict(cfg, wl, args, path=args.path),
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(v_r * 8),
+                    "d2h_bytes_per_step": int(wl.N * 4)},
+            "gpu_launches": int(st["kernel_launches"]) if st else 0,
+            "roofline": roofline,
+            "phases_ms_per_step": {k: st[k] / args.steps for k in ("build_ms", "iter_ms", "final_ms", "fallback_ms", "query_ms")},
+            "fallback_docs": int(st_sync["fallback_docs"]) if st_sync else 0,
+            "launches_per_query": launches_per_query,
+            "clocks": clk.summary(),
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_oracle_rate(wl, q, w, target_s=float(os.environ.get("WMD_CPU_S", "12")))
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,653 @@
+// wmd_host.cpp — host runtime behind the C ABI in include/wmd.h.
+//
+// Owns the handle (device buffers, stream, options, statistics), validates every input on the
+// host (integer bookkeeping is bit-exact and never touches floating point except the FP64
+// normalisation sums), sorts the query (Algorithm 1 line 1) and enqueues the
+// kernels of wmd_kernels.cu on the handle's stream. No arithmetic of the method runs here.
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "wmd_internal.h"
+
+using wmd::Entry;
+
+namespace {
+
+constexpr double kWeightTol = 1e-5;  // |sum - 1| for FP32 weights summed in FP64 (R23)
+
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = true;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();  // clear: unregistered host memory on old runtimes
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaError_t ensure(size_t count) {
+    if (count <= n && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaMalloc(&p, sizeof(T) * std::max<size_t>(count, 1));
+    if (e == cudaSuccess) n = count;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+struct PhaseEvents {
+  cudaEvent_t ev[5];  // start, after build, after iterations, after final, after fallback
+};
+
+}  // namespace
+
+struct wmd_handle {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  // embeddings
+  DevBuf<float> E;
+  int64_t V = 0;
+  int32_t d = 0;
+  // targets
+  bool has_targets = false;
+  DevBuf<int32_t> doc_ptr;
+  DevBuf<Entry> ent;
+  int64_t N = 0, nnz = 0, max_doc_nnz = 0;
+  // per-query device state
+  DevBuf<int32_t> sel;       // WMD_MAX_VR
+  DevBuf<float> rpad;        // WMD_MAX_VR (zero padded to ld)
+  DevBuf<float> Kt, Mt;      // V * ld: K~ and M (FP32, vocab-major)
+  DevBuf<float> colmin;      // V
+  DevBuf<float> ua, ub;      // N * ld
+  DevBuf<float> dist_tmp;    // N (host-output queries)
+  DevBuf<uint8_t> flags;     // N
+  DevBuf<int32_t> flagged;   // N
+  DevBuf<int32_t> counters;  // [0] flagged count, [1] breakdown, [2] fallback count, [3] scratch
+  DevBuf<double> fb_scratch;
+  // pinned staging for the query upload (double buffered)
+  void* stage[2] = {nullptr, nullptr};
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+  int stage_slot = 0;
+  // last query
+  int32_t v_r = 0, ld = 0, path_used = 0;
+  bool u_valid = false;
+  const float* u_last = nullptr;
+  std::vector<int32_t> h_sel;
+  std::vector<float> h_r;
+  // options
+  int64_t opt_path = WMD_PATH_AUTO, opt_timing = 0, opt_fallback = 1, opt_graph = 0;
+  // stats
+  wmd_stats st{};
+  std::vector<PhaseEvents> events;
+  std::string err;
+};
+
+namespace {
+
+wmd_status fail(wmd_handle* h, wmd_status s, const char* fmt, ...) {
+  if (h) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    h->err = buf;
+  }
+  return s;
+}
+
+wmd_status cuda_fail(wmd_handle* h, cudaError_t e, const char* what) {
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    return fail(h, WMD_ERR_OUT_OF_MEMORY, "%s: %s", what, cudaGetErrorString(e));
+  }
+  return fail(h, WMD_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define CK(h, call)                                                    \
+  do {                                                                 \
+    cudaError_t e_ = (call);                                           \
+    if (e_ != cudaSuccess) return cuda_fail((h), e_, #call);           \
+  } while (0)
+
+int32_t round_up8(int32_t x) { return (x + 7) / 8 * 8; }
+
+// Pure-host CSC validation; `bad` receives the first offending column (or nonzero for
+// out-of-range ids) and `msg` a description.
+wmd_status validate_csc(const int64_t* col_ptr, const int32_t* row_idx, const float* val,
+                        int64_t N, int64_t nnz, int64_t V, int64_t* bad, std::string* msg) {
+  if (bad) *bad = -1;
+  if (!col_ptr || !row_idx || !val || N < 1 || nnz < 1 || V < 1) {
+    if (msg) *msg = "NULL array or N/nnz/V < 1";
+    return WMD_ERR_INVALID_ARGUMENT;
+  }
+  if (col_ptr[0] != 0 || col_ptr[N] != nnz) {
+    if (msg) *msg = "col_ptr[0] must be 0 and col_ptr[N] must equal nnz";
+    return WMD_ERR_MALFORMED_CSC;
+  }
+  for (int64_t j = 0; j < N; ++j) {
+    if (col_ptr[j + 1] < col_ptr[j]) {
+      if (bad) *bad = j;
+      if (msg) *msg = "col_ptr decreases at column " + std::to_string(j);
+      return WMD_ERR_MALFORMED_CSC;
+    }
+  }
+  for (int64_t j = 0; j < N; ++j) {
+    const int64_t b = col_ptr[j], e = col_ptr[j + 1];
+    if (b == e) {
+      if (bad) *bad = j;
+      if (msg) *msg = "empty document " + std::to_string(j);
+      return WMD_ERR_EMPTY_DOCUMENT;
+    }
+    double s = 0.0;
+    for (int64_t q = b; q < e; ++q) {
+      const int32_t k = row_idx[q];
+      if (k < 0 || k >= V) {
+        if (bad) *bad = j;
+        if (msg) *msg = "word id " + std::to_string(k) + " out of range in document " + std::to_string(j);
+        return WMD_ERR_INDEX_OUT_OF_RANGE;
+      }
+      if (q > b && k <= row_idx[q - 1]) {
+        if (bad) *bad = j;
+        if (msg) *msg = "row ids not strictly increasing in document " + std::to_string(j);
+        return WMD_ERR_MALFORMED_CSC;
+      }
+      const float w = val[q];
+      if (!(w > 0.f) || !std::isfinite(w)) {
+        if (bad) *bad = j;
+        if (msg) *msg = "weight not finite and > 0 in document " + std::to_string(j);
+        return WMD_ERR_BAD_WEIGHTS;
+      }
+      s += (double)w;
+    }
+    if (std::fabs(s - 1.0) > kWeightTol) {
+      if (bad) *bad = j;
+      if (msg) *msg = "document " + std::to_string(j) + " weights do not sum to 1";
+      return WMD_ERR_BAD_WEIGHTS;
+    }
+  }
+  return WMD_OK;
+}
+
+wmd_status validate_query(const int32_t* ids, const float* w, int32_t n, int64_t V, int64_t* bad,
+                          std::string* msg, std::vector<int32_t>* sel_out,
+                          std::vector<float>* r_out) {
+  if (bad) *bad = -1;
+  if (!ids || !w || n < 1 || n > WMD_MAX_VR || V < 1) {
+    if (msg) *msg = "NULL query or v_r outside [1, WMD_MAX_VR]";
+    return WMD_ERR_INVALID_ARGUMENT;
+  }
+  double s = 0.0;
+  for (int32_t q = 0; q < n; ++q) {
+    if (ids[q] < 0 || ids[q] >= V) {
+      if (bad) *bad = q;
+      if (msg) *msg = "query id out of range at position " + std::to_string(q);
+      return WMD_ERR_INDEX_OUT_OF_RANGE;
+    }
+    if (!(w[q] > 0.f) || !std::isfinite(w[q])) {
+      if (bad) *bad = q;
+      if (msg) *msg = "query weight not finite and > 0 at position " + std::to_string(q);
+      return WMD_ERR_BAD_WEIGHTS;
+    }
+    s += (double)w[q];
+  }
+  if (std::fabs(s - 1.0) > kWeightTol) {
+    if (msg) *msg = "query weights do not sum to 1";
+    return WMD_ERR_BAD_WEIGHTS;
+  }
+  // Algorithm 1 line 1: the selected rows in ascending vocabulary order (stable sort by id).
+  std::vector<int32_t> perm(n);
+  std::iota(perm.begin(), perm.end(), 0);
+  std::stable_sort(perm.begin(), perm.end(), [&](int32_t a, int32_t b) { return ids[a] < ids[b]; });
+  for (int32_t q = 1; q < n; ++q) {
+    if (ids[perm[q]] == ids[perm[q - 1]]) {
+      if (bad) *bad = perm[q];
+      if (msg) *msg = "duplicate query id " + std::to_string(ids[perm[q]]);
+      return WMD_ERR_BAD_WEIGHTS;
+    }
+  }
+  if (sel_out && r_out) {
+    sel_out->resize(n);
+    r_out->resize(n);
+    for (int32_t q = 0; q < n; ++q) {
+      (*sel_out)[q] = ids[perm[q]];
+      (*r_out)[q] = w[perm[q]];
+    }
+  }
+  return WMD_OK;
+}
+
+void drop_targets(wmd_handle* h) {
+  h->has_targets = false;
+  h->doc_ptr.release();
+  h->ent.release();
+  h->N = h->nnz = h->max_doc_nnz = 0;
+  h->u_valid = false;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* wmd_version(void) { return "wmd_b200 0.1 (sm_100a)"; }
+
+const char* wmd_status_string(wmd_status s) {
+  switch (s) {
+    case WMD_OK: return "ok";
+    case WMD_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case WMD_ERR_INDEX_OUT_OF_RANGE: return "index out of range";
+    case WMD_ERR_EMPTY_DOCUMENT: return "empty document";
+    case WMD_ERR_MALFORMED_CSC: return "malformed CSC matrix";
+    case WMD_ERR_BAD_WEIGHTS: return "bad weights";
+    case WMD_ERR_NONFINITE_EMBEDDING: return "non-finite embedding";
+    case WMD_ERR_STATE: return "invalid state";
+    case WMD_ERR_NUMERICAL_BREAKDOWN: return "numerical breakdown";
+    case WMD_ERR_OUT_OF_MEMORY: return "out of device memory";
+    case WMD_ERR_CUDA: return "CUDA error";
+  }
+  return "unknown status";
+}
+
+const char* wmd_last_error(const wmd_handle* h) { return h ? h->err.c_str() : ""; }
+
+wmd_status wmd_partition(const int64_t* col_ptr, int64_t N, int32_t P, int64_t* bounds) {
+  if (!col_ptr || !bounds || N < 0 || P < 1) return WMD_ERR_INVALID_ARGUMENT;
+  const int64_t nnz = col_ptr[N];
+  bounds[0] = 0;
+  for (int32_t g = 1; g < P; ++g) {
+    const int64_t target = (g * nnz + P - 1) / P;  // ceil(g * nnz / P)
+    bounds[g] = std::lower_bound(col_ptr, col_ptr + N + 1, target) - col_ptr;  // binary search
+    if (bounds[g] > N) bounds[g] = N;
+  }
+  bounds[P] = N;
+  return WMD_OK;
+}
+
+wmd_status wmd_validate_csc(const int64_t* col_ptr, const int32_t* row_idx, const float* val,
+                            int64_t N, int64_t nnz, int64_t V, int64_t* bad_index) {
+  return validate_csc(col_ptr, row_idx, val, N, nnz, V, bad_index, nullptr);
+}
+
+wmd_status wmd_validate_query(const int32_t* ids, const float* weights, int32_t n, int64_t V,
+                              int64_t* bad_index) {
+  return validate_query(ids, weights, n, V, bad_index, nullptr, nullptr, nullptr);
+}
+
+wmd_status wmd_create(const float* vocab_emb, int64_t V, int32_t d, int32_t device, wmd_handle** out) {
+  if (!out) return WMD_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  if (!vocab_emb || V < 1 || d < 1 || V >= (int64_t(1) << 31) || device < 0) return WMD_ERR_INVALID_ARGUMENT;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device >= ndev) {
+    cudaGetLastError();
+    return WMD_ERR_CUDA;
+  }
+  DeviceGuard g(device);
+  if (!g.ok) return WMD_ERR_CUDA;
+  wmd_handle* h = new (std::nothrow) wmd_handle();
+  if (!h) return WMD_ERR_OUT_OF_MEMORY;
+  h->device = device;
+  h->V = V;
+  h->d = d;
+  auto bail = [&](wmd_status s) { wmd_destroy(h); return s; };
+  if (cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking) != cudaSuccess) return bail(WMD_ERR_CUDA);
+  h->stream = h->own_stream;
+  const size_t n = (size_t)V * d;
+  if (h->E.ensure(n) != cudaSuccess) return bail(WMD_ERR_OUT_OF_MEMORY);
+  if (is_device_ptr(vocab_emb)) {
+    if (cudaMemcpyAsync(h->E.p, vocab_emb, n * sizeof(float), cudaMemcpyDeviceToDevice, h->stream) != cudaSuccess)
+      return bail(WMD_ERR_CUDA);
+    if (h->counters.ensure(4) != cudaSuccess) return bail(WMD_ERR_OUT_OF_MEMORY);
+    cudaMemsetAsync(h->counters.p, 0, 4 * sizeof(int32_t), h->stream);
+    wmd::launch_check_finite(h->E.p, (int64_t)n, h->counters.p + 3, h->stream);
+    int32_t bad = 0;
+    if (cudaMemcpyAsync(&bad, h->counters.p + 3, sizeof bad, cudaMemcpyDeviceToHost, h->stream) != cudaSuccess ||
+        cudaStreamSynchronize(h->stream) != cudaSuccess)
+      return bail(WMD_ERR_CUDA);
+    if (bad) return bail(WMD_ERR_NONFINITE_EMBEDDING);
+  } else {
+    for (size_t i = 0; i < n; ++i)
+      if (!std::isfinite(vocab_emb[i])) return bail(WMD_ERR_NONFINITE_EMBEDDING);
+    if (cudaMemcpy(h->E.p, vocab_emb, n * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess)
+      return bail(WMD_ERR_CUDA);
+  }
+  if (h->sel.ensure(WMD_MAX_VR) != cudaSuccess || h->rpad.ensure(WMD_MAX_VR) != cudaSuccess ||
+      h->colmin.ensure((size_t)V) != cudaSuccess || h->counters.ensure(4) != cudaSuccess)
+    return bail(WMD_ERR_OUT_OF_MEMORY);
+  for (int s = 0; s < 2; ++s) {
+    if (cudaMallocHost(&h->stage[s], WMD_MAX_VR * 8) != cudaSuccess) return bail(WMD_ERR_OUT_OF_MEMORY);
+    if (cudaEventCreateWithFlags(&h->stage_ev[s], cudaEventDisableTiming) != cudaSuccess) return bail(WMD_ERR_CUDA);
+  }
+  if (cudaStreamSynchronize(h->stream) != cudaSuccess) return bail(WMD_ERR_CUDA);
+  *out = h;
+  return WMD_OK;
+}
+
+void wmd_destroy(wmd_handle* h) {
+  if (!h) return;
+  DeviceGuard g(h->device);
+  if (h->own_stream) cudaStreamSynchronize(h->own_stream);
+  if (h->stream && h->stream != h->own_stream) cudaStreamSynchronize(h->stream);
+  for (auto& pe : h->events)
+    for (auto& e : pe.ev) cudaEventDestroy(e);
+  for (int s = 0; s < 2; ++s) {
+    if (h->stage[s]) cudaFreeHost(h->stage[s]);
+    if (h->stage_ev[s]) cudaEventDestroy(h->stage_ev[s]);
+  }
+  h->E.release(); h->doc_ptr.release(); h->ent.release(); h->sel.release(); h->rpad.release();
+  h->Kt.release(); h->Mt.release(); h->colmin.release(); h->ua.release(); h->ub.release();
+  h->dist_tmp.release(); h->flags.release(); h->flagged.release(); h->counters.release();
+  h->fb_scratch.release();
+  if (h->own_stream) cudaStreamDestroy(h->own_stream);
+  delete h;
+}
+
+wmd_status wmd_set_stream(wmd_handle* h, void* cuda_stream) {
+  if (!h) return WMD_ERR_INVALID_ARGUMENT;
+  h->stream = cuda_stream ? (cudaStream_t)cuda_stream : h->own_stream;
+  return WMD_OK;
+}
+
+wmd_status wmd_set_option(wmd_handle* h, int32_t option, int64_t value) {
+  if (!h) return WMD_ERR_INVALID_ARGUMENT;
+  switch (option) {
+    case WMD_OPT_PATH:
+      if (value < WMD_PATH_AUTO || value > WMD_PATH_FUSED) return fail(h, WMD_ERR_INVALID_ARGUMENT, "bad path");
+      h->opt_path = value;
+      return WMD_OK;
+    case WMD_OPT_TIMING: h->opt_timing = value != 0; return WMD_OK;
+    case WMD_OPT_FALLBACK: h->opt_fallback = value != 0; return WMD_OK;
+    case WMD_OPT_GRAPH: h->opt_graph = value != 0; return WMD_OK;
+  }
+  return fail(h, WMD_ERR_INVALID_ARGUMENT, "unknown option %d", option);
+}
+
+wmd_status wmd_set_targets(wmd_handle* h, const int64_t* col_ptr, const int32_t* row_idx,
+                           const float* val, int64_t N, int64_t nnz) {
+  if (!h) return WMD_ERR_INVALID_ARGUMENT;
+  h->err.clear();
+  DeviceGuard g(h->device);
+  if (!g.ok) return fail(h, WMD_ERR_CUDA, "cudaSetDevice failed");
+  drop_targets(h);
+  if (!col_ptr || !row_idx || !val || N < 1 || nnz < 1 || nnz >= (int64_t(1) << 31) || N >= (int64_t(1) << 31))
+    return fail(h, WMD_ERR_INVALID_ARGUMENT, "NULL array, N/nnz < 1, or nnz >= 2^31");
+  // Device inputs are brought to the host once for validation (bit-exact integer checks).
+  std::vector<int64_t> hc;
+  std::vector<int32_t> hr;
+  std::vector<float> hv;
+  if (is_device_ptr(col_ptr)) {
+    hc.resize(N + 1);
+    CK(h, cudaMemcpy(hc.data(), col_ptr, (N + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    col_ptr = hc.data();
+  }
+  if (col_ptr[N] != nnz) return fail(h, WMD_ERR_MALFORMED_CSC, "col_ptr[N] != nnz");
+  if (is_device_ptr(row_idx)) {
+    hr.resize(nnz);
+    CK(h, cudaMemcpy(hr.data(), row_idx, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    row_idx = hr.data();
+  }
+  if (is_device_ptr(val)) {
+    hv.resize(nnz);
+    CK(h, cudaMemcpy(hv.data(), val, nnz * sizeof(float), cudaMemcpyDeviceToHost));
+    val = hv.data();
+  }
+  int64_t bad = -1;
+  std::string msg;
+  wmd_status s = validate_csc(col_ptr, row_idx, val, N, nnz, h->V, &bad, &msg);
+  if (s != WMD_OK) return fail(h, s, "%s", msg.c_str());
+  std::vector<int32_t> dp(N + 1);
+  int64_t mx = 0;
+  for (int64_t j = 0; j <= N; ++j) dp[j] = (int32_t)col_ptr[j];
+  for (int64_t j = 0; j < N; ++j) mx = std::max(mx, col_ptr[j + 1] - col_ptr[j]);
+  std::vector<Entry> en(nnz);
+  for (int64_t q = 0; q < nnz; ++q) en[q] = Entry{row_idx[q], val[q]};
+  CK(h, h->doc_ptr.ensure(N + 1));
+  CK(h, h->ent.ensure(nnz));
+  CK(h, cudaMemcpyAsync(h->doc_ptr.p, dp.data(), (N + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
+  CK(h, cudaMemcpyAsync(h->ent.p, en.data(), nnz * sizeof(Entry), cudaMemcpyHostToDevice, h->stream));
+  CK(h, h->flags.ensure(N));
+  CK(h, h->flagged.ensure(N));
+  CK(h, h->dist_tmp.ensure(N));
+  CK(h, h->fb_scratch.ensure(wmd::fallback_scratch_bytes(mx) / sizeof(double)));
+  CK(h, cudaStreamSynchronize(h->stream));
+  h->N = N;
+  h->nnz = nnz;
+  h->max_doc_nnz = mx;
+  h->has_targets = true;
+  return WMD_OK;
+}
+
+wmd_status wmd_query(wmd_handle* h, const int32_t* query_ids, const float* query_weights,
+                     int32_t n, float lambda, int32_t iters, float* out_dist) {
+  if (!h) return WMD_ERR_INVALID_ARGUMENT;
+  h->err.clear();
+  if (!h->has_targets) return fail(h, WMD_ERR_STATE, "wmd_query before wmd_set_targets");
+  if (!out_dist || !(lambda > 0.f) || !std::isfinite(lambda) || iters < 0)
+    return fail(h, WMD_ERR_INVALID_ARGUMENT, "out_dist NULL, lambda not finite > 0, or iters < 0");
+  int64_t bad = -1;
+  std::string msg;
+  wmd_status s = validate_query(query_ids, query_weights, n, h->V, &bad, &msg, &h->h_sel, &h->h_r);
+  if (s != WMD_OK) return fail(h, s, "%s", msg.c_str());
+  DeviceGuard g(h->device);
+  if (!g.ok) return fail(h, WMD_ERR_CUDA, "cudaSetDevice failed");
+
+  const int32_t v_r = n, ld = round_up8(n);
+  const int64_t N = h->N;
+  CK(h, h->Kt.ensure((size_t)h->V * ld));
+  CK(h, h->Mt.ensure((size_t)h->V * ld));
+  CK(h, h->ua.ensure((size_t)N * ld));
+  CK(h, h->ub.ensure((size_t)N * ld));
+  cudaStream_t st = h->stream;
+
+  // Upload (sel, r padded with zeros to ld) from pinned staging, double-buffered.
+  const int slot = h->stage_slot;
+  h->stage_slot ^= 1;
+  CK(h, cudaEventSynchronize(h->stage_ev[slot]));
+  int32_t* ssel = (int32_t*)h->stage[slot];
+  float* sr = (float*)((char*)h->stage[slot] + WMD_MAX_VR * 4);
+  std::memset(h->stage[slot], 0, WMD_MAX_VR * 8);
+  for (int32_t i = 0; i < v_r; ++i) { ssel[i] = h->h_sel[i]; sr[i] = h->h_r[i]; }
+  CK(h, cudaMemcpyAsync(h->sel.p, ssel, WMD_MAX_VR * 4, cudaMemcpyHostToDevice, st));
+  CK(h, cudaMemcpyAsync(h->rpad.p, sr, WMD_MAX_VR * 4, cudaMemcpyHostToDevice, st));
+  CK(h, cudaEventRecord(h->stage_ev[slot], st));
+  CK(h, cudaMemsetAsync(h->flags.p, 0, N, st));
+  CK(h, cudaMemsetAsync(h->counters.p, 0, sizeof(int32_t), st));  // flagged-list length
+
+  const bool dev_out = is_device_ptr(out_dist);
+  float* dist = dev_out ? out_dist : h->dist_tmp.p;
+
+  PhaseEvents* pe = nullptr;
+  if (h->opt_timing) {
+    PhaseEvents e{};
+    for (auto& x : e.ev) CK(h, cudaEventCreate(&x));
+    h->events.push_back(e);
+    pe = &h->events.back();
+    CK(h, cudaEventRecord(pe->ev[0], st));
+  }
+  int64_t launches = 0;
+  // a2: M, K~
+  wmd::launch_build_ktilde(h->E.p, h->V, h->d, h->sel.p, v_r, ld, lambda, h->Kt.p, h->Mt.p,
+                           h->colmin.p, st);
+  ++launches;
+  if (pe) CK(h, cudaEventRecord(pe->ev[1], st));
+
+  const bool fused = (h->opt_path == WMD_PATH_FUSED || h->opt_path == WMD_PATH_AUTO) &&
+                     wmd::fused_supported(ld, h->max_doc_nnz);
+  if (h->opt_path == WMD_PATH_FUSED && !fused)
+    return fail(h, WMD_ERR_INVALID_ARGUMENT, "fused path does not support ld=%d, max doc nnz=%lld", ld,
+                (long long)h->max_doc_nnz);
+  if (fused) {
+    wmd::launch_sinkhorn_fused(h->doc_ptr.p, h->ent.p, N, h->Kt.p, h->Mt.p, ld, v_r, h->rpad.p, iters,
+                               dist, h->flags.p, h->flagged.p, h->counters.p, h->max_doc_nnz, st);
+    ++launches;
+    h->st.iter_launches += 1;
+    if (pe) { CK(h, cudaEventRecord(pe->ev[2], st)); CK(h, cudaEventRecord(pe->ev[3], st)); }
+    h->u_valid = false;
+    h->path_used = WMD_PATH_FUSED;
+  } else {
+    // a4: iters fused SDDMM_SpMM launches, u ping-pong
+    const float* u_in = nullptr;
+    float* bufs[2] = {h->ua.p, h->ub.p};
+    for (int32_t t = 0; t < iters; ++t) {
+      float* u_out = bufs[t & 1];
+      wmd::launch_sddmm_spmm_iter(h->doc_ptr.p, h->ent.p, N, h->Kt.p, ld, v_r, h->rpad.p, u_in, u_out,
+                                  h->flags.p, st);
+      u_in = u_out;
+    }
+    launches += iters;
+    h->st.iter_launches += iters;
+    if (pe) CK(h, cudaEventRecord(pe->ev[2], st));
+    // a5
+    wmd::launch_final_wmd(h->doc_ptr.p, h->ent.p, N, h->Kt.p, h->Mt.p, ld, v_r, h->rpad.p, u_in, dist,
+                          h->flags.p, h->flagged.p, h->counters.p, st);
+    ++launches;
+    if (pe) CK(h, cudaEventRecord(pe->ev[3], st));
+    h->u_valid = u_in != nullptr;
+    h->u_last = u_in;
+    h->path_used = WMD_PATH_PER_ITER;
+  }
+  // a6: FP64 re-run of flagged documents (device-side list; zero-cost when empty)
+  if (h->opt_fallback) {
+    wmd::launch_fallback_fp64(h->Mt.p, h->colmin.p, ld, h->rpad.p, v_r, (double)lambda, iters, h->doc_ptr.p,
+                              h->ent.p, h->flagged.p, h->counters.p, h->fb_scratch.p, h->max_doc_nnz, dist,
+                              h->flags.p, h->counters.p + 1, h->counters.p + 2, st);
+    ++launches;
+  }
+  if (pe) CK(h, cudaEventRecord(pe->ev[4], st));
+  CK(h, cudaGetLastError());
+  h->v_r = v_r;
+  h->ld = ld;
+  h->st.queries += 1;
+  h->st.kernel_launches += launches;
+  h->st.last_v_r = v_r;
+  h->st.last_ld = ld;
+  h->st.last_path = h->path_used;
+  if (!dev_out) {
+    CK(h, cudaMemcpyAsync(out_dist, dist, N * sizeof(float), cudaMemcpyDeviceToHost, st));
+    CK(h, cudaStreamSynchronize(st));
+  }
+  return WMD_OK;
+}
+
+wmd_status wmd_sync(wmd_handle* h) {
+  if (!h) return WMD_ERR_INVALID_ARGUMENT;
+  DeviceGuard g(h->device);
+  CK(h, cudaStreamSynchronize(h->stream));
+  if (!h->has_targets || h->st.queries == 0) return WMD_OK;
+  int32_t c[3] = {0, 0, 0};
+  CK(h, cudaMemcpy(c, h->counters.p, sizeof c, cudaMemcpyDeviceToHost));
+  // c[0]: flagged documents of the last query; c[1] breakdown latch and c[2] FP64 re-runs
+  // accumulate on the device until this sync.
+  h->st.flagged_docs = c[0];
+  h->st.fallback_docs += c[2];
+  int32_t z[2] = {0, 0};
+  CK(h, cudaMemcpy(h->counters.p + 1, z, sizeof z, cudaMemcpyHostToDevice));
+  if (c[1]) return fail(h, WMD_ERR_NUMERICAL_BREAKDOWN, "a distance stayed non-finite after the FP64 re-run");
+  return WMD_OK;
+}
+
+wmd_status wmd_get_stats(wmd_handle* h, wmd_stats* out) {
+  if (!h || !out) return WMD_ERR_INVALID_ARGUMENT;
+  DeviceGuard g(h->device);
+  wmd_stats s = h->st;
+  s.build_ms = s.iter_ms = s.final_ms = s.fallback_ms = s.query_ms = 0.0;
+  s.timing_valid = 0;
+  if (!h->events.empty()) {
+    CK(h, cudaEventSynchronize(h->events.back().ev[4]));
+    for (auto& pe : h->events) {
+      float t[4], all;
+      for (int q = 0; q < 4; ++q) CK(h, cudaEventElapsedTime(&t[q], pe.ev[q], pe.ev[q + 1]));
+      CK(h, cudaEventElapsedTime(&all, pe.ev[0], pe.ev[4]));
+      s.build_ms += t[0]; s.iter_ms += t[1]; s.final_ms += t[2]; s.fallback_ms += t[3]; s.query_ms += all;
+    }
+    s.timing_valid = 1;
+  }
+  *out = s;
+  return WMD_OK;
+}
+
+wmd_status wmd_reset_stats(wmd_handle* h) {
+  if (!h) return WMD_ERR_INVALID_ARGUMENT;
+  DeviceGuard g(h->device);
+  cudaStreamSynchronize(h->stream);
+  for (auto& pe : h->events)
+    for (auto& e : pe.ev) cudaEventDestroy(e);
+  h->events.clear();
+  h->st = wmd_stats{};
+  return WMD_OK;
+}
+
+wmd_status wmd_get_query_rows(wmd_handle* h, int32_t* sel, float* r) {
+  if (!h || !sel || !r) return WMD_ERR_INVALID_ARGUMENT;
+  if (h->st.queries == 0) return fail(h, WMD_ERR_STATE, "no query yet");
+  DeviceGuard g(h->device);
+  CK(h, cudaStreamSynchronize(h->stream));
+  CK(h, cudaMemcpy(sel, h->sel.p, h->v_r * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  CK(h, cudaMemcpy(r, h->rpad.p, h->v_r * sizeof(float), cudaMemcpyDeviceToHost));
+  return WMD_OK;
+}
+
+wmd_status wmd_read_kernel(wmd_handle* h, int64_t k0, int64_t count, float* ktilde, float* m,
+                           float* colmin) {
+  if (!h || k0 < 0 || count < 0 || k0 + count > h->V) return WMD_ERR_INVALID_ARGUMENT;
+  if (h->st.queries == 0) return fail(h, WMD_ERR_STATE, "no query yet");
+  DeviceGuard g(h->device);
+  CK(h, cudaStreamSynchronize(h->stream));
+  const size_t row = (size_t)h->ld;
+  if (ktilde) CK(h, cudaMemcpy(ktilde, h->Kt.p + k0 * row, count * row * 4, cudaMemcpyDeviceToHost));
+  if (m) CK(h, cudaMemcpy(m, h->Mt.p + k0 * row, count * row * 4, cudaMemcpyDeviceToHost));
+  if (colmin) CK(h, cudaMemcpy(colmin, h->colmin.p + k0, count * 4, cudaMemcpyDeviceToHost));
+  return WMD_OK;
+}
+
+wmd_status wmd_read_scaling(wmd_handle* h, int64_t j0, int64_t count, float* u) {
+  if (!h || !u || j0 < 0 || count < 0 || j0 + count > h->N) return WMD_ERR_INVALID_ARGUMENT;
+  if (!h->u_valid) return fail(h, WMD_ERR_STATE, "no per-iteration u available (fused path or iters == 0)");
+  DeviceGuard g(h->device);
+  CK(h, cudaStreamSynchronize(h->stream));
+  CK(h, cudaMemcpy(u, h->u_last + j0 * h->ld, count * h->ld * 4, cudaMemcpyDeviceToHost));
+  return WMD_OK;
+}
+
+wmd_status wmd_read_flags(wmd_handle* h, uint8_t* flags) {
+  if (!h || !flags) return WMD_ERR_INVALID_ARGUMENT;
+  if (!h->has_targets) return fail(h, WMD_ERR_STATE, "no targets");
+  DeviceGuard g(h->device);
+  CK(h, cudaStreamSynchronize(h->stream));
+  CK(h, cudaMemcpy(flags, h->flags.p, h->N, cudaMemcpyDeviceToHost));
+  return WMD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,69 @@
+// Internal interface between the host runtime (wmd_host.cpp) and the CUDA kernels
+// (wmd_kernels.cu). Not installed; not part of the C ABI (include/wmd.h is).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "wmd.h"
+
+#define WMD_MAX_VR_DEV WMD_MAX_VR
+
+namespace wmd {
+
+// One CSC nonzero of the target matrix c: vocabulary word k and weight c_kj, packed so a
+// lane fetches both with one 8-byte load (D1 in SURVEY.md §2.4).
+struct Entry {
+  int32_t k;
+  float c;
+};
+
+// Flag bits per document.
+constexpr uint8_t kFlagFp32Range = 1;  // an FP32 iterate left the normal range
+constexpr uint8_t kFlagFp64 = 2;       // recomputed in FP64
+
+// Device-side per-query scalars the kernels read (written by one H2D copy per query).
+struct QueryDev {
+  int32_t v_r;
+  int32_t ld;          // row stride of K~ / M / u (floats), v_r rounded up to 8
+  float lambda;
+  int32_t iters;
+};
+
+// --- a2: distance + column-rescaled kernel build -------
+void launch_build_ktilde(const float* E, int64_t V, int d, const int32_t* sel, int v_r, int ld,
+                         float lambda, float* Kt, float* Mt, float* colmin, cudaStream_t st);
+
+// --- a4: one fused SDDMM_SpMM iteration for all documents ------------
+// u_in == nullptr: first iteration with the constant u0 = 1/x0 = v_r.
+void launch_sddmm_spmm_iter(const int32_t* doc_ptr, const Entry* ent, int64_t N, const float* Kt,
+                            int ld, int v_r, const float* rpad, const float* u_in, float* u_out,
+                            uint8_t* flags, cudaStream_t st);
+
+// --- a5: final u/v/WMD step -----------------------------------
+void launch_final_wmd(const int32_t* doc_ptr, const Entry* ent, int64_t N, const float* Kt,
+                      const float* Mt, int ld, int v_r, const float* rpad, const float* u_in,
+                      float* dist, uint8_t* flags, int32_t* flagged_list, int32_t* flagged_count,
+                      cudaStream_t st);
+
+// --- NEXT-1: all iterations + final step in one launch ------------------------------------
+// Returns false if the shape is not supported by the fused kernel (caller uses the
+// per-iteration path).
+bool fused_supported(int ld, int64_t max_doc_nnz);
+void launch_sinkhorn_fused(const int32_t* doc_ptr, const Entry* ent, int64_t N, const float* Kt,
+                           const float* Mt, int ld, int v_r, const float* rpad, int iters,
+                           float* dist, uint8_t* flags, int32_t* flagged_list,
+                           int32_t* flagged_count, int64_t max_doc_nnz, cudaStream_t st);
+
+// --- a6: FP64 re-run of flagged documents (no CPU fallback) --------------------------------
+constexpr int kFallbackBlocks = 296;  // 2 per SM
+size_t fallback_scratch_bytes(int64_t max_doc_nnz);
+void launch_fallback_fp64(const float* Mt, const float* colmin, int ld, const float* rpad, int v_r,
+                          double lambda, int iters, const int32_t* doc_ptr, const Entry* ent,
+                          const int32_t* flagged_list, const int32_t* flagged_count,
+                          double* scratch, int64_t max_doc_nnz, float* dist, uint8_t* flags,
+                          int32_t* breakdown, int32_t* fallback_count, cudaStream_t st);
+
+// --- validation helpers (device-resident inputs) -------------------------------------------
+void launch_check_finite(const float* x, int64_t n, int32_t* bad, cudaStream_t st);
+
+}  // namespace wmd

@@ -1,0 +1,101 @@
+"""Multi-GPU driver: target documents (columns of c) sharded across ranks, one process per GPU.
+
+Documents are independent for the whole solve (Algorithm 1 touches column j only through
+c[:,j], x[:,j], u[:,j]), so each rank runs the full hot path on its own
+nnz-balanced contiguous document range (the paper's binary-search nnz split, PAPER.md:158,
+snapped to document boundaries: wmd_partition) with no inter-GPU traffic inside the loop.
+The one exchange step is the output: a padded all_gather_into_tensor of the FP32 distances
+(NCCL over NVLink/NVSwitch), then a bit-exact compaction by the shard bounds.
+
+The embeddings and the per-query K~ table are replicated (each rank builds its own K~: no
+traffic). Per-document arithmetic does not depend on shard membership, so the distances are
+bitwise identical for every world size.
+"""
+from __future__ import annotations
+
+from typing import Optional, Tuple
+
+import numpy as np
+
+from . import wmd
+
+
+def shard_bounds(col_ptr, world: int) -> np.ndarray:
+    return wmd.wmd_partition(col_ptr, world)
+
+
+def local_shard(col_ptr, row_idx, val, bounds, rank: int) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
+    """Rebased CSC of documents [bounds[rank], bounds[rank+1]) (integer bookkeeping only)."""
+    b0, b1 = int(bounds[rank]), int(bounds[rank + 1])
+    e0, e1 = int(col_ptr[b0]), int(col_ptr[b1])
+    cp = np.asarray(col_ptr[b0:b1 + 1], dtype=np.int64) - e0
+    return cp, np.ascontiguousarray(row_idx[e0:e1]), np.ascontiguousarray(val[e0:e1])
+
+
+def gather_distances(local, bounds, group=None, out=None):
+    """All-gather the ranks' local distance vectors (lengths bounds[g+1]-bounds[g]) into the
+    global order. `local` is a 1-D float32 tensor on this rank's device (CUDA for NCCL, CPU for
+    gloo). Pads every shard to N_max = max shard length, one all_gather_into_tensor, then
+    compacts: out[bounds[g] + i] = buf[g * N_max + i]."""
+    import torch
+    import torch.distributed as dist
+
+    world = len(bounds) - 1
+    lens = np.diff(np.asarray(bounds, np.int64))
+    n_max = int(max(1, lens.max()))
+    send = torch.zeros(n_max, dtype=local.dtype, device=local.device)
+    send[: local.shape[0]] = local
+    buf = torch.empty(world * n_max, dtype=local.dtype, device=local.device)
+    dist.all_gather_into_tensor(buf, send, group=group)
+    N = int(bounds[-1])
+    if out is None:
+        out = torch.empty(N, dtype=local.dtype, device=local.device)
+    if world > 0:
+        idx = _compaction_index(tuple(int(b) for b in bounds), n_max, str(local.device))
+        torch.index_select(buf, 0, idx, out=out)
+    return out
+
+
+_IDX_CACHE = {}
+
+
+def _compaction_index(bounds, n_max, device):
+    key = (bounds, n_max, device)
+    if key not in _IDX_CACHE:
+        import torch
+        b = np.asarray(bounds, np.int64)
+        idx = np.concatenate([g * n_max + np.arange(b[g + 1] - b[g]) for g in range(len(b) - 1)])
+        _IDX_CACHE[key] = torch.from_numpy(idx.astype(np.int64)).to(device)
+    return _IDX_CACHE[key]
+
+
+class ShardedEngine:
+    """One rank's view: owns a wmd handle over its document shard."""
+
+    def __init__(self, vocab_emb, col_ptr, row_idx, val, rank: int, world: int, device: int,
+                 group=None, path: int = wmd.WMD_PATH_AUTO, timing: bool = False):
+        self.rank, self.world, self.group = rank, world, group
+        self.bounds = shard_bounds(col_ptr, world)
+        self.N = int(np.shape(col_ptr)[0]) - 1
+        cp, ri, va = local_shard(col_ptr, row_idx, val, self.bounds, rank)
+        self.n_local = cp.shape[0] - 1
+        self.nnz_local = int(cp[-1])
+        self.engine: Optional[wmd.Engine] = None
+        self.engine = wmd.Engine(vocab_emb, device=device, path=path, timing=timing)
+        if self.n_local > 0:
+            self.engine.set_targets(cp, ri, va)
+        import torch
+        self._local = torch.zeros(max(self.n_local, 1), dtype=torch.float32, device=f"cuda:{device}")
+        self._out = torch.empty(self.N, dtype=torch.float32, device=f"cuda:{device}")
+
+    def query(self, ids, weights, lam: float, iters: int):
+        """Distances of all N documents (global order) on every rank."""
+        if self.n_local > 0:
+            self.engine.query(ids, weights, lam, iters, out=self._local[: self.n_local])
+        if self.world == 1:
+            return self._local[: self.n_local]
+        return gather_distances(self._local[: self.n_local], self.bounds, self.group, out=self._out)
+
+    def close(self):
+        if self.engine is not None:
+            self.engine.close()

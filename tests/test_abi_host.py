@@ -1,0 +1,125 @@
+"""CPU-side tests of the C ABI (no GPU needed): the library loads and exports every symbol
+include/wmd.h declares; the pure-host entry points (partition, validation, status strings)
+are bit-exact and return the documented error codes."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def W():
+    from paper_2005_06727_b200 import build
+    build.build()
+    from paper_2005_06727_b200 import wmd
+    return wmd
+
+
+def header_symbols():
+    txt = open(os.path.join(ROOT, "include", "wmd.h")).read()
+    return sorted(set(re.findall(r"WMD_API\s+[\w\s\*]+?\b(wmd_\w+)\s*\(", txt)))
+
+
+def test_header_declares_the_north_star_entry_points():
+    syms = header_symbols()
+    for s in ("wmd_create", "wmd_set_targets", "wmd_query", "wmd_destroy", "wmd_partition"):
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol(W):
+    lib = ctypes.CDLL(W.LIB_PATH)
+    missing = [s for s in header_symbols() if not hasattr(lib, s)]
+    assert not missing, missing
+    assert set(header_symbols()) == set(W.EXPORTED)
+
+
+def test_status_strings(W):
+    assert W.wmd_status_string(W.WMD_OK) == "ok"
+    for s in range(1, 11):
+        assert W.wmd_status_string(s) not in ("", "unknown status")
+    assert W.wmd_status_string(99) == "unknown status"
+    assert "sm_100a" in W.wmd_version()
+
+
+def test_partition_golden_and_oracle_equivalence(W, golden):
+    for ex in golden["partition"]:
+        assert W.wmd_partition(np.array(ex["col_ptr"]), ex["P"]).tolist() == ex["bounds"], ex["cite"]
+    rng = np.random.default_rng(3)
+    for _ in range(500):
+        N = int(rng.integers(0, 80))
+        lens = rng.integers(1, 30, size=N)
+        cp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+        P = int(rng.integers(1, 17))
+        assert np.array_equal(W.wmd_partition(cp, P), oracle.partition(cp, P))
+
+
+def test_partition_real_config_bit_exact(W):
+    w = synth.make_workload("tweet", n_queries=0)
+    for P in (1, 2, 3, 4, 8):
+        assert np.array_equal(W.wmd_partition(w.col_ptr, P), oracle.partition(w.col_ptr, P))
+
+
+def test_partition_rejects_bad_args(W):
+    with pytest.raises(W.WmdError):
+        W.wmd_partition(np.array([0, 1]), 0)
+
+
+def _csc(docs, V=10):
+    return synth.csc_from_lists(docs, V)
+
+
+def test_validate_csc_codes(W):
+    V = 10
+    ok = _csc([{1: 0.5, 3: 0.5}, {2: 1.0}])
+    assert W.wmd_validate_csc(*ok, V) == (W.WMD_OK, -1)
+    cp, ri, va = ok
+    # out of range id
+    assert W.wmd_validate_csc(cp, np.array([1, 10, 2], np.int32), va, V)[0] == W.WMD_ERR_INDEX_OUT_OF_RANGE
+    # rows not strictly increasing
+    assert W.wmd_validate_csc(cp, np.array([3, 1, 2], np.int32), va, V) == (W.WMD_ERR_MALFORMED_CSC, 0)
+    assert W.wmd_validate_csc(cp, np.array([3, 3, 2], np.int32), va, V) == (W.WMD_ERR_MALFORMED_CSC, 0)
+    # empty document (SPEC.md:58 EmptyDocument)
+    assert W.wmd_validate_csc(np.array([0, 2, 2, 3]), np.array([1, 3, 2], np.int32),
+                              np.array([.5, .5, 1], np.float32), V) == (W.WMD_ERR_EMPTY_DOCUMENT, 1)
+    # col_ptr[0] != 0 / decreasing
+    assert W.wmd_validate_csc(np.array([1, 2, 3]), ri, va, V)[0] == W.WMD_ERR_MALFORMED_CSC
+    assert W.wmd_validate_csc(np.array([0, 3, 2, 3]), np.array([1, 2, 3], np.int32),
+                              np.array([.2, .3, .5], np.float32), V)[0] == W.WMD_ERR_MALFORMED_CSC
+    # weights: non-positive, NaN, not normalised
+    assert W.wmd_validate_csc(cp, ri, np.array([1.0, 0.0, 1.0], np.float32), V) == (W.WMD_ERR_BAD_WEIGHTS, 0)
+    assert W.wmd_validate_csc(cp, ri, np.array([0.5, np.nan, 1.0], np.float32), V)[0] == W.WMD_ERR_BAD_WEIGHTS
+    assert W.wmd_validate_csc(cp, ri, np.array([0.5, 0.5, 0.9], np.float32), V) == (W.WMD_ERR_BAD_WEIGHTS, 1)
+    # the generator's FP32-rounded weights pass the 1e-5 FP64 normalisation check
+    w = synth.make_workload("tiny", n_queries=0)
+    assert W.wmd_validate_csc(w.col_ptr, w.row_idx, w.val, w.cfg.V)[0] == W.WMD_OK
+
+
+def test_validate_query_codes(W):
+    V = 10
+    assert W.wmd_validate_query([3, 1], [0.5, 0.5], V)[0] == W.WMD_OK
+    assert W.wmd_validate_query([3, 3], [0.5, 0.5], V)[0] == W.WMD_ERR_BAD_WEIGHTS     # duplicate id
+    assert W.wmd_validate_query([3, 10], [0.5, 0.5], V) == (W.WMD_ERR_INDEX_OUT_OF_RANGE, 1)
+    assert W.wmd_validate_query([3, -1], [0.5, 0.5], V)[0] == W.WMD_ERR_INDEX_OUT_OF_RANGE
+    assert W.wmd_validate_query([3, 1], [0.5, 0.4], V)[0] == W.WMD_ERR_BAD_WEIGHTS      # sum != 1
+    assert W.wmd_validate_query([3, 1], [1.0, 0.0], V)[0] == W.WMD_ERR_BAD_WEIGHTS      # zero weight
+    ids = np.arange(129, dtype=np.int32)
+    assert W.wmd_validate_query(ids, np.full(129, 1 / 129, np.float32), 200)[0] == W.WMD_ERR_INVALID_ARGUMENT
+    ids = np.arange(128, dtype=np.int32)
+    assert W.wmd_validate_query(ids, np.full(128, 1 / 128, np.float32), 200)[0] == W.WMD_OK
+
+
+def test_create_rejects_bad_arguments_before_touching_cuda(W):
+    E = np.zeros((4, 3), np.float32)
+    with pytest.raises(W.WmdError) as e:
+        W.wmd_create(E, 0, 3, 0)
+    assert e.value.status == W.WMD_ERR_INVALID_ARGUMENT
+    with pytest.raises(W.WmdError) as e:
+        W.wmd_create(E, 4, 0, 0)
+    assert e.value.status == W.WMD_ERR_INVALID_ARGUMENT

@@ -1,0 +1,422 @@
+"""GPU parity: the CUDA path (through the C ABI) against the FP64 oracle on the same seeded
+inputs. Distances: |gpu - oracle| <= 1e-4 |oracle| + 1e-5 (north_star 1e-4 relative, with the
+absolute floor of DESIGN.md R22 for near-zero distances). Bookkeeping (query compaction,
+partition, shard concatenation, determinism): bit-exact."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+RTOL, ATOL = 1e-4, 1e-5
+
+
+@pytest.fixture(scope="module")
+def W():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    from paper_2005_06727_b200 import build
+    build.build()
+    from paper_2005_06727_b200 import wmd
+    return wmd
+
+
+def run_gpu(W, E, cp, ri, va, q, w, lam, iters, path=1, fallback=True, out="host", handle=None):
+    h = handle or W.wmd_create(E, device=0)
+    try:
+        W.wmd_set_option(h, W.WMD_OPT_PATH, path)
+        W.wmd_set_option(h, W.WMD_OPT_FALLBACK, int(fallback))
+        W.wmd_set_targets(h, cp, ri, va)
+        N = cp.shape[0] - 1
+        if out == "host":
+            d = np.empty(N, np.float32)
+            W.wmd_query(h, q, w, lam, iters, d)
+        else:
+            import torch
+            t = torch.empty(N, dtype=torch.float32, device="cuda:0")
+            W.wmd_set_stream(h, torch.cuda.current_stream())
+            W.wmd_query(h, q, w, lam, iters, t)
+            torch.cuda.synchronize()
+            d = t.cpu().numpy()
+        W.wmd_sync(h)
+        return d
+    finally:
+        if handle is None:
+            W.wmd_destroy(h)
+
+
+def assert_parity(g, o, what=""):
+    g = np.asarray(g, np.float64)
+    err = np.abs(g - o)
+    bound = RTOL * np.abs(o) + ATOL
+    bad = np.nonzero(~(err <= bound))[0]
+    assert bad.size == 0, (f"{what}: {bad.size} docs out of tolerance; first {bad[:5]} "
+                           f"gpu={g[bad[:5]]} oracle={o[bad[:5]]}")
+
+
+PATHS = [1]  # per-iteration SDDMM_SpMM path; the fused path is added in test_fused_gpu.py
+
+
+# ------------------------------------------------------------------ full configs, small
+
+@pytest.mark.parametrize("path", PATHS)
+def test_tiny_full(W, path):
+    wl = synth.make_workload("tiny")
+    q, w = wl.queries[0]
+    cfg = wl.cfg
+    o = oracle.sinkhorn_wmd(wl.E, wl.col_ptr, wl.row_idx, wl.val, q, w, cfg.lam, cfg.iters, dense=True)
+    g = run_gpu(W, wl.E, wl.col_ptr, wl.row_idx, wl.val, q, w, cfg.lam, cfg.iters, path=path)
+    assert_parity(g, o, "tiny")
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_tweet_full(W, path):
+    wl = synth.make_workload("tweet")
+    q, w = wl.queries[0]
+    cfg = wl.cfg
+    o = oracle.sinkhorn_wmd(wl.E, wl.col_ptr, wl.row_idx, wl.val, q, w, cfg.lam, cfg.iters)
+    g = run_gpu(W, wl.E, wl.col_ptr, wl.row_idx, wl.val, q, w, cfg.lam, cfg.iters, path=path)
+    assert_parity(g, o, "tweet")
+
+
+# ------------------------------------------------------------------ full-size configs, sampled docs
+
+def _sampled_parity(W, name, n_sample, path, qi=0):
+    wl = synth.make_workload(name, n_queries=qi + 1)
+    q, w = wl.queries[qi]
+    cfg = wl.cfg
+    g = run_gpu(W, wl.E, wl.col_ptr, wl.row_idx, wl.val, q, w, cfg.lam, cfg.iters, path=path)
+    rng = np.random.default_rng(123)
+    docs = np.sort(rng.choice(wl.N, size=n_sample, replace=False))
+    docs = np.unique(np.concatenate([docs, [0, wl.N - 1]]))
+    cp, ri, va = synth.subset_docs(wl.col_ptr, wl.row_idx, wl.val, docs)
+    o = oracle.sinkhorn_wmd(wl.E, cp, ri, va, q, w, cfg.lam, cfg.iters)
+    assert_parity(g[docs], o, name)
+    assert np.all(np.isfinite(g))
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_long_sampled(W, path):
+    _sampled_parity(W, "long", 300, path)
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_scaling_sampled(W, path):
+    _sampled_parity(W, "scaling", 1000, path)
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("qi", [0, 7])
+def test_many_sampled(W, path, qi):
+    _sampled_parity(W, "many", 500, path, qi=qi)
+
+
+# ------------------------------------------------------------------ step a1 / a2 / a4 parity
+
+def test_query_compaction_bit_exact(W):
+    wl = synth.make_workload("tiny")
+    rng = np.random.default_rng(5)
+    q, w = wl.queries[0]
+    perm = rng.permutation(q.shape[0])
+    h = W.wmd_create(wl.E)
+    try:
+        W.wmd_set_targets(h, wl.col_ptr, wl.row_idx, wl.val)
+        d = np.empty(wl.N, np.float32)
+        W.wmd_query(h, q[perm], w[perm], 10.0, 3, d)
+        sel, r = W.wmd_get_query_rows(h, q.shape[0])
+        osel, orr = oracle.select_nonzero(wl.cfg.V, q[perm], w[perm])
+        assert np.array_equal(sel, osel)
+        assert np.array_equal(r.astype(np.float64), orr)
+        # the same query in the original order gives bit-identical distances
+        d2 = np.empty(wl.N, np.float32)
+        W.wmd_query(h, q, w, 10.0, 3, d2)
+        assert np.array_equal(d, d2)
+    finally:
+        W.wmd_destroy(h)
+
+
+@pytest.mark.parametrize("name", ["tiny", "tweet"])
+def test_kernel_build_parity(W, name):
+    """a2: M and K~ = exp(-lambda (M - min_i M)) against the FP64 oracle's M."""
+    wl = synth.make_workload(name)
+    q, w = wl.queries[0]
+    lam = wl.cfg.lam
+    h = W.wmd_create(wl.E)
+    try:
+        W.wmd_set_targets(h, wl.col_ptr, wl.row_idx, wl.val)
+        d = np.empty(wl.N, np.float32)
+        W.wmd_query(h, q, w, lam, 1, d)
+        st = W.wmd_get_stats(h)
+        ld = st["last_ld"]
+        V = wl.cfg.V
+        ks = np.arange(0, V, max(1, V // 4000))
+        kt, km, cm = W.wmd_read_kernel(h, 0, V, ld)
+    finally:
+        W.wmd_destroy(h)
+    sel, r = oracle.select_nonzero(V, q, w)
+    v_r = sel.shape[0]
+    assert ld == (v_r + 7) // 8 * 8
+    assert np.all(kt[:, v_r:] == 0) and np.all(km[:, v_r:] == 0)
+    M = oracle.euclidean_rows(wl.E, sel)                    # (v_r, V) FP64
+    m = M.min(axis=0)
+    np.testing.assert_allclose(cm[ks], m[ks], rtol=2e-6, atol=1e-6)
+    ref = np.exp(-lam * (M - m[None, :])).T                 # (V, v_r)
+    # exact ones where the query word itself is the column minimum (M = 0)
+    assert np.all(kt[sel, np.arange(v_r)] == 1.0)
+    lk = np.log(np.maximum(kt[ks, :v_r].astype(np.float64), 1e-300))
+    lr = np.log(ref[ks])
+    mask = ref[ks] > 1e-30
+    # |d ln K~| <= lambda * |dM| + argument rounding: M has FP32 relative error ~1e-6
+    assert np.abs(lk - lr)[mask].max() < 1e-3
+    # M itself (FP32 direct difference): relative error ~1e-6; exact zero self-distance
+    np.testing.assert_allclose(km[ks, :v_r], M.T[ks], rtol=5e-6, atol=1e-5)
+    assert np.all(km[sel, np.arange(v_r)] == 0.0)
+
+
+def test_scaling_vector_parity_per_iteration_path(W):
+    """a4: after t iterations u matches the oracle's 1/x up to the per-document gauge."""
+    wl = synth.make_workload("tiny")
+    q, w = wl.queries[0]
+    for iters in (1, 2, 15):
+        h = W.wmd_create(wl.E)
+        try:
+            W.wmd_set_option(h, W.WMD_OPT_PATH, W.WMD_PATH_PER_ITER)
+            W.wmd_set_targets(h, wl.col_ptr, wl.row_idx, wl.val)
+            d = np.empty(wl.N, np.float32)
+            W.wmd_query(h, q, w, wl.cfg.lam, iters, d)
+            ld = W.wmd_get_stats(h)["last_ld"]
+            u = W.wmd_read_scaling(h, 0, wl.N, ld)[:, : q.shape[0]].astype(np.float64)
+        finally:
+            W.wmd_destroy(h)
+        _, st = oracle.sinkhorn_wmd(wl.E, wl.col_ptr, wl.row_idx, wl.val, q, w, wl.cfg.lam, iters,
+                                    return_state=True)
+        uo = st["u"]
+        # gauge-invariant comparison: normalise each document by its largest entry
+        ug = u / u.max(axis=1, keepdims=True)
+        un = uo / uo.max(axis=1, keepdims=True)
+        mask = un > 1e-20
+        rel = np.abs(ug - un)[mask] / un[mask]
+        assert rel.max() < 2e-3, (iters, rel.max())
+        # the gauge is a power of two: max u of each document lies in [2^-64, 2^64]
+        assert np.all(np.abs(np.log2(u.max(axis=1))) < 64)
+
+
+# ------------------------------------------------------------------ edge cases
+
+@pytest.mark.parametrize("path", PATHS)
+def test_single_query_word_closed_form(W, path):
+    """v_r = 1 (forced transport): WMD_j = sum_k c_kj M_0k."""
+    wl = synth.make_workload("tiny")
+    q = np.array([5], np.int32)
+    g = run_gpu(W, wl.E, wl.col_ptr, wl.row_idx, wl.val, q, [1.0], 10.0, 15, path=path)
+    o = oracle.sinkhorn_wmd(wl.E, wl.col_ptr, wl.row_idx, wl.val, q, [1.0], 10.0, 15)
+    assert_parity(g, o, "v_r=1")
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_single_word_docs_and_query_equals_doc(W, path):
+    wl = synth.make_workload("tiny")
+    V = wl.cfg.V
+    # single-word docs + the query's own histogram as a doc (distance ~ 0)
+    q, w = wl.queries[0]
+    docs = [{int(k): 1.0} for k in (0, 3, 77, V - 1)]
+    docs.append({int(k): float(x) for k, x in zip(q, w)})
+    cp, ri, va = synth.csc_from_lists(docs, V)
+    for lam, iters in ((0.5, 15), (10.0, 15), (10.0, 1)):
+        g = run_gpu(W, wl.E, cp, ri, va, q, w, lam, iters, path=path)
+        o = oracle.sinkhorn_wmd(wl.E, cp, ri, va, q, w, lam, iters)
+        assert_parity(g, o, f"lam={lam} iters={iters}")
+    assert abs(g[-1]) < 1e-3
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("v_r", [1, 2, 7, 8, 9, 16, 17, 31, 32, 33, 64, 65, 100, 128])
+def test_query_width_boundaries(W, path, v_r):
+    """Every K~ row-width class (ld = v_r rounded up to 8; 2..32 lanes per row), incl. the max."""
+    wl = synth.make_workload("tiny")
+    rng = np.random.default_rng(v_r)
+    q = np.sort(rng.choice(wl.cfg.V, v_r, replace=False)).astype(np.int32)
+    cnt = rng.geometric(0.5, v_r).astype(np.float64)
+    w = (cnt / cnt.sum()).astype(np.float32)
+    cp, ri, va = synth.subset_docs(wl.col_ptr, wl.row_idx, wl.val, np.arange(37))  # ragged: 37 docs
+    g = run_gpu(W, wl.E, cp, ri, va, q, w, 10.0, 15, path=path)
+    o = oracle.sinkhorn_wmd(wl.E, cp, ri, va, q, w, 10.0, 15)
+    assert_parity(g, o, f"v_r={v_r}")
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("iters", [0, 1, 2, 40, 100])
+def test_iteration_counts(W, path, iters):
+    wl = synth.make_workload("tiny")
+    q, w = wl.queries[0]
+    g = run_gpu(W, wl.E, wl.col_ptr, wl.row_idx, wl.val, q, w, 10.0, iters, path=path)
+    o = oracle.sinkhorn_wmd(wl.E, wl.col_ptr, wl.row_idx, wl.val, q, w, 10.0, iters)
+    assert_parity(g, o, f"iters={iters}")
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_single_document_and_long_document(W, path):
+    """N = 1, and a 1000-word document (many 32-entry chunks)."""
+    wl = synth.make_workload("tiny")
+    q, w = wl.queries[0]
+    rng = np.random.default_rng(2)
+    ids = np.sort(rng.choice(wl.cfg.V, 1000, replace=False))
+    cnt = rng.geometric(0.3, 1000).astype(np.float64)
+    docs = [{int(k): float(x) for k, x in zip(ids, (cnt / cnt.sum()).astype(np.float32))}]
+    cp, ri, va = synth.csc_from_lists(docs, wl.cfg.V)
+    g = run_gpu(W, wl.E, cp, ri, va, q, w, 10.0, 15, path=path)
+    o = oracle.sinkhorn_wmd(wl.E, cp, ri, va, q, w, 10.0, 15)
+    assert_parity(g, o, "long doc")
+
+
+def _degenerate_case():
+    """Query = doc plus one more word (query strictly contains the doc's word set). Some query
+    row of K~ restricted to the doc underflows in FP32 (SURVEY Finding 4), so the FP32 path must
+    flag the doc and the FP64 GPU re-run must produce the oracle's value."""
+    wl = synth.make_workload("tweet", n_queries=0, N=200)
+    V = wl.cfg.V
+    rng = np.random.default_rng(0)
+    docs, queries = [], []
+    for j in range(6):
+        ids = np.sort(rng.choice(np.arange(100, V), 12, replace=False))
+        cnt = rng.geometric(0.6, 12).astype(np.float64)
+        docs.append({int(k): float(x) for k, x in zip(ids, (cnt / cnt.sum()).astype(np.float32))})
+        queries.append(ids)
+    extra = int(rng.integers(100, V))
+    q_ids = np.unique(np.concatenate([queries[0], [extra]])).astype(np.int32)
+    cnt = rng.geometric(0.6, q_ids.shape[0]).astype(np.float64)
+    q_w = (cnt / cnt.sum()).astype(np.float32)
+    cp, ri, va = synth.csc_from_lists(docs, V)
+    return wl.E, cp, ri, va, q_ids, q_w
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_degenerate_doc_goes_through_fp64_fallback(W, path):
+    E, cp, ri, va, q, w = _degenerate_case()
+    o = oracle.sinkhorn_wmd(E, cp, ri, va, q, w, 10.0, 15)
+    assert np.all(np.isfinite(o))
+    h = W.wmd_create(E)
+    try:
+        W.wmd_set_option(h, W.WMD_OPT_PATH, path)
+        W.wmd_set_targets(h, cp, ri, va)
+        d = np.empty(cp.shape[0] - 1, np.float32)
+        W.wmd_set_option(h, W.WMD_OPT_FALLBACK, 0)
+        W.wmd_query(h, q, w, 10.0, 15, d)
+        W.wmd_sync(h)
+        flags = W.wmd_read_flags(h, cp.shape[0] - 1)
+        assert flags[0] & 1, "doc 0 (query superset) must be flagged in FP32"
+        W.wmd_set_option(h, W.WMD_OPT_FALLBACK, 1)
+        W.wmd_query(h, q, w, 10.0, 15, d)
+        W.wmd_sync(h)
+        flags = W.wmd_read_flags(h, cp.shape[0] - 1)
+        st = W.wmd_get_stats(h)
+    finally:
+        W.wmd_destroy(h)
+    assert flags[0] & 2
+    assert st["fallback_docs"] >= 1
+    assert_parity(d, o, "degenerate")
+
+
+# ------------------------------------------------------------------ determinism / sharding
+
+@pytest.mark.parametrize("path", PATHS)
+def test_bitwise_determinism_and_shard_invariance(W, path):
+    wl = synth.make_workload("tweet")
+    q, w = wl.queries[0]
+    cfg = wl.cfg
+    full = run_gpu(W, wl.E, wl.col_ptr, wl.row_idx, wl.val, q, w, cfg.lam, cfg.iters, path=path)
+    again = run_gpu(W, wl.E, wl.col_ptr, wl.row_idx, wl.val, q, w, cfg.lam, cfg.iters, path=path)
+    assert np.array_equal(full, again)
+    for P in (2, 3, 4, 8):
+        b = W.wmd_partition(wl.col_ptr, P)
+        assert np.array_equal(b, oracle.partition(wl.col_ptr, P))
+        parts = []
+        for g in range(P):
+            if b[g] == b[g + 1]:
+                continue
+            cp, ri, va = synth.subset_docs(wl.col_ptr, wl.row_idx, wl.val, np.arange(b[g], b[g + 1]))
+            parts.append(run_gpu(W, wl.E, cp, ri, va, q, w, cfg.lam, cfg.iters, path=path))
+        assert np.array_equal(np.concatenate(parts), full), P
+
+
+def test_device_output_equals_host_output(W):
+    wl = synth.make_workload("tiny")
+    q, w = wl.queries[0]
+    a = run_gpu(W, wl.E, wl.col_ptr, wl.row_idx, wl.val, q, w, 10.0, 15, out="host")
+    b = run_gpu(W, wl.E, wl.col_ptr, wl.row_idx, wl.val, q, w, 10.0, 15, out="device")
+    assert np.array_equal(a, b)
+
+
+def test_device_resident_inputs(W):
+    import torch
+    wl = synth.make_workload("tiny")
+    q, w = wl.queries[0]
+    Ed = torch.from_numpy(wl.E).cuda()
+    h = W.wmd_create(Ed, device=0)
+    try:
+        W.wmd_set_targets(h, torch.from_numpy(wl.col_ptr).cuda(), torch.from_numpy(wl.row_idx).cuda(),
+                          torch.from_numpy(wl.val).cuda())
+        d = np.empty(wl.N, np.float32)
+        W.wmd_query(h, q, w, 10.0, 15, d)
+    finally:
+        W.wmd_destroy(h)
+    assert np.array_equal(d, run_gpu(W, wl.E, wl.col_ptr, wl.row_idx, wl.val, q, w, 10.0, 15))
+
+
+# ------------------------------------------------------------------ ABI errors on the GPU
+
+def test_abi_errors_on_device(W):
+    wl = synth.make_workload("tiny")
+    q, w = wl.queries[0]
+    h = W.wmd_create(wl.E)
+    try:
+        d = np.empty(wl.N, np.float32)
+        with pytest.raises(W.WmdError) as e:
+            W.wmd_query(h, q, w, 10.0, 15, d)
+        assert e.value.status == W.WMD_ERR_STATE
+        bad = wl.val.copy()
+        bad[0] = -1
+        with pytest.raises(W.WmdError) as e:
+            W.wmd_set_targets(h, wl.col_ptr, wl.row_idx, bad)
+        assert e.value.status == W.WMD_ERR_BAD_WEIGHTS
+        W.wmd_set_targets(h, wl.col_ptr, wl.row_idx, wl.val)
+        for args, code in (((q, w, -1.0, 15), W.WMD_ERR_INVALID_ARGUMENT),
+                           ((q, w, 10.0, -1), W.WMD_ERR_INVALID_ARGUMENT),
+                           ((np.array([0, 0], np.int32), np.array([.5, .5], np.float32), 10.0, 3),
+                            W.WMD_ERR_BAD_WEIGHTS),
+                           ((np.array([wl.cfg.V], np.int32), np.array([1.0], np.float32), 10.0, 3),
+                            W.WMD_ERR_INDEX_OUT_OF_RANGE)):
+            with pytest.raises(W.WmdError) as e:
+                W.wmd_query(h, *args, d)
+            assert e.value.status == code
+        W.wmd_query(h, q, w, 10.0, 15, d)   # still usable after errors
+        assert np.all(np.isfinite(d))
+    finally:
+        W.wmd_destroy(h)
+    Enan = wl.E.copy()
+    Enan[3, 2] = np.nan
+    with pytest.raises(W.WmdError) as e:
+        W.wmd_create(Enan)
+    assert e.value.status == W.WMD_ERR_NONFINITE_EMBEDDING
+
+
+def test_timing_stats(W):
+    wl = synth.make_workload("tiny")
+    q, w = wl.queries[0]
+    h = W.wmd_create(wl.E)
+    try:
+        W.wmd_set_option(h, W.WMD_OPT_TIMING, 1)
+        W.wmd_set_option(h, W.WMD_OPT_PATH, W.WMD_PATH_PER_ITER)
+        W.wmd_set_targets(h, wl.col_ptr, wl.row_idx, wl.val)
+        d = np.empty(wl.N, np.float32)
+        for _ in range(3):
+            W.wmd_query(h, q, w, 10.0, 15, d)
+        st = W.wmd_get_stats(h)
+    finally:
+        W.wmd_destroy(h)
+    assert st["queries"] == 3 and st["timing_valid"] == 1
+    assert st["iter_launches"] == 45
+    assert st["build_ms"] > 0 and st["iter_ms"] > 0 and st["query_ms"] >= st["iter_ms"]
