@@ -83,6 +83,7 @@ struct wmd_handle {
   // targets
   bool has_targets = false;
   DevBuf<int32_t> doc_ptr;
+  DevBuf<int32_t> order;     // documents sorted by length (stable counting sort)
   DevBuf<Entry> ent;
   int64_t N = 0, nnz = 0, max_doc_nnz = 0;
   // per-query device state
@@ -91,6 +92,7 @@ struct wmd_handle {
   DevBuf<float> Kt, Mt;      // V * ld: K~ and M (FP32, vocab-major)
   DevBuf<float> colmin;      // V
   DevBuf<float> ua, ub;      // N * ld
+  DevBuf<uint32_t> umask;    // N * ceil(ld/32): rows with an underflowed K~ entry, per doc
   DevBuf<float> dist_tmp;    // N (host-output queries)
   DevBuf<uint8_t> flags;     // N
   DevBuf<int32_t> flagged;   // N
@@ -252,6 +254,7 @@ wmd_status validate_query(const int32_t* ids, const float* w, int32_t n, int64_t
 void drop_targets(wmd_handle* h) {
   h->has_targets = false;
   h->doc_ptr.release();
+  h->order.release();
   h->ent.release();
   h->N = h->nnz = h->max_doc_nnz = 0;
   h->u_valid = false;
@@ -366,8 +369,8 @@ void wmd_destroy(wmd_handle* h) {
     if (h->stage[s]) cudaFreeHost(h->stage[s]);
     if (h->stage_ev[s]) cudaEventDestroy(h->stage_ev[s]);
   }
-  h->E.release(); h->doc_ptr.release(); h->ent.release(); h->sel.release(); h->rpad.release();
-  h->Kt.release(); h->Mt.release(); h->colmin.release(); h->ua.release(); h->ub.release();
+  h->E.release(); h->doc_ptr.release(); h->order.release(); h->ent.release(); h->sel.release(); h->rpad.release();
+  h->Kt.release(); h->Mt.release(); h->colmin.release(); h->ua.release(); h->ub.release(); h->umask.release();
   h->dist_tmp.release(); h->flags.release(); h->flagged.release(); h->counters.release();
   h->fb_scratch.release();
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
@@ -431,10 +434,18 @@ wmd_status wmd_set_targets(wmd_handle* h, const int64_t* col_ptr, const int32_t*
   int64_t mx = 0;
   for (int64_t j = 0; j <= N; ++j) dp[j] = (int32_t)col_ptr[j];
   for (int64_t j = 0; j < N; ++j) mx = std::max(mx, col_ptr[j + 1] - col_ptr[j]);
+  // processing order: stable counting sort of the documents by length (integer bookkeeping)
+  std::vector<int64_t> cnt(mx + 2, 0);
+  for (int64_t j = 0; j < N; ++j) cnt[col_ptr[j + 1] - col_ptr[j] + 1]++;
+  for (int64_t L = 1; L < mx + 2; ++L) cnt[L] += cnt[L - 1];
+  std::vector<int32_t> ord(N);
+  for (int64_t j = 0; j < N; ++j) ord[cnt[col_ptr[j + 1] - col_ptr[j]]++] = (int32_t)j;
   std::vector<Entry> en(nnz);
   for (int64_t q = 0; q < nnz; ++q) en[q] = Entry{row_idx[q], val[q]};
   CK(h, h->doc_ptr.ensure(N + 1));
   CK(h, h->ent.ensure(nnz));
+  CK(h, h->order.ensure(N));
+  CK(h, cudaMemcpyAsync(h->order.p, ord.data(), N * sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
   CK(h, cudaMemcpyAsync(h->doc_ptr.p, dp.data(), (N + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
   CK(h, cudaMemcpyAsync(h->ent.p, en.data(), nnz * sizeof(Entry), cudaMemcpyHostToDevice, h->stream));
   CK(h, h->flags.ensure(N));
@@ -469,6 +480,7 @@ wmd_status wmd_query(wmd_handle* h, const int32_t* query_ids, const float* query
   CK(h, h->Mt.ensure((size_t)h->V * ld));
   CK(h, h->ua.ensure((size_t)N * ld));
   CK(h, h->ub.ensure((size_t)N * ld));
+  CK(h, h->umask.ensure((size_t)N * ((ld + 31) / 32)));
   cudaStream_t st = h->stream;
 
   // Upload (sel, r padded with zeros to ld) from pinned staging, double-buffered.
@@ -522,16 +534,16 @@ wmd_status wmd_query(wmd_handle* h, const int32_t* query_ids, const float* query
     float* bufs[2] = {h->ua.p, h->ub.p};
     for (int32_t t = 0; t < iters; ++t) {
       float* u_out = bufs[t & 1];
-      wmd::launch_sddmm_spmm_iter(h->doc_ptr.p, h->ent.p, N, h->Kt.p, ld, v_r, h->rpad.p, u_in, u_out,
-                                  h->flags.p, st);
+      wmd::launch_sddmm_spmm_iter(h->order.p, h->doc_ptr.p, h->ent.p, N, h->Kt.p, ld, v_r, h->rpad.p, u_in, u_out,
+                                  h->umask.p, h->flags.p, st);
       u_in = u_out;
     }
     launches += iters;
     h->st.iter_launches += iters;
     if (pe) CK(h, cudaEventRecord(pe->ev[2], st));
     // a5
-    wmd::launch_final_wmd(h->doc_ptr.p, h->ent.p, N, h->Kt.p, h->Mt.p, ld, v_r, h->rpad.p, u_in, dist,
-                          h->flags.p, h->flagged.p, h->counters.p, st);
+    wmd::launch_final_wmd(h->order.p, h->doc_ptr.p, h->ent.p, N, h->Kt.p, h->Mt.p, ld, v_r, h->rpad.p, u_in,
+                          h->umask.p, dist, h->flags.p, h->flagged.p, h->counters.p, st);
     ++launches;
     if (pe) CK(h, cudaEventRecord(pe->ev[3], st));
     h->u_valid = u_in != nullptr;

@@ -35,15 +35,16 @@ void launch_build_ktilde(const float* E, int64_t V, int d, const int32_t* sel, i
 
 // --- a4: one fused SDDMM_SpMM iteration for all documents ------------
 // u_in == nullptr: first iteration with the constant u0 = 1/x0 = v_r.
-void launch_sddmm_spmm_iter(const int32_t* doc_ptr, const Entry* ent, int64_t N, const float* Kt,
-                            int ld, int v_r, const float* rpad, const float* u_in, float* u_out,
-                            uint8_t* flags, cudaStream_t st);
+// `order` lists the documents sorted by length (processing order only; results are per document).
+void launch_sddmm_spmm_iter(const int32_t* order, const int32_t* doc_ptr, const Entry* ent, int64_t N,
+                            const float* Kt, int ld, int v_r, const float* rpad, const float* u_in,
+                            float* u_out, uint32_t* umask, uint8_t* flags, cudaStream_t st);
 
 // --- a5: final u/v/WMD step -----------------------------------
-void launch_final_wmd(const int32_t* doc_ptr, const Entry* ent, int64_t N, const float* Kt,
-                      const float* Mt, int ld, int v_r, const float* rpad, const float* u_in,
-                      float* dist, uint8_t* flags, int32_t* flagged_list, int32_t* flagged_count,
-                      cudaStream_t st);
+void launch_final_wmd(const int32_t* order, const int32_t* doc_ptr, const Entry* ent, int64_t N,
+                      const float* Kt, const float* Mt, int ld, int v_r, const float* rpad,
+                      const float* u_in, const uint32_t* umask, float* dist, uint8_t* flags,
+                      int32_t* flagged_list, int32_t* flagged_count, cudaStream_t st);
 
 // --- NEXT-1: all iterations + final step in one launch ------------------------------------
 // Returns false if the shape is not supported by the fused kernel (caller uses the

@@ -148,216 +148,237 @@ __global__ void __launch_bounds__(256) build_ktilde_kernel(const float* __restri
 }
 
 // ============================================================================================
-// a4. sddmm_spmm_iter: one warp per target document j; G lanes per K~ row (float4 each), so a
-// warp step handles NG = 32/G nonzeros. Per nonzero e = (k, c_kj):
-//     s_e   = sum_i K~_ki u_ij              (SDDMM: K^T u only at c's support)
-//     v~_e  = c_kj / s_e                     (c .* 1./(K^T u))
-//     acc_i += K~_ki v~_e                    (SpMM: K v, v never stored)
-// then u_ij = r_i / acc_i  (= 1/x with x = diag(1/r) K v; update_x_u) and an
-// exact per-document power-of-two gauge 2^-round((e_max+e_min)/2) (R21).
-// Documents are owned by one warp: no atomics, deterministic.
-// Bound: L2->SM gather of K~ rows (4*ld bytes per nonzero) + HBM stream of c and u.
+// a4 + a5. sinkhorn_pass<G, U, FINAL>: one pass over all target documents.
+//
+// FINAL = false (a4, one launch per iteration; the paper's fused SDDMM_SpMM):
+//   per nonzero e = (k, c_kj):  s_e = sum_i K~_ki u_ij           (SDDMM at c's support, :146)
+//                                v~_e = c_kj / s_e                (c .* 1./(K^T u))
+//                                acc_i += K~_ki v~_e              (SpMM K v; v never stored)
+//   then u_ij = r_i / acc_i (= 1/x, x = diag(1/r) K v; update_x_u) and the exact
+//   per-document power-of-two gauge 2^-floor((e_max+e_min)/2) (R21).
+// FINAL = true (a5): s_e, v~_e as above, q_e = sum_i K~_ki M_ik u_i and
+//   WMD_j = sum_e v~_e q_e (= sum_i u_i ((K.*M) v)_i, summed over e instead of i).
+//
+// Mapping: one warp per document (warp-persistent, next document prefetched while the current
+// one's K~ rows are in flight); G lanes per K~ row (float4 each, ld <= 4G); NG = 32/G groups
+// per warp, each taking U consecutive nonzeros per step (STEP = NG*U <= 32 gathers in flight
+// per warp). The U partial dot products of a group are combined by a transpose-reduce
+// (U-1 shuffles for U = G instead of U log2 G), so each lane ends with the full s of ONE
+// nonzero: one division per lane per step, then U broadcasts of v~ for the axpy.
+// Documents are owned by one warp: no atomics in the arithmetic, deterministic.
+// Bound: K~ row gathers from L2 (4*ld bytes per nonzero) + the HBM stream of c and u.
 // ============================================================================================
+template <int X>
+struct Log2 { static constexpr int value = 1 + Log2<X / 2>::value; };
+template <>
+struct Log2<1> { static constexpr int value = 0; };
+
+// p[0..U) per lane; returns, in lane `sub` of a G-lane group, the group sum of p[sub >> SHIFT]
+// where SHIFT = log2(G) - log2(U).
 template <int G, int U>
-__global__ void __launch_bounds__(256, 3) sddmm_spmm_iter_kernel(
-    const int32_t* __restrict__ doc_ptr, const Entry* __restrict__ ent, int64_t N,
-    const float* __restrict__ Kt, int ld, float u0, const float* __restrict__ rpad,
-    const float* __restrict__ u_in, float* __restrict__ u_out, uint8_t* __restrict__ flags) {
-  constexpr int NG = 32 / G, STEP = NG * U;
-  static_assert(STEP <= 32, "one step covers at most one 32-entry chunk");
-  const int lane = threadIdx.x & 31, grp = lane / G, sub = lane % G;
-  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const bool act = sub * 4 < ld;
-  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
-  const float4 r = act ? ldg4(rpad + sub * 4) : zero;
-  auto load_u = [&](int64_t jj) -> float4 {
-    if (u_in == nullptr) {  // x0 = 1/v_r  =>  u0 = v_r on the v_r real rows (PAPER.md:59)
-      return make_float4(r.x > 0.f ? u0 : 0.f, r.y > 0.f ? u0 : 0.f, r.z > 0.f ? u0 : 0.f,
-                         r.w > 0.f ? u0 : 0.f);
-    }
-    return act ? ldg4(u_in + jj * ld + sub * 4) : zero;
-  };
-  // Warp-persistent over documents j = warp, warp + nwarps, ...; the next document's pointers,
-  // first 32 entries and u are prefetched while the current document's K~ rows are in flight.
-  int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  int b = 0, e = 0;
-  int2 my = make_int2(0, 0);
-  float4 u = zero;
-  if (j < N) {
-    b = __ldg(doc_ptr + j); e = __ldg(doc_ptr + j + 1);
-    if (lane < e - b) my = __ldg(reinterpret_cast<const int2*>(ent) + b + lane);
-    u = load_u(j);
-  }
-  for (; j < N; j += nwarps) {
-    const int64_t jn = j + nwarps;
-    int bn = 0, en = 0;
-    if (jn < N) { bn = __ldg(doc_ptr + jn); en = __ldg(doc_ptr + jn + 1); }
-    int2 myn = make_int2(0, 0);
-    float4 unx = zero;
-    bool prefetched = false;
-    const float4 uscaled = make_float4(u.x * u0 * kUnderScale, u.y * u0 * kUnderScale,
-                                       u.z * u0 * kUnderScale, u.w * u0 * kUnderScale);
-    float4 acc = zero, under = zero;
-    bool bad = false;
-    for (int base = b; base < e; base += 32) {
-      const int cnt = min(32, e - base);
-      if (base != b) {
-        my = make_int2(0, 0);
-        if (lane < cnt) my = __ldg(reinterpret_cast<const int2*>(ent) + base + lane);
+__device__ __forceinline__ float transpose_reduce(float (&p)[U], int sub) {
+#pragma unroll
+  for (int r = 0, o = G / 2; o >= 1; ++r, o >>= 1) {
+    const int n = U >> r;  // values still held (compile-time after unrolling)
+    if (n > 1) {
+      const bool upper = (sub & o) != 0;
+#pragma unroll
+      for (int t = 0; t < n / 2; ++t) {
+        const float send = upper ? p[t] : p[t + n / 2];
+        const float keep = upper ? p[t + n / 2] : p[t];
+        p[t] = keep + __shfl_xor_sync(kFull, send, o);
       }
-      for (int s0 = 0; s0 < cnt; s0 += STEP) {
-        float4 kr[U];
-        float cv[U];
-#pragma unroll
-        for (int q = 0; q < U; ++q) {
-          const int idx = s0 + q * NG + grp;
-          const int k = __shfl_sync(kFull, my.x, idx & 31);
-          const float c = __int_as_float(__shfl_sync(kFull, my.y, idx & 31));
-          const bool valid = idx < cnt;
-          cv[q] = valid ? c : 0.f;
-          kr[q] = (valid && act) ? ldg4(Kt + (int64_t)k * ld + sub * 4) : zero;
-        }
-        if (!prefetched) {  // overlap the next document's metadata with these gathers
-          prefetched = true;
-          if (jn < N) {
-            if (lane < en - bn) myn = __ldg(reinterpret_cast<const int2*>(ent) + bn + lane);
-            unx = load_u(jn);
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < U; ++q) {
-          float s = dot4(kr[q], u);
-#pragma unroll
-          for (int off = G / 2; off; off >>= 1) s += __shfl_xor_sync(kFull, s, off);
-          if (cv[q] != 0.f) {
-            const float vt = cv[q] / s;
-            // certificate: underflowed K~ entries must not matter (see kUnderScale)
-            bad |= (kr[q].x < FLT_MIN && uscaled.x > s) | (kr[q].y < FLT_MIN && uscaled.y > s) |
-                   (kr[q].z < FLT_MIN && uscaled.z > s) | (kr[q].w < FLT_MIN && uscaled.w > s);
-            under.x += kr[q].x < FLT_MIN ? vt : 0.f; under.y += kr[q].y < FLT_MIN ? vt : 0.f;
-            under.z += kr[q].z < FLT_MIN ? vt : 0.f; under.w += kr[q].w < FLT_MIN ? vt : 0.f;
-            axpy4(acc, kr[q], vt);
-          }
-        }
-      }
+    } else {
+      p[0] += __shfl_xor_sync(kFull, p[0], o);
     }
-#pragma unroll
-    for (int off = G; off < 32; off <<= 1) {
-      const float4 o = shfl_xor4(acc, off);
-      acc.x += o.x; acc.y += o.y; acc.z += o.z; acc.w += o.w;
-      const float4 p = shfl_xor4(under, off);
-      under.x += p.x; under.y += p.y; under.z += p.z; under.w += p.w;
-    }
-    float4 un;
-    un.x = r.x > 0.f ? r.x / acc.x : 0.f; un.y = r.y > 0.f ? r.y / acc.y : 0.f;
-    un.z = r.z > 0.f ? r.z / acc.z : 0.f; un.w = r.w > 0.f ? r.w / acc.w : 0.f;
-    // range certificate + gauge over the real rows
-    float mx = 0.f, mn = FLT_MAX;
-#define WMD_ROW(c)                                               \
-    if (r.c > 0.f) {                                             \
-      bad |= !normal_pos(un.c) || under.c * kUnderScale > acc.c; \
-      mx = fmaxf(mx, un.c); mn = fminf(mn, un.c);                \
-    }
-    WMD_ROW(x) WMD_ROW(y) WMD_ROW(z) WMD_ROW(w)
-#undef WMD_ROW
-    bad = __any_sync(kFull, bad);
-#pragma unroll
-    for (int off = G / 2; off; off >>= 1) {
-      mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, off));
-      mn = fminf(mn, __shfl_xor_sync(kFull, mn, off));
-    }
-    if (!bad) {
-      const int g = (ilogbf(mx) + ilogbf(mn)) >> 1;  // floor((e_max + e_min) / 2)
-      un.x = ldexpf(un.x, -g); un.y = ldexpf(un.y, -g); un.z = ldexpf(un.z, -g); un.w = ldexpf(un.w, -g);
-    } else if (lane == 0) {
-      flags[j] |= kFlagFp32Range;
-    }
-    if (grp == 0 && act) *reinterpret_cast<float4*>(u_out + j * ld + sub * 4) = un;
-    b = bn; e = en; my = myn; u = unx;
   }
+  return p[0];
 }
 
-// ============================================================================================
-// a5. final_wmd: u from the last iteration; per nonzero
-//     s_e = sum_i K~_ki u_i,  v~_e = c_kj / s_e,  q_e = sum_i K~_ki M_ik u_i,  WMD_j = sum_e v~_e q_e
-// (= sum_i u_i ((K.*M) v)_i; summed over e instead of i). Non-finite results and
-// documents flagged by the iterations go to the FP64 fallback list.
-// ============================================================================================
-template <int G, int U>
-__global__ void __launch_bounds__(256) final_wmd_kernel(
-    const int32_t* __restrict__ doc_ptr, const Entry* __restrict__ ent, int64_t N,
-    const float* __restrict__ Kt, const float* __restrict__ Mt, int ld, float u0,
-    const float* __restrict__ rpad, const float* __restrict__ u_in, float* __restrict__ dist,
-    uint8_t* __restrict__ flags, int32_t* __restrict__ flagged_list,
-    int32_t* __restrict__ flagged_count) {
+__device__ __forceinline__ uint32_t under_bits(float4 k) {
+  return (k.x < FLT_MIN ? 1u : 0u) | (k.y < FLT_MIN ? 2u : 0u) | (k.z < FLT_MIN ? 4u : 0u) |
+         (k.w < FLT_MIN ? 8u : 0u);
+}
+
+template <int G, int U, bool FINAL, bool MAKE_MASK>
+__global__ void __launch_bounds__(256, FINAL ? 2 : 3) sinkhorn_pass_kernel(
+    const int32_t* __restrict__ order, const int32_t* __restrict__ doc_ptr,
+    const Entry* __restrict__ ent, int64_t N, const float* __restrict__ Kt,
+    const float* __restrict__ Mt, int ld, int v_r, const float* __restrict__ rpad,
+    const float* __restrict__ u_in, float* __restrict__ u_out, uint32_t* __restrict__ umask,
+    int mask_words, float* __restrict__ dist, uint8_t* __restrict__ flags,
+    int32_t* __restrict__ flagged_list, int32_t* __restrict__ flagged_count) {
   constexpr int NG = 32 / G;
+  constexpr int SHIFT = Log2<G>::value - Log2<U>::value;
+  static_assert(U <= G, "at most one nonzero per lane per step");
   const int lane = threadIdx.x & 31, grp = lane / G, sub = lane % G;
-  const int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (j >= N) return;
+  const int qm = sub >> SHIFT;                       // this lane's nonzero slot within a step
+  const bool owner = (sub & ((1 << SHIFT) - 1)) == 0;
+  const int gbase = grp * G;
+  const int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   const bool act = sub * 4 < ld;
+  const float u0 = (float)v_r;
+  const int mword = (sub * 4) >> 5, mshift = (sub * 4) & 31;
   const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  const float4 r = act ? ldg4(rpad + sub * 4) : zero;
+  const int2* ent2 = reinterpret_cast<const int2*>(ent);
+
+  // Round structure: in each round the warp's NG groups take NG consecutive documents of the
+  // length-sorted order, so their step counts match; the next round is prefetched.
+  auto head = [&](int64_t pos, int64_t& jj, int& bb, int& nn) {
+    jj = -1; bb = 0; nn = 0;
+    if (pos < N) {
+      jj = __ldg(order + pos);
+      bb = __ldg(doc_ptr + jj);
+      nn = __ldg(doc_ptr + jj + 1) - bb;
+    }
+  };
+  auto body = [&](int64_t jj, int bb, int nn, int2& e0, float4& uu, uint32_t& mb) {
+    e0 = make_int2(0, 0); uu = zero; mb = 0u;
+    if (jj < 0) return;
+    if (qm < nn) e0 = __ldg(ent2 + bb + qm);
+    if (u_in == nullptr) {  // x0 = 1/v_r  =>  u0 = v_r on the v_r real rows (PAPER.md:59)
+      uu = make_float4(r.x > 0.f ? u0 : 0.f, r.y > 0.f ? u0 : 0.f, r.z > 0.f ? u0 : 0.f,
+                       r.w > 0.f ? u0 : 0.f);
+    } else if (act) {
+      uu = ldg4(u_in + jj * ld + sub * 4);
+    }
+    if (!MAKE_MASK && act) mb = (__ldg(umask + jj * mask_words + mword) >> mshift) & 0xFu;
+  };
+
+  int64_t pos = warp * NG + grp;
+  int64_t j;
+  int b, n;
+  head(pos, j, b, n);
+  int2 my;
   float4 u;
-  if (u_in == nullptr) {
-    const float4 r = act ? ldg4(rpad + sub * 4) : zero;
-    u.x = r.x > 0.f ? u0 : 0.f; u.y = r.y > 0.f ? u0 : 0.f;
-    u.z = r.z > 0.f ? u0 : 0.f; u.w = r.w > 0.f ? u0 : 0.f;
-  } else {
-    u = act ? ldg4(u_in + j * ld + sub * 4) : zero;
-  }
-  const float4 uscaled = make_float4(u.x * u0 * kUnderScale, u.y * u0 * kUnderScale,
-                                     u.z * u0 * kUnderScale, u.w * u0 * kUnderScale);
-  const int b = doc_ptr[j], e = doc_ptr[j + 1];
-  float wsum = 0.f;
-  bool bad = false;
-  for (int base = b; base < e; base += 32) {
-    const int cnt = min(32, e - base);
-    int2 my = make_int2(0, 0);
-    if (lane < cnt) my = __ldg(reinterpret_cast<const int2*>(ent) + base + lane);
-    for (int s0 = 0; s0 < cnt; s0 += NG * U) {
-      float4 kr[U], km[U];
-      float cv[U];
+  uint32_t mbits;
+  body(j, b, n, my, u, mbits);
+  for (int64_t rb = warp * NG; rb < N; rb += nwarps * NG, pos += nwarps * NG) {
+    int64_t jn;
+    int bn, nn_;
+    head(pos + nwarps * NG, jn, bn, nn_);
+    int2 myn;
+    float4 unx;
+    uint32_t mbn;
+    bool prefetched = false;
+    const int steps = __reduce_max_sync(kFull, (n + U - 1) / U);
+    float4 acc = zero;
+    float smin = FLT_MAX, vmax = 0.f, wsum = 0.f;
+    uint32_t ubits = 0u;
+    for (int s = 0; s < steps; ++s) {
+      const int eb = s * U;
+      float4 kr[U], mr[U];
 #pragma unroll
       for (int q = 0; q < U; ++q) {
-        const int idx = s0 + q * NG + grp;
-        const int k = __shfl_sync(kFull, my.x, idx & 31);
-        const float c = __int_as_float(__shfl_sync(kFull, my.y, idx & 31));
-        const bool valid = idx < cnt;
-        cv[q] = valid ? c : 0.f;
-        kr[q] = (valid && act) ? ldg4(Kt + (int64_t)k * ld + sub * 4) : zero;
-        km[q] = (valid && act) ? ldg4(Mt + (int64_t)k * ld + sub * 4) : zero;
+        const int k = __shfl_sync(kFull, my.x, gbase + (q << SHIFT));
+        const bool valid = eb + q < n && act;
+        kr[q] = valid ? ldg4(Kt + (int64_t)k * ld + sub * 4) : zero;
+        if (FINAL) mr[q] = valid ? ldg4(Mt + (int64_t)k * ld + sub * 4) : zero;
+        if (MAKE_MASK && valid) ubits |= under_bits(kr[q]);
       }
+      const bool myvalid = eb + qm < n;
+      const float c = __int_as_float(my.y);
+      // next step's nonzero (and, once per round, the next round's document) while K~ is in flight
+      my = make_int2(0, 0);
+      if (eb + U + qm < n) my = __ldg(ent2 + b + eb + U + qm);
+      if (!prefetched) {
+        prefetched = true;
+        body(jn, bn, nn_, myn, unx, mbn);
+      }
+      float p[U];
 #pragma unroll
-      for (int q = 0; q < U; ++q) {
-        const float4 kmq = make_float4(kr[q].x * km[q].x, kr[q].y * km[q].y, kr[q].z * km[q].z,
-                                       kr[q].w * km[q].w);  // (K .* M)
-        float s = dot4(kr[q], u), t = dot4(kmq, u);
+      for (int q = 0; q < U; ++q) p[q] = dot4(kr[q], u);
+      const float sv = transpose_reduce<G, U>(p, sub);
+      float vt = 0.f;
+      if (myvalid) {
+        vt = c / sv;
+        smin = fminf(smin, sv);
+        vmax = fmaxf(vmax, vt);
+      }
+      if (FINAL) {
+        float t[U];
 #pragma unroll
-        for (int off = G / 2; off; off >>= 1) {
-          s += __shfl_xor_sync(kFull, s, off);
-          t += __shfl_xor_sync(kFull, t, off);
+        for (int q = 0; q < U; ++q) {  // (K .* M) row times u
+          const float4 km = make_float4(kr[q].x * mr[q].x, kr[q].y * mr[q].y,
+                                        kr[q].z * mr[q].z, kr[q].w * mr[q].w);
+          t[q] = dot4(km, u);
         }
-        if (cv[q] != 0.f) {
-          const float vt = cv[q] / s;
-          bad |= !(fabsf(vt) <= FLT_MAX);
-          bad |= (kr[q].x < FLT_MIN && uscaled.x > s) | (kr[q].y < FLT_MIN && uscaled.y > s) |
-                 (kr[q].z < FLT_MIN && uscaled.z > s) | (kr[q].w < FLT_MIN && uscaled.w > s);
-          wsum = fmaf(vt, t, wsum);
+        const float tv = transpose_reduce<G, U>(t, sub);
+        if (myvalid && owner) wsum = fmaf(vt, tv, wsum);
+      } else {
+#pragma unroll
+        for (int q = 0; q < U; ++q) axpy4(acc, kr[q], __shfl_sync(kFull, vt, gbase + (q << SHIFT)));
+      }
+    }
+    // ---- per-document epilogue (each G-lane group owns one document)
+    if (MAKE_MASK) {  // rows with an underflowed K~ entry in this document (iteration-invariant)
+      mbits = ubits;
+      if (!FINAL) {
+        for (int w = 0; w < mask_words; ++w) {
+          uint32_t word = (act && mword == w) ? (ubits << mshift) : 0u;
+#pragma unroll
+          for (int off = G / 2; off; off >>= 1) word |= __shfl_xor_sync(kFull, word, off);
+          if (sub == 0 && j >= 0) umask[j * mask_words + w] = word;
         }
       }
     }
-  }
-  // sum the NG per-group partials (each replicated across its G lanes)
+    // FP32 range certificate (see kUnderScale)
+    float umu = 0.f;
+    if (mbits & 1u) umu = fmaxf(umu, u.x);
+    if (mbits & 2u) umu = fmaxf(umu, u.y);
+    if (mbits & 4u) umu = fmaxf(umu, u.z);
+    if (mbits & 8u) umu = fmaxf(umu, u.w);
 #pragma unroll
-  for (int off = G; off < 32; off <<= 1) wsum += __shfl_xor_sync(kFull, wsum, off);
-  bad = __any_sync(kFull, bad);
-  if (lane == 0) {
-    dist[j] = wsum;
-    const bool need = bad || !(fabsf(wsum) <= FLT_MAX) || (flags[j] & kFlagFp32Range);
-    if (need) {
-      flags[j] |= kFlagFp32Range;
-      const int32_t slot = atomicAdd(flagged_count, 1);
-      flagged_list[slot] = (int32_t)j;
+    for (int off = G / 2; off; off >>= 1) {
+      smin = fminf(smin, __shfl_xor_sync(kFull, smin, off));
+      vmax = fmaxf(vmax, __shfl_xor_sync(kFull, vmax, off));
+      umu = fmaxf(umu, __shfl_xor_sync(kFull, umu, off));
     }
+    int bad = ((umu * u0) * kUnderScale > smin || !(vmax <= FLT_MAX)) ? 1 : 0;
+    if (FINAL) {
+#pragma unroll
+      for (int off = G / 2; off; off >>= 1) {
+        wsum += __shfl_xor_sync(kFull, wsum, off);
+        bad |= __shfl_xor_sync(kFull, bad, off);
+      }
+      if (sub == 0 && j >= 0) {
+        dist[j] = wsum;
+        if (bad || !(fabsf(wsum) <= FLT_MAX) || (flags[j] & kFlagFp32Range)) {
+          flags[j] |= kFlagFp32Range;
+          flagged_list[atomicAdd(flagged_count, 1)] = (int32_t)j;
+        }
+      }
+    } else {
+      float4 un;
+      un.x = r.x > 0.f ? r.x / acc.x : 0.f; un.y = r.y > 0.f ? r.y / acc.y : 0.f;
+      un.z = r.z > 0.f ? r.z / acc.z : 0.f; un.w = r.w > 0.f ? r.w / acc.w : 0.f;
+      const float vcap = (float)n * vmax * kUnderScale;  // bound on the underflowed terms
+      float mx = 0.f, mn = FLT_MAX;
+#define WMD_ROW(c, bit)                                                   \
+      if (r.c > 0.f) {                                                    \
+        bad |= (!normal_pos(un.c) || ((mbits & bit) && vcap > acc.c));    \
+        mx = fmaxf(mx, un.c); mn = fminf(mn, un.c);                       \
+      }
+      WMD_ROW(x, 1u) WMD_ROW(y, 2u) WMD_ROW(z, 4u) WMD_ROW(w, 8u)
+#undef WMD_ROW
+#pragma unroll
+      for (int off = G / 2; off; off >>= 1) {
+        mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, off));
+        mn = fminf(mn, __shfl_xor_sync(kFull, mn, off));
+        bad |= __shfl_xor_sync(kFull, bad, off);
+      }
+      if (!bad) {
+        const int g = (ilogbf(mx) + ilogbf(mn)) >> 1;  // floor((e_max + e_min) / 2)
+        const float sc = ldexpf(1.0f, -g);             // |g| <= 126 when all u are normal
+        un.x *= sc; un.y *= sc; un.z *= sc; un.w *= sc;
+      } else if (sub == 0 && j >= 0) {
+        flags[j] |= kFlagFp32Range;
+      }
+      if (act && j >= 0) *reinterpret_cast<float4*>(u_out + j * ld + sub * 4) = un;
+    }
+    j = jn; b = bn; n = nn_; my = myn; u = unx; mbits = mbn;
   }
 }
 
@@ -465,7 +486,8 @@ void launch_build_ktilde(const float* E, int64_t V, int d, const int32_t* sel, i
   build_ktilde_kernel<<<(unsigned)grid, 256, smem, st>>>(E, V, d, sel, v_r, ld, lambda, Kt, Mt, colmin);
 }
 
-// U = gathers in flight per lane per step: NG*U covers a 32-entry chunk where registers allow.
+// U = nonzeros per group per step: U = G up to 8 so that the transpose-reduce leaves exactly one
+// nonzero per lane (fewer lanes idle); (32/G) documents per warp.
 #define WMD_DISPATCH_G(ld, MACRO) \
   switch (lanes_per_row(ld)) {    \
     case 2: MACRO(2, 2); break;   \
@@ -475,8 +497,9 @@ void launch_build_ktilde(const float* E, int64_t V, int d, const int32_t* sel, i
     default: MACRO(32, 8); break; \
   }
 
-// Persistent grid for the per-iteration kernel: 3 resident 256-thread blocks per SM.
-unsigned iter_grid(int64_t N) {
+// Persistent grid for the pass kernels: `per_sm` resident 256-thread blocks per SM, or fewer if
+// the documents (groups_per_warp per warp) do not need them.
+unsigned pass_grid(int64_t N, int ld, int per_sm) {
   static int sms = 0;
   if (!sms) {
     int dev = 0;
@@ -484,27 +507,47 @@ unsigned iter_grid(int64_t N) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (sms <= 0) sms = 148;
   }
-  const int64_t need = (N + 7) / 8;
-  return (unsigned)std::min<int64_t>(need, (int64_t)sms * 3);
+  const int ng = 32 / lanes_per_row(ld);
+  const int64_t warps = (N + ng - 1) / ng;
+  const int64_t need = (warps + 7) / 8;
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)sms * per_sm));
 }
 
-void launch_sddmm_spmm_iter(const int32_t* doc_ptr, const Entry* ent, int64_t N, const float* Kt,
-                            int ld, int v_r, const float* rpad, const float* u_in, float* u_out,
-                            uint8_t* flags, cudaStream_t st) {
-  const unsigned grid = iter_grid(N);
-#define L_(G, U) sddmm_spmm_iter_kernel<G, U><<<grid, 256, 0, st>>>(doc_ptr, ent, N, Kt, ld, (float)v_r, rpad, u_in, u_out, flags)
-  WMD_DISPATCH_G(ld, L_)
+int mask_words_for(int ld) { return (ld + 31) / 32; }
+
+void launch_sddmm_spmm_iter(const int32_t* order, const int32_t* doc_ptr, const Entry* ent, int64_t N,
+                            const float* Kt, int ld, int v_r, const float* rpad, const float* u_in,
+                            float* u_out, uint32_t* umask, uint8_t* flags, cudaStream_t st) {
+  const unsigned grid = pass_grid(N, ld, 3);
+  const int mw = mask_words_for(ld);
+  // the first iteration records the underflow row masks, later ones read them
+  if (u_in == nullptr) {
+#define L_(G, U) sinkhorn_pass_kernel<G, U, false, true><<<grid, 256, 0, st>>>(order, doc_ptr, ent, N, Kt, nullptr, ld, v_r, rpad, u_in, u_out, umask, mw, nullptr, flags, nullptr, nullptr)
+    WMD_DISPATCH_G(ld, L_)
 #undef L_
+  } else {
+#define L_(G, U) sinkhorn_pass_kernel<G, U, false, false><<<grid, 256, 0, st>>>(order, doc_ptr, ent, N, Kt, nullptr, ld, v_r, rpad, u_in, u_out, umask, mw, nullptr, flags, nullptr, nullptr)
+    WMD_DISPATCH_G(ld, L_)
+#undef L_
+  }
 }
 
-void launch_final_wmd(const int32_t* doc_ptr, const Entry* ent, int64_t N, const float* Kt,
-                      const float* Mt, int ld, int v_r, const float* rpad, const float* u_in,
-                      float* dist, uint8_t* flags, int32_t* flagged_list, int32_t* flagged_count,
-                      cudaStream_t st) {
-  const unsigned grid = (unsigned)((N + 7) / 8);
-#define L_(G, U) final_wmd_kernel<G, U><<<grid, 256, 0, st>>>(doc_ptr, ent, N, Kt, Mt, ld, (float)v_r, rpad, u_in, dist, flags, flagged_list, flagged_count)
-  WMD_DISPATCH_G(ld, L_)
+void launch_final_wmd(const int32_t* order, const int32_t* doc_ptr, const Entry* ent, int64_t N,
+                      const float* Kt, const float* Mt, int ld, int v_r, const float* rpad,
+                      const float* u_in, const uint32_t* umask, float* dist, uint8_t* flags,
+                      int32_t* flagged_list, int32_t* flagged_count, cudaStream_t st) {
+  const unsigned grid = pass_grid(N, ld, 2);
+  const int mw = mask_words_for(ld);
+  uint32_t* um = const_cast<uint32_t*>(umask);
+  if (u_in == nullptr) {  // iters == 0: no iteration recorded the masks
+#define L_(G, U) sinkhorn_pass_kernel<G, U, true, true><<<grid, 256, 0, st>>>(order, doc_ptr, ent, N, Kt, Mt, ld, v_r, rpad, u_in, nullptr, um, mw, dist, flags, flagged_list, flagged_count)
+    WMD_DISPATCH_G(ld, L_)
 #undef L_
+  } else {
+#define L_(G, U) sinkhorn_pass_kernel<G, U, true, false><<<grid, 256, 0, st>>>(order, doc_ptr, ent, N, Kt, Mt, ld, v_r, rpad, u_in, nullptr, um, mw, dist, flags, flagged_list, flagged_count)
+    WMD_DISPATCH_G(ld, L_)
+#undef L_
+  }
 }
 
 size_t fallback_scratch_bytes(int64_t max_doc_nnz) {
