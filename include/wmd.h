@@ -46,6 +46,7 @@ extern "C" {
 #endif
 
 #define WMD_MAX_VR 128          /* maximum distinct query words v_r per query */
+#define WMD_MAX_V (1 << 24)     /* maximum vocabulary size (V * WMD_MAX_VR < 2^31: 32-bit row offsets) */
 
 typedef struct wmd_handle wmd_handle; /* opaque; one per GPU / rank */
 
@@ -96,7 +97,7 @@ typedef struct {
 
 /* Create a handle on CUDA device `device` holding a copy of the embeddings.
  * vocab_emb: host or device, V x d FP32 row-major (the paper's `vecs`).
- * Errors: INVALID_ARGUMENT (NULL, V<1, d<1, V >= 2^31), NONFINITE_EMBEDDING, OUT_OF_MEMORY, CUDA.
+ * Errors: INVALID_ARGUMENT (NULL, V<1, d<1, V > WMD_MAX_V), NONFINITE_EMBEDDING, OUT_OF_MEMORY, CUDA.
  * On error *out is set to NULL. */
 WMD_API wmd_status wmd_create(const float* vocab_emb, int64_t V, int32_t d, int32_t device, wmd_handle** out);
 

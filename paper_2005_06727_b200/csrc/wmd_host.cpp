@@ -311,7 +311,7 @@ wmd_status wmd_validate_query(const int32_t* ids, const float* weights, int32_t 
 wmd_status wmd_create(const float* vocab_emb, int64_t V, int32_t d, int32_t device, wmd_handle** out) {
   if (!out) return WMD_ERR_INVALID_ARGUMENT;
   *out = nullptr;
-  if (!vocab_emb || V < 1 || d < 1 || V >= (int64_t(1) << 31) || device < 0) return WMD_ERR_INVALID_ARGUMENT;
+  if (!vocab_emb || V < 1 || d < 1 || V > WMD_MAX_V || device < 0) return WMD_ERR_INVALID_ARGUMENT;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || device >= ndev) {
     cudaGetLastError();
@@ -476,8 +476,9 @@ wmd_status wmd_query(wmd_handle* h, const int32_t* query_ids, const float* query
 
   const int32_t v_r = n, ld = round_up8(n);
   const int64_t N = h->N;
-  CK(h, h->Kt.ensure((size_t)h->V * ld));
-  CK(h, h->Mt.ensure((size_t)h->V * ld));
+  // +128 floats: the pass kernels gather unpredicated float4s up to 4*32 floats past a row
+  CK(h, h->Kt.ensure((size_t)h->V * ld + 128));
+  CK(h, h->Mt.ensure((size_t)h->V * ld + 128));
   CK(h, h->ua.ensure((size_t)N * ld));
   CK(h, h->ub.ensure((size_t)N * ld));
   CK(h, h->umask.ensure((size_t)N * ((ld + 31) / 32)));

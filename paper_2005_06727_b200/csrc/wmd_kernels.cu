@@ -223,6 +223,8 @@ __global__ void __launch_bounds__(256, FINAL ? 2 : 3) sinkhorn_pass_kernel(
   const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
   const float4 r = act ? ldg4(rpad + sub * 4) : zero;
   const int2* ent2 = reinterpret_cast<const int2*>(ent);
+  const float* kb = Kt + sub * 4;                    // this lane's float4 of every K~ row
+  const float* mb = FINAL ? Mt + sub * 4 : nullptr;  // ... and of every M row
 
   // Round structure: in each round the warp's NG groups take NG consecutive documents of the
   // length-sorted order, so their step counts match; the next round is prefetched.
@@ -272,11 +274,12 @@ __global__ void __launch_bounds__(256, FINAL ? 2 : 3) sinkhorn_pass_kernel(
       float4 kr[U], mr[U];
 #pragma unroll
       for (int q = 0; q < U; ++q) {
-        const int k = __shfl_sync(kFull, my.x, gbase + (q << SHIFT));
-        const bool valid = eb + q < n && act;
-        kr[q] = valid ? ldg4(Kt + (int64_t)k * ld + sub * 4) : zero;
-        if (FINAL) mr[q] = valid ? ldg4(Mt + (int64_t)k * ld + sub * 4) : zero;
-        if (MAKE_MASK && valid) ubits |= under_bits(kr[q]);
+        // Unpredicated gathers: empty slots carry k = 0 (row 0) and lanes past ld read into the
+        // next row (the tables are padded); both only meet u = 0 / v~ = 0 below.
+        const uint32_t off = (uint32_t)__shfl_sync(kFull, my.x, gbase + (q << SHIFT)) * (uint32_t)ld;
+        kr[q] = ldg4(kb + off);
+        if (FINAL) mr[q] = ldg4(mb + off);
+        if (MAKE_MASK && eb + q < n && act) ubits |= under_bits(kr[q]);
       }
       const bool myvalid = eb + qm < n;
       const float c = __int_as_float(my.y);
