@@ -13,8 +13,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libwmd_b200.so")
-SOURCES = ["wmd_kernels.cu", "wmd_host.cpp"]
-HEADERS = ["wmd_internal.h", os.path.join("..", "..", "include", "wmd.h")]
+SOURCES = ["wmd_kernels.cu", "wmd_fused.cu", "wmd_host.cpp"]
+HEADERS = ["wmd_internal.h", "wmd_device.cuh", os.path.join("..", "..", "include", "wmd.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -40,17 +40,19 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str = None) -> str:
+    """Build the library; `defines`/`out` build an experiment variant to another path."""
+    lib = out or LIB
+    if not force and not defines and out is None and not _stale():
         return LIB
     objs = []
-    build_dir = os.path.join(PKG, "build")
+    build_dir = os.path.join(PKG, "build" if out is None else "build_" + os.path.basename(out))
     os.makedirs(build_dir, exist_ok=True)
     nvcc = _nvcc()
     for s in SOURCES:
         src = os.path.join(CSRC, s)
         obj = os.path.join(build_dir, s + ".o")
-        cmd = [nvcc, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
+        cmd = [nvcc, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
         if s.endswith(".cpp"):
             cuda_inc = os.path.join(os.path.dirname(os.path.dirname(nvcc)), "include")
             cmd = ["g++", "-O2", "-std=c++17", "-fPIC", "-fvisibility=hidden", "-Wall",
@@ -63,14 +65,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
         with open(os.path.join(build_dir, s + ".ptxas.txt"), "w") as f:
             f.write(res.stderr)
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static",
            "-o", tmp, *objs]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

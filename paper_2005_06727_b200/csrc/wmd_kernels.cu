@@ -33,6 +33,33 @@ __device__ __forceinline__ float4 shfl_xor4(float4 v, int off) {
   return v;
 }
 __device__ __forceinline__ bool normal_pos(float x) { return x >= FLT_MIN && x <= FLT_MAX; }
+
+// L2 residency: the K~ / M tables (<= V*ld*4 bytes, 51 MB at Scaling) are gathered every
+// iteration and must stay in the 126 MB L2 while ~1 GB of c and u streams past them. Table
+// gathers carry an evict_last policy; the streamed arrays use .cs (evict-first) loads/stores.
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ float4 ldg4_keep(const float4* p, uint64_t pol) {
+#ifdef WMD_NO_L2_HINTS
+  return __ldg(p);
+#else
+  float4 v;
+  asm("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "l"(p), "l"(pol));
+  return v;
+#endif
+}
+#ifdef WMD_STREAM_HINTS
+#define WMD_LDS(p) __ldcs(p)
+#define WMD_STS(p, v) __stcs(p, v)
+#else
+#define WMD_LDS(p) __ldg(p)
+#define WMD_STS(p, v) (*(p) = (v))
+#endif
 __device__ __forceinline__ float max4(float4 v) { return fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)); }
 
 // FP32 range certificate (R21). A K~ entry below FLT_MIN = 2^-126 is subnormal or
@@ -200,8 +227,11 @@ __device__ __forceinline__ uint32_t under_bits(float4 k) {
          (k.w < FLT_MIN ? 8u : 0u);
 }
 
+#ifndef PASS_BLOCKS_PER_SM
+#define PASS_BLOCKS_PER_SM 3
+#endif
 template <int G, int U, bool FINAL, bool MAKE_MASK>
-__global__ void __launch_bounds__(256, FINAL ? 2 : 3) sinkhorn_pass_kernel(
+__global__ void __launch_bounds__(256, FINAL ? 2 : PASS_BLOCKS_PER_SM) sinkhorn_pass_kernel(
     const int32_t* __restrict__ order, const int32_t* __restrict__ doc_ptr,
     const Entry* __restrict__ ent, int64_t N, const float* __restrict__ Kt,
     const float* __restrict__ Mt, int ld, int v_r, const float* __restrict__ rpad,
@@ -223,30 +253,32 @@ __global__ void __launch_bounds__(256, FINAL ? 2 : 3) sinkhorn_pass_kernel(
   const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
   const float4 r = act ? ldg4(rpad + sub * 4) : zero;
   const int2* ent2 = reinterpret_cast<const int2*>(ent);
-  const float* kb = Kt + sub * 4;                    // this lane's float4 of every K~ row
-  const float* mb = FINAL ? Mt + sub * 4 : nullptr;  // ... and of every M row
+  const uint32_t ld4 = (uint32_t)ld >> 2;           // row stride in float4s
+  const float4* kb = reinterpret_cast<const float4*>(Kt) + sub;  // this lane's float4 of a K~ row
+  const float4* mb = FINAL ? reinterpret_cast<const float4*>(Mt) + sub : nullptr;  // ... of an M row
+  const uint64_t keep = l2_evict_last_policy();
 
   // Round structure: in each round the warp's NG groups take NG consecutive documents of the
   // length-sorted order, so their step counts match; the next round is prefetched.
   auto head = [&](int64_t pos, int64_t& jj, int& bb, int& nn) {
     jj = -1; bb = 0; nn = 0;
     if (pos < N) {
-      jj = __ldg(order + pos);
-      bb = __ldg(doc_ptr + jj);
-      nn = __ldg(doc_ptr + jj + 1) - bb;
+      jj = WMD_LDS(order + pos);
+      bb = WMD_LDS(doc_ptr + jj);
+      nn = WMD_LDS(doc_ptr + jj + 1) - bb;
     }
   };
   auto body = [&](int64_t jj, int bb, int nn, int2& e0, float4& uu, uint32_t& mb) {
     e0 = make_int2(0, 0); uu = zero; mb = 0u;
     if (jj < 0) return;
-    if (qm < nn) e0 = __ldg(ent2 + bb + qm);
+    if (qm < nn) e0 = WMD_LDS(ent2 + bb + qm);
     if (u_in == nullptr) {  // x0 = 1/v_r  =>  u0 = v_r on the v_r real rows
       uu = make_float4(r.x > 0.f ? u0 : 0.f, r.y > 0.f ? u0 : 0.f, r.z > 0.f ? u0 : 0.f,
                        r.w > 0.f ? u0 : 0.f);
     } else if (act) {
-      uu = ldg4(u_in + jj * ld + sub * 4);
+      uu = WMD_LDS(reinterpret_cast<const float4*>(u_in + jj * ld) + sub);
     }
-    if (!MAKE_MASK && act) mb = (__ldg(umask + jj * mask_words + mword) >> mshift) & 0xFu;
+    if (!MAKE_MASK && act) mb = (WMD_LDS(umask + jj * mask_words + mword) >> mshift) & 0xFu;
   };
 
   int64_t pos = warp * NG + grp;
@@ -276,16 +308,16 @@ __global__ void __launch_bounds__(256, FINAL ? 2 : 3) sinkhorn_pass_kernel(
       for (int q = 0; q < U; ++q) {
         // Unpredicated gathers: empty slots carry k = 0 (row 0) and lanes past ld read into the
         // next row (the tables are padded); both only meet u = 0 / v~ = 0 below.
-        const uint32_t off = (uint32_t)__shfl_sync(kFull, my.x, gbase + (q << SHIFT)) * (uint32_t)ld;
-        kr[q] = ldg4(kb + off);
-        if (FINAL) mr[q] = ldg4(mb + off);
+        const uint32_t row = (uint32_t)__shfl_sync(kFull, my.x, gbase + (q << SHIFT)) * ld4;
+        kr[q] = ldg4_keep(kb + row, keep);
+        if (FINAL) mr[q] = ldg4_keep(mb + row, keep);
         if (MAKE_MASK && eb + q < n && act) ubits |= under_bits(kr[q]);
       }
       const bool myvalid = eb + qm < n;
       const float c = __int_as_float(my.y);
       // next step's nonzero (and, once per round, the next round's document) while K~ is in flight
       my = make_int2(0, 0);
-      if (eb + U + qm < n) my = __ldg(ent2 + b + eb + U + qm);
+      if (eb + U + qm < n) my = WMD_LDS(ent2 + b + eb + U + qm);
       if (!prefetched) {
         prefetched = true;
         body(jn, bn, nn_, myn, unx, mbn);
@@ -355,8 +387,9 @@ __global__ void __launch_bounds__(256, FINAL ? 2 : 3) sinkhorn_pass_kernel(
       }
     } else {
       float4 un;
-      un.x = r.x > 0.f ? r.x / acc.x : 0.f; un.y = r.y > 0.f ? r.y / acc.y : 0.f;
-      un.z = r.z > 0.f ? r.z / acc.z : 0.f; un.w = r.w > 0.f ? r.w / acc.w : 0.f;
+      // padded rows (r = 0) divide by 1, not by their garbage acc: no IEEE slow path
+      un.x = r.x / (r.x > 0.f ? acc.x : 1.f); un.y = r.y / (r.y > 0.f ? acc.y : 1.f);
+      un.z = r.z / (r.z > 0.f ? acc.z : 1.f); un.w = r.w / (r.w > 0.f ? acc.w : 1.f);
       const float vcap = (float)n * vmax * kUnderScale;  // bound on the underflowed terms
       float mx = 0.f, mn = FLT_MAX;
 #define WMD_ROW(c, bit)                                                   \
@@ -379,7 +412,7 @@ __global__ void __launch_bounds__(256, FINAL ? 2 : 3) sinkhorn_pass_kernel(
       } else if (sub == 0 && j >= 0) {
         flags[j] |= kFlagFp32Range;
       }
-      if (act && j >= 0) *reinterpret_cast<float4*>(u_out + j * ld + sub * 4) = un;
+      if (act && j >= 0) WMD_STS(reinterpret_cast<float4*>(u_out + j * ld) + sub, un);
     }
     j = jn; b = bn; n = nn_; my = myn; u = unx; mbits = mbn;
   }
@@ -521,7 +554,7 @@ int mask_words_for(int ld) { return (ld + 31) / 32; }
 void launch_sddmm_spmm_iter(const int32_t* order, const int32_t* doc_ptr, const Entry* ent, int64_t N,
                             const float* Kt, int ld, int v_r, const float* rpad, const float* u_in,
                             float* u_out, uint32_t* umask, uint8_t* flags, cudaStream_t st) {
-  const unsigned grid = pass_grid(N, ld, 3);
+  const unsigned grid = pass_grid(N, ld, PASS_BLOCKS_PER_SM);
   const int mw = mask_words_for(ld);
   // the first iteration records the underflow row masks, later ones read them
   if (u_in == nullptr) {
@@ -571,10 +604,5 @@ void launch_fallback_fp64(const float* Mt, const float* colmin, int ld, const fl
 void launch_check_finite(const float* x, int64_t n, int32_t* bad, cudaStream_t st) {
   check_finite_kernel<<<148 * 4, 256, 0, st>>>(x, n, bad);
 }
-
-bool fused_supported(int, int64_t) { return false; }
-void launch_sinkhorn_fused(const int32_t*, const Entry*, int64_t, const float*, const float*, int,
-                           int, const float*, int, float*, uint8_t*, int32_t*, int32_t*, int64_t,
-                           cudaStream_t) {}
 
 }  // namespace wmd

@@ -17,7 +17,8 @@ from typing import Optional
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libwmd_b200.so")
+# WMD_LIB overrides the library path (performance experiments with build variants only)
+LIB_PATH = os.environ.get("WMD_LIB") or os.path.join(_PKG, "libwmd_b200.so")
 
 WMD_MAX_VR = 128
 

@@ -33,7 +33,12 @@ def run_gpu(W, E, cp, ri, va, q, w, lam, iters, path=1, fallback=True, out="host
         N = cp.shape[0] - 1
         if out == "host":
             d = np.empty(N, np.float32)
-            W.wmd_query(h, q, w, lam, iters, d)
+            try:
+                W.wmd_query(h, q, w, lam, iters, d)
+            except W.WmdError as e:
+                if path == W.WMD_PATH_FUSED and "fused path does not support" in str(e):
+                    pytest.skip(f"fused path: unsupported shape ({e})")
+                raise
         else:
             import torch
             t = torch.empty(N, dtype=torch.float32, device="cuda:0")
@@ -57,7 +62,7 @@ def assert_parity(g, o, what=""):
                            f"gpu={g[bad[:5]]} oracle={o[bad[:5]]}")
 
 
-PATHS = [1]  # per-iteration SDDMM_SpMM path; the fused path is added in test_fused_gpu.py
+PATHS = [1, 2]  # WMD_PATH_PER_ITER (one SDDMM_SpMM launch per iteration), WMD_PATH_FUSED (NEXT-1)
 
 
 # ------------------------------------------------------------------ full configs, small
@@ -357,6 +362,7 @@ def test_device_resident_inputs(W):
     Ed = torch.from_numpy(wl.E).cuda()
     h = W.wmd_create(Ed, device=0)
     try:
+        W.wmd_set_option(h, W.WMD_OPT_PATH, W.WMD_PATH_PER_ITER)  # run_gpu's default path
         W.wmd_set_targets(h, torch.from_numpy(wl.col_ptr).cuda(), torch.from_numpy(wl.row_idx).cuda(),
                           torch.from_numpy(wl.val).cuda())
         d = np.empty(wl.N, np.float32)
@@ -420,3 +426,35 @@ def test_timing_stats(W):
     assert st["queries"] == 3 and st["timing_valid"] == 1
     assert st["iter_launches"] == 45
     assert st["build_ms"] > 0 and st["iter_ms"] > 0 and st["query_ms"] >= st["iter_ms"]
+
+
+def test_auto_path_selection_and_cross_path_agreement(W):
+    """AUTO runs the fused kernel when the shape fits (tweet-like docs, v_r <= 64), else the
+    per-iteration kernel; both agree with each other to the parity tolerance."""
+    wl = synth.make_workload("tweet")
+    q, w = wl.queries[0]
+    res = {}
+    for path in (W.WMD_PATH_AUTO, W.WMD_PATH_PER_ITER, W.WMD_PATH_FUSED):
+        h = W.wmd_create(wl.E)
+        try:
+            W.wmd_set_option(h, W.WMD_OPT_PATH, path)
+            W.wmd_set_targets(h, wl.col_ptr, wl.row_idx, wl.val)
+            d = np.empty(wl.N, np.float32)
+            W.wmd_query(h, q, w, wl.cfg.lam, wl.cfg.iters, d)
+            res[path] = (d, W.wmd_get_stats(h)["last_path"])
+        finally:
+            W.wmd_destroy(h)
+    assert res[W.WMD_PATH_AUTO][1] == W.WMD_PATH_FUSED
+    assert np.array_equal(res[W.WMD_PATH_AUTO][0], res[W.WMD_PATH_FUSED][0])
+    a, b = res[W.WMD_PATH_PER_ITER][0].astype(np.float64), res[W.WMD_PATH_FUSED][0].astype(np.float64)
+    assert np.all(np.abs(a - b) <= 2e-4 * np.abs(a) + 2e-5)
+    # long documents exceed the fused kernel's register budget: AUTO falls back per iteration
+    cp, ri, va = synth.csc_from_lists([{int(k): 1.0 / 100 for k in range(100)}], wl.cfg.V)
+    h = W.wmd_create(wl.E)
+    try:
+        W.wmd_set_targets(h, cp, ri, va)
+        d = np.empty(1, np.float32)
+        W.wmd_query(h, q, w, wl.cfg.lam, wl.cfg.iters, d)
+        assert W.wmd_get_stats(h)["last_path"] == W.WMD_PATH_PER_ITER
+    finally:
+        W.wmd_destroy(h)
