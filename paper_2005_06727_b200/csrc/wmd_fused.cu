@@ -109,24 +109,29 @@ __global__ void __launch_bounds__(256, fused_blocks_per_sm<LD, NW>()) sinkhorn_f
 #pragma unroll
       for (int c = 0; c < CPL; ++c) su[lane + 32 * c] = u[c];
       __syncwarp();
-      float s[NW];
+      // four independent FMA chains per dot product (FMA latency, few resident warps)
+      float s[NW], sp[NW][4];
 #pragma unroll
-      for (int w = 0; w < NW; ++w) s[w] = 0.f;
+      for (int w = 0; w < NW; ++w) sp[w][0] = sp[w][1] = sp[w][2] = sp[w][3] = 0.f;
 #pragma unroll
       for (int q = 0; q < LD / 4; ++q) {
         const float4 uu = *reinterpret_cast<const float4*>(su + 4 * q);
 #pragma unroll
         for (int w = 0; w < NW; ++w) {
-          s[w] = fmaf(kr[w][4 * q], uu.x, s[w]);
-          s[w] = fmaf(kr[w][4 * q + 1], uu.y, s[w]);
-          s[w] = fmaf(kr[w][4 * q + 2], uu.z, s[w]);
-          s[w] = fmaf(kr[w][4 * q + 3], uu.w, s[w]);
+          sp[w][0] = fmaf(kr[w][4 * q], uu.x, sp[w][0]);
+          sp[w][1] = fmaf(kr[w][4 * q + 1], uu.y, sp[w][1]);
+          sp[w][2] = fmaf(kr[w][4 * q + 2], uu.z, sp[w][2]);
+          sp[w][3] = fmaf(kr[w][4 * q + 3], uu.w, sp[w][3]);
         }
       }
+#pragma unroll
+      for (int w = 0; w < NW; ++w) s[w] = (sp[w][0] + sp[w][1]) + (sp[w][2] + sp[w][3]);
       uint32_t smin_b = 0xffffffffu, vmax_b = 0u, umu_b = 0u;
 #pragma unroll
       for (int w = 0; w < NW; ++w) {
-        vt[w] = ve[w] ? ce[w] / s[w] : 0.f;
+        // empty slots divide 1 by 1 (a zero numerator would take the IEEE slow path)
+        vt[w] = (ve[w] ? ce[w] : 1.f) / (ve[w] ? s[w] : 1.f);
+        if (!ve[w]) vt[w] = 0.f;
         if (ve[w]) smin_b = min(smin_b, __float_as_uint(s[w]));
         vmax_b = max(vmax_b, __float_as_uint(vt[w]));
       }
@@ -144,26 +149,29 @@ __global__ void __launch_bounds__(256, fused_blocks_per_sm<LD, NW>()) sinkhorn_f
 #pragma unroll
       for (int w = 0; w < NW; ++w) sv[lane + 32 * w] = vt[w];
       __syncwarp();
-      float acc[CPL];
+      float acc[CPL], ap[CPL][4];
 #pragma unroll
-      for (int c = 0; c < CPL; ++c) acc[c] = 0.f;
+      for (int c = 0; c < CPL; ++c) ap[c][0] = ap[c][1] = ap[c][2] = ap[c][3] = 0.f;
 #pragma unroll
       for (int e4 = 0; e4 < NMAX / 4; ++e4) {
         const float4 vv = *reinterpret_cast<const float4*>(sv + 4 * e4);
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
-          acc[c] = fmaf(kc[c][4 * e4], vv.x, acc[c]);
-          acc[c] = fmaf(kc[c][4 * e4 + 1], vv.y, acc[c]);
-          acc[c] = fmaf(kc[c][4 * e4 + 2], vv.z, acc[c]);
-          acc[c] = fmaf(kc[c][4 * e4 + 3], vv.w, acc[c]);
+          ap[c][0] = fmaf(kc[c][4 * e4], vv.x, ap[c][0]);
+          ap[c][1] = fmaf(kc[c][4 * e4 + 1], vv.y, ap[c][1]);
+          ap[c][2] = fmaf(kc[c][4 * e4 + 2], vv.z, ap[c][2]);
+          ap[c][3] = fmaf(kc[c][4 * e4 + 3], vv.w, ap[c][3]);
         }
       }
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) acc[c] = (ap[c][0] + ap[c][1]) + (ap[c][2] + ap[c][3]);
       const float vcap = (float)n * __uint_as_float(vmax_b) * kUnderScale;
       uint32_t umax_b = 0u, umin_b = 0xffffffffu;
       float un[CPL];
 #pragma unroll
       for (int c = 0; c < CPL; ++c) {
-        un[c] = r[c] / (r[c] > 0.f ? acc[c] : 1.f);
+        un[c] = (r[c] > 0.f ? r[c] : 1.f) / (r[c] > 0.f ? acc[c] : 1.f);  // padded rows: 1/1
+        if (!(r[c] > 0.f)) un[c] = 0.f;
         if (r[c] > 0.f) {
           bad |= under[c] && vcap > acc[c];
           umax_b = max(umax_b, __float_as_uint(un[c]));

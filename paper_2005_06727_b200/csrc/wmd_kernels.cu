@@ -326,11 +326,13 @@ __global__ void __launch_bounds__(256, FINAL ? 2 : PASS_BLOCKS_PER_SM) sinkhorn_
 #pragma unroll
       for (int q = 0; q < U; ++q) p[q] = dot4(kr[q], u);
       const float sv = transpose_reduce<G, U>(p, sub);
-      float vt = 0.f;
+      // empty slots divide 1 by 1 (a zero numerator would take the IEEE division slow path)
+      float vt = (myvalid ? c : 1.f) / (myvalid ? sv : 1.f);
       if (myvalid) {
-        vt = c / sv;
         smin = fminf(smin, sv);
         vmax = fmaxf(vmax, vt);
+      } else {
+        vt = 0.f;
       }
       if (FINAL) {
         float t[U];
@@ -387,9 +389,11 @@ __global__ void __launch_bounds__(256, FINAL ? 2 : PASS_BLOCKS_PER_SM) sinkhorn_
       }
     } else {
       float4 un;
-      // padded rows (r = 0) divide by 1, not by their garbage acc: no IEEE slow path
-      un.x = r.x / (r.x > 0.f ? acc.x : 1.f); un.y = r.y / (r.y > 0.f ? acc.y : 1.f);
-      un.z = r.z / (r.z > 0.f ? acc.z : 1.f); un.w = r.w / (r.w > 0.f ? acc.w : 1.f);
+      // padded rows (r = 0) compute 1/1, not 0/garbage: a zero numerator takes the IEEE slow path
+#define WMD_UDIV(c) \
+      un.c = (r.c > 0.f ? r.c : 1.f) / (r.c > 0.f ? acc.c : 1.f); if (!(r.c > 0.f)) un.c = 0.f;
+      WMD_UDIV(x) WMD_UDIV(y) WMD_UDIV(z) WMD_UDIV(w)
+#undef WMD_UDIV
       const float vcap = (float)n * vmax * kUnderScale;  // bound on the underflowed terms
       float mx = 0.f, mn = FLT_MAX;
 #define WMD_ROW(c, bit)                                                   \
