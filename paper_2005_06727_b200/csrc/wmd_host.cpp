@@ -86,7 +86,7 @@ struct wmd_handle {
   DevBuf<int32_t> order;     // documents sorted by length (stable counting sort)
   DevBuf<Entry> ent;
   int64_t N = 0, nnz = 0, max_doc_nnz = 0;
-  int64_t n_short = 0;       // documents with <= 32 nonzeros (prefix of `order`)
+  std::vector<int64_t> len_prefix;  // [L] = documents with fewer than L nonzeros (host)
   // per-query device state
   DevBuf<int32_t> sel;       // WMD_MAX_VR
   DevBuf<float> rpad;        // WMD_MAX_VR (zero padded to ld)
@@ -439,8 +439,8 @@ wmd_status wmd_set_targets(wmd_handle* h, const int64_t* col_ptr, const int32_t*
   std::vector<int64_t> cnt(mx + 2, 0);
   for (int64_t j = 0; j < N; ++j) cnt[col_ptr[j + 1] - col_ptr[j] + 1]++;
   for (int64_t L = 1; L < mx + 2; ++L) cnt[L] += cnt[L - 1];
-  // cnt[L] = number of documents shorter than L; documents with <= 32 nonzeros come first
-  const int64_t n_short = cnt[std::min<int64_t>(mx, 32) + 1];
+  // cnt[L] = number of documents shorter than L (kept: length buckets of the sorted order)
+  std::vector<int64_t> len_prefix = cnt;
   std::vector<int32_t> ord(N);
   for (int64_t j = 0; j < N; ++j) ord[cnt[col_ptr[j + 1] - col_ptr[j]]++] = (int32_t)j;
   std::vector<Entry> en(nnz);
@@ -459,7 +459,7 @@ wmd_status wmd_set_targets(wmd_handle* h, const int64_t* col_ptr, const int32_t*
   h->N = N;
   h->nnz = nnz;
   h->max_doc_nnz = mx;
-  h->n_short = n_short;
+  h->len_prefix.swap(len_prefix);
   h->has_targets = true;
   return WMD_OK;
 }
@@ -526,9 +526,10 @@ wmd_status wmd_query(wmd_handle* h, const int32_t* query_ids, const float* query
     return fail(h, WMD_ERR_INVALID_ARGUMENT, "fused path does not support ld=%d, max doc nnz=%lld", ld,
                 (long long)h->max_doc_nnz);
   if (fused) {
-    wmd::launch_sinkhorn_fused(h->order.p, h->doc_ptr.p, h->ent.p, N, h->n_short, h->Kt.p, h->Mt.p, ld,
-                               v_r, h->rpad.p, iters, dist, h->flags.p, h->flagged.p, h->counters.p, st);
-    const int64_t nl = (h->n_short > 0) + (N > h->n_short);
+    wmd::launch_sinkhorn_fused(h->order.p, h->doc_ptr.p, h->ent.p, N, h->len_prefix.data(),
+                               h->max_doc_nnz, h->Kt.p, h->Mt.p, ld, v_r, h->rpad.p, iters, dist,
+                               h->flags.p, h->flagged.p, h->counters.p, st);
+    const int64_t nl = wmd::fused_launch_count(h->len_prefix.data(), h->max_doc_nnz, N);
     launches += nl;
     h->st.iter_launches += nl;
     if (pe) { CK(h, cudaEventRecord(pe->ev[2], st)); CK(h, cudaEventRecord(pe->ev[3], st)); }

@@ -48,13 +48,15 @@ void launch_final_wmd(const int32_t* order, const int32_t* doc_ptr, const Entry*
 
 // --- NEXT-1: all iterations + final step in one launch (wmd_fused.cu) ------------------------
 // Returns false if the shape is not supported by the fused kernel (the caller then uses the
-// per-iteration path). `n_short` = number of documents with <= 32 nonzeros (a prefix of the
-// length-sorted `order`).
+// per-iteration path). `len_prefix` (host, max_len + 2 entries): len_prefix[L] = number of
+// documents with fewer than L nonzeros, i.e. bucket boundaries in the length-sorted `order`.
 bool fused_supported(int ld, int64_t max_doc_nnz);
 void launch_sinkhorn_fused(const int32_t* order, const int32_t* doc_ptr, const Entry* ent, int64_t N,
-                           int64_t n_short, const float* Kt, const float* Mt, int ld, int v_r,
-                           const float* rpad, int iters, float* dist, uint8_t* flags,
-                           int32_t* flagged_list, int32_t* flagged_count, cudaStream_t st);
+                           const int64_t* len_prefix, int64_t max_len, const float* Kt,
+                           const float* Mt, int ld, int v_r, const float* rpad, int iters,
+                           float* dist, uint8_t* flags, int32_t* flagged_list,
+                           int32_t* flagged_count, cudaStream_t st);
+int fused_launch_count(const int64_t* len_prefix, int64_t max_len, int64_t N);
 
 // --- a6: FP64 re-run of flagged documents (no CPU fallback) --------------------------------
 constexpr int kFallbackBlocks = 296;  // 2 per SM
