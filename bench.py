@@ -292,16 +292,23 @@ def main():
                 "share_of_step": st["iter_ms"] / max(st["query_ms"], 1e-9),
             }
         else:
-            t_launch = st["iter_ms"] / 1e3 / max(1, st["iter_launches"])
-            flops = 4.0 * v_r * nnz_l * (cfg.iters + 1)           # 2 FMAs per nnz-update
+            # fused path: all iterations + final in one pass (one launch per length bucket);
+            # the roofline is over the whole fused phase of the step
+            t_phase = st["iter_ms"] / 1e3 / args.steps
+            flops = 4.0 * v_r * nnz_l * (cfg.iters + 1)           # 2 FMAs per (nnz, row) per pass
             clk = peaks.get("sm_max_mhz", 1965.0)
             peak_tf = 148 * 128 * 2 * clk * 1e6 / 1e12
             roofline = {
                 "kernel": "sinkhorn_fused", "bound": "alu",
-                "achieved": flops / t_launch / 1e12, "peak": peak_tf, "unit": "TFLOP/s",
-                "frac": flops / t_launch / 1e12 / peak_tf,
-                "peak_source": f"148 SMs x 128 FP32 FMA/clk x 2 x {clk:.0f} MHz (DESIGN.md §5)",
-                "launch_ms": t_launch * 1e3, "traffic": None,
+                "achieved": flops / t_phase / 1e12, "peak": peak_tf, "unit": "TFLOP/s",
+                "frac": flops / t_phase / 1e12 / peak_tf,
+                "peak_source": f"derived: 148 SMs x 128 FP32 FMA/clk x 2 flops x {clk:.0f} MHz "
+                               "(sm_max_mhz of MEASURED_PEAKS.json; DESIGN.md §5)",
+                "algorithmic_flops_per_step": flops,
+                "phase_ms": t_phase * 1e3,
+                "launches_per_step": st["iter_launches"] / args.steps,
+                "l2_gather_bytes_per_step": 2 * 4 * v_r * nnz_l,  # K~ and M rows, once
+                "traffic": None,
                 "share_of_step": st["iter_ms"] / max(st["query_ms"], 1e-9),
             }
         line = {

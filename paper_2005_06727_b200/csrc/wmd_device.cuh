@@ -52,6 +52,16 @@ __device__ __forceinline__ float ldg_keep(const float* p, uint64_t pol) {
 #endif
 }
 
+// Fast reciprocal (MUFU.RCP, relative error <= 2^-23, subnormal input -> inf). Used where the
+// input is either normal or the document is flagged anyway: s_e >= u_{i*} (the column-minimum
+// row has K~ = 1) is normal whenever u is, and a subnormal acc_i yields u_i = inf, which the
+// range check rejects.
+__device__ __forceinline__ float rcp_fast(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // Exact power-of-two gauge factor 2^-floor((e_max + e_min)/2) from the bit patterns of the
 // largest and smallest (positive, normal) entries: the biased exponent is bits >> 23.
 __device__ __forceinline__ float gauge_scale(uint32_t max_bits, uint32_t min_bits) {

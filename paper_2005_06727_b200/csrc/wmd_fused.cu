@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(kFusedThreads, fused_min_blocks<LD, NE>()) sin
 #pragma unroll
       for (int w = 0; w < NW; ++w) {
         const float s = (sp[w][0] + sp[w][1]) + (sp[w][2] + sp[w][3]);
-        vt[w] = ve[w] ? ce[w] * __frcp_rn(s) : 0.f;
+        vt[w] = ve[w] ? ce[w] * rcp_fast(s) : 0.f;
         if (ve[w]) smin_b = min(smin_b, __float_as_uint(s));
         vmax_b = max(vmax_b, __float_as_uint(vt[w]));
       }
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(kFusedThreads, fused_min_blocks<LD, NE>()) sin
 #pragma unroll
       for (int c = 0; c < CPL; ++c) {
         const float acc = (ap[c][0] + ap[c][1]) + (ap[c][2] + ap[c][3]);
-        un[c] = r[c] > 0.f ? r[c] * __frcp_rn(acc) : 0.f;
+        un[c] = r[c] > 0.f ? r[c] * rcp_fast(acc) : 0.f;
         if (r[c] > 0.f) {
           bad_l |= under[c] && vcap > acc;
           umax_b = max(umax_b, __float_as_uint(un[c]));
