@@ -3,8 +3,18 @@
 The compute path lives in libwmd_b200.so (CUDA kernels for sm_100a behind the C ABI in
 include/wmd.h); `wmd` is the thin ctypes binding and `sharded` the multi-GPU driver
 (doc-column shards + one NCCL all-gather of the distances).
-"""
-from . import wmd  # noqa: F401  (raises if the CUDA library is missing: no CPU fallback)
-from .wmd import Engine, WmdError  # noqa: F401
 
-__all__ = ["wmd", "Engine", "WmdError"]
+`wmd` is imported on first use (PEP 562), so `paper_2005_06727_b200.build` can run on a clean
+tree; importing `wmd` raises if the CUDA library is missing (no CPU fallback).
+"""
+import importlib
+
+__all__ = ["wmd", "sharded", "Engine", "WmdError"]
+
+
+def __getattr__(name):
+    if name in ("wmd", "sharded"):
+        return importlib.import_module(f".{name}", __name__)
+    if name in ("Engine", "WmdError"):
+        return getattr(importlib.import_module(".wmd", __name__), name)
+    raise AttributeError(name)
