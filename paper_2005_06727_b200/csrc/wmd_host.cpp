@@ -90,7 +90,9 @@ struct wmd_handle {
   // per-query device state
   DevBuf<int32_t> sel;       // WMD_MAX_VR
   DevBuf<float> rpad;        // WMD_MAX_VR (zero padded to ld)
-  DevBuf<float> Kt, Mt;      // V * ld: K~ and M (FP32, vocab-major)
+  DevBuf<float> Kt;          // V * ld: K~ (FP32, vocab-major; per-iteration path only)
+  DevBuf<float> Mx;          // V * (ld + 4): M rows + m_k (FP32, vocab-major)
+  bool kt_valid = false;     // Kt holds the last query's K~
   DevBuf<float> colmin;      // V
   DevBuf<float> ua, ub;      // N * ld
   DevBuf<uint32_t> umask;    // N * ceil(ld/32): rows with an underflowed K~ entry, per doc
@@ -371,7 +373,7 @@ void wmd_destroy(wmd_handle* h) {
     if (h->stage_ev[s]) cudaEventDestroy(h->stage_ev[s]);
   }
   h->E.release(); h->doc_ptr.release(); h->order.release(); h->ent.release(); h->sel.release(); h->rpad.release();
-  h->Kt.release(); h->Mt.release(); h->colmin.release(); h->ua.release(); h->ub.release(); h->umask.release();
+  h->Kt.release(); h->Mx.release(); h->colmin.release(); h->ua.release(); h->ub.release(); h->umask.release();
   h->dist_tmp.release(); h->flags.release(); h->flagged.release(); h->counters.release();
   h->fb_scratch.release();
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
@@ -481,8 +483,13 @@ wmd_status wmd_query(wmd_handle* h, const int32_t* query_ids, const float* query
   const int32_t v_r = n, ld = round_up8(n);
   const int64_t N = h->N;
   // +128 floats: the pass kernels gather unpredicated float4s up to 4*32 floats past a row
-  CK(h, h->Kt.ensure((size_t)h->V * ld + 128));
-  CK(h, h->Mt.ensure((size_t)h->V * ld + 128));
+  const bool fused = (h->opt_path == WMD_PATH_FUSED || h->opt_path == WMD_PATH_AUTO) &&
+                     wmd::fused_supported(ld, h->max_doc_nnz);
+  if (h->opt_path == WMD_PATH_FUSED && !fused)
+    return fail(h, WMD_ERR_INVALID_ARGUMENT, "fused path does not support ld=%d, max doc nnz=%lld", ld,
+                (long long)h->max_doc_nnz);
+  if (!fused) CK(h, h->Kt.ensure((size_t)h->V * ld + 128));
+  CK(h, h->Mx.ensure((size_t)h->V * (ld + 4) + 128));
   CK(h, h->ua.ensure((size_t)N * ld));
   CK(h, h->ub.ensure((size_t)N * ld));
   CK(h, h->umask.ensure((size_t)N * ((ld + 31) / 32)));
@@ -515,19 +522,15 @@ wmd_status wmd_query(wmd_handle* h, const int32_t* query_ids, const float* query
   }
   int64_t launches = 0;
   // a2: M, K~
-  wmd::launch_build_ktilde(h->E.p, h->V, h->d, h->sel.p, v_r, ld, lambda, h->Kt.p, h->Mt.p,
-                           h->colmin.p, st);
+  wmd::launch_build_ktilde(h->E.p, h->V, h->d, h->sel.p, v_r, ld, lambda, fused ? nullptr : h->Kt.p,
+                           h->Mx.p, h->colmin.p, st);
+  h->kt_valid = !fused;
   ++launches;
   if (pe) CK(h, cudaEventRecord(pe->ev[1], st));
 
-  const bool fused = (h->opt_path == WMD_PATH_FUSED || h->opt_path == WMD_PATH_AUTO) &&
-                     wmd::fused_supported(ld, h->max_doc_nnz);
-  if (h->opt_path == WMD_PATH_FUSED && !fused)
-    return fail(h, WMD_ERR_INVALID_ARGUMENT, "fused path does not support ld=%d, max doc nnz=%lld", ld,
-                (long long)h->max_doc_nnz);
   if (fused) {
     wmd::launch_sinkhorn_fused(h->order.p, h->doc_ptr.p, h->ent.p, N, h->len_prefix.data(),
-                               h->max_doc_nnz, h->Kt.p, h->Mt.p, ld, v_r, h->rpad.p, iters, dist,
+                               h->max_doc_nnz, h->Mx.p, ld, v_r, h->rpad.p, lambda, iters, dist,
                                h->flags.p, h->flagged.p, h->counters.p, st);
     const int64_t nl = wmd::fused_launch_count(h->len_prefix.data(), h->max_doc_nnz, N);
     launches += nl;
@@ -549,7 +552,7 @@ wmd_status wmd_query(wmd_handle* h, const int32_t* query_ids, const float* query
     h->st.iter_launches += iters;
     if (pe) CK(h, cudaEventRecord(pe->ev[2], st));
     // a5
-    wmd::launch_final_wmd(h->order.p, h->doc_ptr.p, h->ent.p, N, h->Kt.p, h->Mt.p, ld, v_r, h->rpad.p, u_in,
+    wmd::launch_final_wmd(h->order.p, h->doc_ptr.p, h->ent.p, N, h->Kt.p, h->Mx.p, ld, v_r, h->rpad.p, u_in,
                           h->umask.p, dist, h->flags.p, h->flagged.p, h->counters.p, st);
     ++launches;
     if (pe) CK(h, cudaEventRecord(pe->ev[3], st));
@@ -559,7 +562,7 @@ wmd_status wmd_query(wmd_handle* h, const int32_t* query_ids, const float* query
   }
   // a6: FP64 re-run of flagged documents (device-side list; zero-cost when empty)
   if (h->opt_fallback) {
-    wmd::launch_fallback_fp64(h->Mt.p, h->colmin.p, ld, h->rpad.p, v_r, (double)lambda, iters, h->doc_ptr.p,
+    wmd::launch_fallback_fp64(h->Mx.p, h->colmin.p, ld, h->rpad.p, v_r, (double)lambda, iters, h->doc_ptr.p,
                               h->ent.p, h->flagged.p, h->counters.p, h->fb_scratch.p, h->max_doc_nnz, dist,
                               h->flags.p, h->counters.p + 1, h->counters.p + 2, st);
     ++launches;
@@ -644,9 +647,12 @@ wmd_status wmd_read_kernel(wmd_handle* h, int64_t k0, int64_t count, float* ktil
   if (h->st.queries == 0) return fail(h, WMD_ERR_STATE, "no query yet");
   DeviceGuard g(h->device);
   CK(h, cudaStreamSynchronize(h->stream));
-  const size_t row = (size_t)h->ld;
+  const size_t row = (size_t)h->ld, rowx = row + 4;
+  if (ktilde && !h->kt_valid)
+    return fail(h, WMD_ERR_STATE, "K~ table not built by the last query (fused path builds M only)");
   if (ktilde) CK(h, cudaMemcpy(ktilde, h->Kt.p + k0 * row, count * row * 4, cudaMemcpyDeviceToHost));
-  if (m) CK(h, cudaMemcpy(m, h->Mt.p + k0 * row, count * row * 4, cudaMemcpyDeviceToHost));
+  if (m && count > 0)
+    CK(h, cudaMemcpy2D(m, row * 4, h->Mx.p + k0 * rowx, rowx * 4, row * 4, count, cudaMemcpyDeviceToHost));
   if (colmin) CK(h, cudaMemcpy(colmin, h->colmin.p + k0, count * 4, cudaMemcpyDeviceToHost));
   return WMD_OK;
 }

@@ -30,8 +30,10 @@ struct QueryDev {
 };
 
 // --- a2: distance + column-rescaled kernel build -------
+// Mx: V rows of ld + 4 floats [M_k0 .. M_k,ld-1 (zero beyond v_r), m_k = min_i M_ik, 0, 0, 0].
+// Kt (V x ld, K~ = exp(-lambda (M - m))) is written only when non-null (per-iteration path).
 void launch_build_ktilde(const float* E, int64_t V, int d, const int32_t* sel, int v_r, int ld,
-                         float lambda, float* Kt, float* Mt, float* colmin, cudaStream_t st);
+                         float lambda, float* Kt, float* Mx, float* colmin, cudaStream_t st);
 
 // --- a4: one fused SDDMM_SpMM iteration for all documents ------------
 // u_in == nullptr: first iteration with the constant u0 = 1/x0 = v_r.
@@ -52,16 +54,16 @@ void launch_final_wmd(const int32_t* order, const int32_t* doc_ptr, const Entry*
 // documents with fewer than L nonzeros, i.e. bucket boundaries in the length-sorted `order`.
 bool fused_supported(int ld, int64_t max_doc_nnz);
 void launch_sinkhorn_fused(const int32_t* order, const int32_t* doc_ptr, const Entry* ent, int64_t N,
-                           const int64_t* len_prefix, int64_t max_len, const float* Kt,
-                           const float* Mt, int ld, int v_r, const float* rpad, int iters,
-                           float* dist, uint8_t* flags, int32_t* flagged_list,
-                           int32_t* flagged_count, cudaStream_t st);
+                           const int64_t* len_prefix, int64_t max_len, const float* Mx, int ld,
+                           int v_r, const float* rpad, float lambda, int iters, float* dist,
+                           uint8_t* flags, int32_t* flagged_list, int32_t* flagged_count,
+                           cudaStream_t st);
 int fused_launch_count(const int64_t* len_prefix, int64_t max_len, int64_t N);
 
 // --- a6: FP64 re-run of flagged documents (no CPU fallback) --------------------------------
 constexpr int kFallbackBlocks = 296;  // 2 per SM
 size_t fallback_scratch_bytes(int64_t max_doc_nnz);
-void launch_fallback_fp64(const float* Mt, const float* colmin, int ld, const float* rpad, int v_r,
+void launch_fallback_fp64(const float* Mx, const float* colmin, int ld, const float* rpad, int v_r,
                           double lambda, int iters, const int32_t* doc_ptr, const Entry* ent,
                           const int32_t* flagged_list, const int32_t* flagged_count,
                           double* scratch, int64_t max_doc_nnz, float* dist, uint8_t* flags,

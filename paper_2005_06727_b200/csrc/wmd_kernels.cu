@@ -77,7 +77,8 @@ constexpr float kUnderScale = 0x1p-133f;  // 2^-149 / 2^-16
 //        M_ik  = sqrt(sum_t (E[sel_i,t] - E[k,t])^2)        (direct difference so
 //                                                             M_{i,sel_i} == 0 exactly)
 //        m_k   = min_i M_ik
-//        K~_ki = expf(-lambda (M_ik - m_k)),  and M itself                (vocab-major, ld floats)
+//        K~_ki = expf(-lambda (M_ik - m_k))   (vocab-major, ld floats; per-iteration path only)
+//        Mx_k  = [M_k0 .. M_k,ld-1, m_k, 0, 0, 0] (vocab-major, ld + 4 floats; zero beyond v_r)
 // Block: 256 threads, 64 vocabulary words x all query rows (32-row tiles), d staged through
 // shared memory in chunks of 32. Thread micro-tile: 2 rows x 4 words, float4 smem reads.
 // Bound: FP32 issue (2 flops per (i,k,t) triple, PAPER.md:260 counts 3) vs reading E once.
@@ -88,7 +89,7 @@ __global__ void __launch_bounds__(256) build_ktilde_kernel(const float* __restri
                                                            int d, const int32_t* __restrict__ sel,
                                                            int v_r, int ld, float lambda,
                                                            float* __restrict__ Kt,
-                                                           float* __restrict__ Mt,
+                                                           float* __restrict__ Mx,
                                                            float* __restrict__ colmin) {
   extern __shared__ __align__(16) float smem[];
   float* Qs = smem;                          // [BK_TI][BK_STR]
@@ -161,14 +162,13 @@ __global__ void __launch_bounds__(256) build_ktilde_kernel(const float* __restri
     for (int i = lane; i < v_r; i += 32) mn = fminf(mn, mrow[i]);
 #pragma unroll
     for (int off = 16; off; off >>= 1) mn = fminf(mn, __shfl_xor_sync(kFull, mn, off));
-    for (int i = lane; i < ld; i += 32) {
-      float kt = 0.f, m = 0.f;
-      if (i < v_r) {
-        m = mrow[i];
-        kt = expf(-lambda * (m - mn));
-      }
-      Kt[k * ld + i] = kt;
-      Mt[k * ld + i] = m;
+    const int ldx = ld + 4;  // Mx row: M_k0..M_k,ld-1 (zero beyond v_r), m_k, 3 zeros
+    for (int i = lane; i < ldx; i += 32) {
+      float m = 0.f;
+      if (i < v_r) m = mrow[i];
+      else if (i == ld) m = mn;
+      Mx[k * ldx + i] = m;
+      if (Kt && i < ld) Kt[k * ld + i] = i < v_r ? expf(-lambda * (m - mn)) : 0.f;
     }
     if (lane == 0) colmin[k] = mn;
   }
@@ -256,6 +256,7 @@ __global__ void __launch_bounds__(256, FINAL ? 2 : PASS_BLOCKS_PER_SM) sinkhorn_
   const uint32_t ld4 = (uint32_t)ld >> 2;           // row stride in float4s
   const float4* kb = reinterpret_cast<const float4*>(Kt) + sub;  // this lane's float4 of a K~ row
   const float4* mb = FINAL ? reinterpret_cast<const float4*>(Mt) + sub : nullptr;  // ... of an M row
+  const uint32_t ldx4 = ld4 + 1;                    // Mx row stride in float4s (ld + 4 floats)
   const uint64_t keep = l2_evict_last_policy();
 
   // Round structure: in each round the warp's NG groups take NG consecutive documents of the
@@ -308,9 +309,9 @@ __global__ void __launch_bounds__(256, FINAL ? 2 : PASS_BLOCKS_PER_SM) sinkhorn_
       for (int q = 0; q < U; ++q) {
         // Unpredicated gathers: empty slots carry k = 0 (row 0) and lanes past ld read into the
         // next row (the tables are padded); both only meet u = 0 / v~ = 0 below.
-        const uint32_t row = (uint32_t)__shfl_sync(kFull, my.x, gbase + (q << SHIFT)) * ld4;
-        kr[q] = ldg4_keep(kb + row, keep);
-        if (FINAL) mr[q] = ldg4_keep(mb + row, keep);
+        const uint32_t kk = (uint32_t)__shfl_sync(kFull, my.x, gbase + (q << SHIFT));
+        kr[q] = ldg4_keep(kb + kk * ld4, keep);
+        if (FINAL) mr[q] = ldg4_keep(mb + kk * ldx4, keep);
         if (MAKE_MASK && eb + q < n && act) ubits |= under_bits(kr[q]);
       }
       const bool myvalid = eb + qm < n;
@@ -450,7 +451,7 @@ __global__ void __launch_bounds__(256) fallback_fp64_kernel(
     for (int p = threadIdx.x; p < L * v_r; p += blockDim.x) {
       const int e_ = p / v_r, i = p % v_r;
       const int k = ent[b + e_].k;
-      Kb[p] = exp(-lambda * ((double)Mt[(int64_t)k * ld + i] - (double)colmin[k]));
+      Kb[p] = exp(-lambda * ((double)Mt[(int64_t)k * (ld + 4) + i] - (double)colmin[k]));
     }
     for (int i = threadIdx.x; i < v_r; i += blockDim.x) u[i] = (double)v_r;  // x0 = 1/v_r
     __syncthreads();
@@ -482,7 +483,7 @@ __global__ void __launch_bounds__(256) fallback_fp64_kernel(
       for (int i = 0; i < v_r; ++i) {
         const double kk = Kb[(int64_t)e_ * v_r + i];
         s += kk * u[i];
-        t += kk * (double)Mt[(int64_t)k * ld + i] * u[i];
+        t += kk * (double)Mt[(int64_t)k * (ld + 4) + i] * u[i];
       }
       qv[e_] = ((double)ent[b + e_].c / s) * t;
     }

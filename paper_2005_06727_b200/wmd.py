@@ -236,11 +236,12 @@ def wmd_get_query_rows(h, v_r: int):
     return sel, r
 
 
-def wmd_read_kernel(h, k0: int, count: int, ld: int):
-    kt = np.empty((count, ld), np.float32)
+def wmd_read_kernel(h, k0: int, count: int, ld: int, ktilde: bool = True):
+    """K~ (per-iteration path only; None when ktilde=False), M and colmin rows [k0, k0+count)."""
+    kt = np.empty((count, ld), np.float32) if ktilde else None
     km = np.empty((count, ld), np.float32)
     cm = np.empty(count, np.float32)
-    _check(lib.wmd_read_kernel(h, k0, count, kt.ctypes.data_as(ctypes.c_void_p),
+    _check(lib.wmd_read_kernel(h, k0, count, kt.ctypes.data_as(ctypes.c_void_p) if ktilde else None,
                                km.ctypes.data_as(ctypes.c_void_p), cm.ctypes.data_as(ctypes.c_void_p)), h)
     return kt, km, cm
 
