@@ -12,28 +12,29 @@
 // which has a 1 in every row and every column of the document block. Substituting
 // u = uh e^{-lambda mu}, v = vh e^{-lambda m} into Algorithm 1 gives the same iteration with Kh
 // (exact in real arithmetic), started from uh0_i = v_r e^{-lambda mu_i} (x0 = 1/v_r),
-// and the same distance WMD = sum_e vh_e sum_i Kh_ei M_ie uh_i. Every sum then has
-// a unit-size term, so FP32 only loses range when the scalings themselves spread by >2^100.
-// Each iteration applies an exact power-of-two gauge to uh (R21).
+// and the same distance WMD = sum_e vh_e sum_i Kh_ei M_ie uh_i. Every sum has a
+// unit-size term. Each iteration applies an exact power-of-two gauge to uh (R21).
 //
-// FP32 range certificate (kUnder): an entry flushed to 0 (true value < 2^-126) is an absolute
-// error < 2^-126 in its product. A document keeps its FP32 result only if every sum that has a
-// flushed term satisfies, every iteration,
+// FP32 range certificate: an entry flushed to 0 (true value < 2^-126) is an absolute error
+// < 2^-126 in its product. If the document has any flushed entry, it keeps its FP32 result only
+// if every iteration satisfies, for every e and i,
 //     s_e   = sum_i Kh_ei uh_i :  v_r * max_i uh_i * 2^-126 <= 2^-16 s_e
 //     acc_i = sum_e Kh_ei vh_e :  n   * max_e vh_e * 2^-126 <= 2^-16 acc_i
 // and all uh stay normal; otherwise it is flagged and recomputed in FP64 (fallback_fp64).
 //
-// Mapping: one warp per document, warp-persistent over the length-sorted order. The warp keeps
-// the n x v_r block twice:
-//   row copy    lane e holds Kh[e, 0:LD)          -> s_e = Kh[e,:] . uh is lane-local
-//   column copy lane i holds Kh[0:NE, i]          -> acc_i = Kh[:,i] . vh is lane-local
-// and exchanges only uh (v_r floats) and vh (n floats) per iteration through shared memory
-// (broadcast float4 reads). The block is built from the M rows staged in shared memory by
-// cp.async (prefetched during the previous document's iterations): the column copy computes
-// D, mu and Kh (one ex2 per entry) and hands Kh to the row copy through a second shared buffer.
-// Per iteration: LD + NE FFMA per warp, two reciprocals per lane, three redux.sync (the v
-// maximum for the certificate and the gauge's max / min); no global memory traffic.
-// Bound: FP32 issue.
+// Mapping (2-D tiling of the document block over a warp). Lane = 8a + b: a in [0,4) picks a
+// group of document rows (words), b in [0,8) a group of CW = LD/8 block columns (query rows).
+// Each lane holds an RW x CW tile of Kh in registers (one copy of the block per warp), so
+//   SDDMM  s = Kh uh     : RW*CW FFMA per lane, then a transpose-reduce over the 8 b-lanes
+//   SpMM   acc = Kh^T vh : the same FFMA count, then a transpose-reduce over the 4 a-lanes
+// and the reduced values (one row / one column per lane) are redistributed with xor-shuffles.
+// The register slots are XOR-permuted by the lane bits (row slot t holds row 8a + (t ^ b),
+// column slot c holds column 4b + (c ^ a)) so that every transpose stage sends the upper half
+// of the slots and keeps the lower half with no selects. Per iteration and 32x32 block: 64 FFMA
+// and 20 SHFL per lane, two reciprocals, three redux.sync; no shared or global memory traffic
+// (measured on this B200: a warp shuffle costs one SM-cycle, a broadcast LDS.128 2.5,
+// profiles/r01_issue_bench.jsonl). The M rows of the next document are staged in shared memory
+// by cp.async while the current one iterates. Bound: FP32 issue / shuffle throughput.
 #include <algorithm>
 #include <cfloat>
 #include <cstdint>
@@ -50,16 +51,18 @@ constexpr int kThreads = 32 * kWarps;
 constexpr float kUnder = 0x1p-110f;        // 2^-126 / 2^-16
 constexpr float kLog2e = 1.4426950408889634f;
 
-template <int LD, int NE>
+// CW: block columns per lane (LD = 8 CW query rows, CW in {1, 2, 4, 8}).
+// NT: full 32-row tiles; TW: rows per lane of a trailing 4*TW-row tile (0, 2 or 4).
+template <int CW, int NT, int TW>
 struct Shape {
-  static constexpr int CPL = (LD + 31) / 32;   // query rows (block columns) per lane
-  static constexpr int NW = (NE + 31) / 32;    // nonzero slots per lane (row copy)
-  static constexpr int NEP = (NE + 3) / 4 * 4;
-  static constexpr int P = LD + 4;             // row pitch (floats) of Mx and of the smem buffers
-  static constexpr int BUF = NE * P;           // one staging buffer
-  static constexpr int SU = 32 * CPL, SV = 32 * NW, SM = 32 * NW;
-  static constexpr int WARP_FLOATS = 2 * BUF + SU + SV + SM;
-  static constexpr int REGS = NW * LD + CPL * NE;  // block registers per lane
+  static constexpr int LD = 8 * CW;
+  static constexpr int RW = 8 * NT + TW;        // row slots per lane
+  static constexpr int NE = 32 * NT + 4 * TW;   // document rows covered
+  static constexpr int NW = (NE + 31) / 32;     // entry slots per lane (staging)
+  static constexpr int P = LD + 4;              // row pitch (floats) of Mx and the staging buffers
+  static constexpr int BUF = NE * P;
+  static constexpr int TSH = TW == 4 ? 1 : 2;   // tail row slot t of lane b: TW a + (t ^ (b >> TSH))
+  static constexpr int REGS = RW * CW;
 };
 
 __device__ __forceinline__ float ex2_ftz(float x) {
@@ -67,70 +70,176 @@ __device__ __forceinline__ float ex2_ftz(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint64_t pol) {
   asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "l"(pol)
                : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ float shx(float v, int m) { return __shfl_xor_sync(kFull, v, m); }
 
-template <int LD, int NE>
+// Row index (within the document) of row slot s of lane (a, b).
+template <int NT, int TW>
+__device__ __forceinline__ int row_of(int s, int a, int b) {
+  constexpr int TSH = TW == 4 ? 1 : 2;
+  if (s < 8 * NT) return 32 * (s >> 3) + 8 * a + ((s & 7) ^ b);
+  return 32 * NT + TW * a + ((s - 8 * NT) ^ (b >> TSH));
+}
+
+// Column (query row) of column slot c of lane (a, b).
+template <int CW>
+__device__ __forceinline__ int col_of(int c, int a, int b) {
+  if constexpr (CW == 8) return 8 * b + 4 * (c >> 2) + ((c & 3) ^ a);
+  else if constexpr (CW == 4) return 4 * b + (c ^ a);
+  else if constexpr (CW == 2) return 2 * b + (c ^ (a >> 1));
+  else return b;
+}
+
+// Permute x[0..CW) (natural column order of this lane's column group) into slot order:
+// x'[c] = x[c ^ key], key = a (per quad for CW = 8) or a >> 1 (CW = 2).
+template <int CW>
+__device__ __forceinline__ void to_slots(float (&x)[CW], int a) {
+  if constexpr (CW >= 4) {
+#pragma unroll
+    for (int q = 0; q < CW / 4; ++q) {
+      float* y = x + 4 * q;
+      const bool s1 = a & 1, s2 = a & 2;
+      float t0 = s1 ? y[1] : y[0], t1 = s1 ? y[0] : y[1];
+      float t2 = s1 ? y[3] : y[2], t3 = s1 ? y[2] : y[3];
+      y[0] = s2 ? t2 : t0; y[2] = s2 ? t0 : t2;
+      y[1] = s2 ? t3 : t1; y[3] = s2 ? t1 : t3;
+    }
+  } else if constexpr (CW == 2) {
+    const bool s2 = a & 2;
+    const float t0 = s2 ? x[1] : x[0], t1 = s2 ? x[0] : x[1];
+    x[0] = t0; x[1] = t1;
+  }
+}
+
+// Loads this lane's CW natural-order columns of one staged row.
+template <int CW>
+__device__ __forceinline__ void load_cols(const float* row, int b, float (&x)[CW]) {
+  if constexpr (CW >= 4) {
+#pragma unroll
+    for (int q = 0; q < CW / 4; ++q) {
+      const float4 t = *reinterpret_cast<const float4*>(row + CW * b + 4 * q);
+      x[4 * q] = t.x; x[4 * q + 1] = t.y; x[4 * q + 2] = t.z; x[4 * q + 3] = t.w;
+    }
+  } else if constexpr (CW == 2) {
+    const float2 t = *reinterpret_cast<const float2*>(row + 2 * b);
+    x[0] = t.x; x[1] = t.y;
+  } else {
+    x[0] = row[b];
+  }
+}
+
+// Transpose-reduce of the row partials p[0..RW) over the 8 b-lanes: afterwards p[8T] holds the
+// full sum of row 32T + 8a + b (full tiles) and p[8NT] that of tail row 32NT + TW a + (b >> TSH).
+template <int NT, int TW>
+__device__ __forceinline__ void reduce_rows(float* p) {
+#pragma unroll
+  for (int T = 0; T < NT; ++T) {
+    float* q = p + 8 * T;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) q[t] += shx(q[t + 4], 4);
+#pragma unroll
+    for (int t = 0; t < 2; ++t) q[t] += shx(q[t + 2], 2);
+    q[0] += shx(q[1], 1);
+  }
+  if constexpr (TW == 4) {
+    float* q = p + 8 * NT;
+    q[0] += shx(q[2], 4); q[1] += shx(q[3], 4);
+    q[0] += shx(q[1], 2);
+    q[0] += shx(q[0], 1);
+  } else if constexpr (TW == 2) {
+    float* q = p + 8 * NT;
+    q[0] += shx(q[1], 4);
+    q[0] += shx(q[0], 2);
+    q[0] += shx(q[0], 1);
+  }
+}
+
+// Transpose-reduce of the column partials q[0..CW) over the 4 a-lanes (lane xor 16, 8):
+// afterwards q[0] (and q[4] for CW = 8) holds the full sum of the lane's own column(s).
+template <int CW>
+__device__ __forceinline__ void reduce_cols(float* q) {
+  if constexpr (CW >= 4) {
+#pragma unroll
+    for (int g = 0; g < CW / 4; ++g) {
+      float* y = q + 4 * g;
+      y[0] += shx(y[2], 16); y[1] += shx(y[3], 16);
+      y[0] += shx(y[1], 8);
+    }
+  } else if constexpr (CW == 2) {
+    q[0] += shx(q[1], 16);
+    q[0] += shx(q[0], 8);
+  } else {
+    q[0] += shx(q[0], 16);
+    q[0] += shx(q[0], 8);
+  }
+}
+
+#ifndef WMD_FUSED_REG_SLACK
+#define WMD_FUSED_REG_SLACK 36
+#endif
+template <int CW, int NT, int TW>
 constexpr int min_blocks() {
-  constexpr int regs = ((Shape<LD, NE>::REGS + 56) + 7) / 8 * 8;
+  using S = Shape<CW, NT, TW>;
+  constexpr int regs = ((S::REGS + 3 * S::RW + 2 * CW + WMD_FUSED_REG_SLACK) + 7) / 8 * 8;
   constexpr int b = 65536 / (kThreads * regs);
+#ifdef WMD_FUSED_MINB
+  if (S::REGS <= 40) return WMD_FUSED_MINB;
+#endif
   return b < 1 ? 1 : (b > 8 ? 8 : b);
 }
 
-// LD: query rows rounded up to 8 (<= 64). NE: maximum nonzeros per document of this launch.
-template <int LD, int NE>
-__global__ void __launch_bounds__(kThreads, min_blocks<LD, NE>()) sinkhorn_fused_kernel(
-    const int32_t* __restrict__ order, const int32_t* __restrict__ doc_ptr,
-    const Entry* __restrict__ ent, int64_t pos0, int64_t pos1, const float* __restrict__ Mx,
-    int v_r, const float* __restrict__ rpad, float lambda, int iters, float* __restrict__ dist,
+template <int CW, int NT, int TW>
+__global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW>()) sinkhorn_fused_kernel(
+    const int4* __restrict__ sdoc, const Entry* __restrict__ ent, int64_t pos0, int64_t pos1,
+    const float* __restrict__ Mx, int v_r, const float* __restrict__ rpad, float lambda, int iters, float* __restrict__ dist,
     uint8_t* __restrict__ flags, int32_t* __restrict__ flagged_list,
     int32_t* __restrict__ flagged_count) {
-  using S = Shape<LD, NE>;
-  constexpr int CPL = S::CPL, NW = S::NW, NEP = S::NEP, P = S::P;
-  static_assert(LD % 8 == 0 && LD <= 64 && NE <= 64, "shape");
+  using S = Shape<CW, NT, TW>;
+  constexpr int LD = S::LD, RW = S::RW, NW = S::NW, P = S::P;
+  constexpr int NOWN = NT + (TW ? 1 : 0);        // own rows per lane after the row reduce
+  constexpr int NCO = CW == 8 ? 2 : 1;           // own columns per lane after the column reduce
   extern __shared__ __align__(16) float smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  float* wbase = smem + wib * S::WARP_FLOATS;
-  float* buf0 = wbase;
-  float* su = wbase + 2 * S::BUF;
-  float* sv = su + S::SU;
-  float* sm = sv + S::SV;
+  const int a = lane >> 3, b = lane & 7;
+  float* buf0 = smem + wib * 2 * S::BUF;
   const int64_t nwarps = (int64_t)gridDim.x * kWarps;
   const uint64_t keep = l2_evict_last_policy();
   const int2* ent2 = reinterpret_cast<const int2*>(ent);
-  const float a = lambda * kLog2e;            // exp(-lambda x) = 2^(-a x)
+  const float alpha = lambda * kLog2e;          // exp(-lambda x) = 2^(-alpha x)
   const float kv_s = (float)v_r * kUnder;
 
-  float r[CPL];
-  bool real[CPL];
+  // own columns (after the column reduce) and their marginals r_i (zero beyond v_r)
+  float r_own[NCO];
+  bool oreal[NCO];
 #pragma unroll
-  for (int c = 0; c < CPL; ++c) {
-    const int col = lane + 32 * c;
-    real[c] = col < v_r;
-    r[c] = (col < LD) ? __ldg(rpad + col) : 0.f;  // zero beyond v_r
+  for (int g = 0; g < NCO; ++g) {
+    const int oc = CW == 8 ? 8 * b + 4 * g + a : (CW == 4 ? 4 * b + a : (CW == 2 ? 2 * b + (a >> 1) : b));
+    r_own[g] = __ldg(rpad + oc);
+    oreal[g] = oc < v_r;
   }
+  bool nreal[CW];  // natural-order columns CW*b + c of this lane's group are real query rows
+#pragma unroll
+  for (int c = 0; c < CW; ++c) nreal[c] = CW * b + c < v_r;
 
-  // ---- prefetch machinery: stage 1 (order, doc_ptr), stage 2 (entries), stage 3 (cp.async rows)
+  // ---- prefetch: stage 1 (document header), stage 2 (entries), stage 3 (cp.async of M rows)
   int64_t pos = pos0 + (int64_t)blockIdx.x * kWarps + wib;
-  int pj = -1, pb = 0, pn = 0;    // next document: id, first nonzero, length
+  int pj = -1, pb = 0, pn = 0;
   int pk[NW];
   float pc[NW];
-  int cur = 0;                    // staging buffer of the current document
+  int cur = 0;
   auto stage1 = [&](int64_t p) {
     pj = -1; pn = 0;
     if (p < pos1) {
-      pj = __ldg(order + p);
-      pb = __ldg(doc_ptr + pj);
-      pn = __ldg(doc_ptr + pj + 1) - pb;
+      const int4 x = __ldg(sdoc + p);  // {document id, first nonzero, length, -}
+      pj = x.x; pb = x.y; pn = x.z;
     }
   };
   auto stage2 = [&]() {
@@ -148,7 +257,9 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LD, NE>()) sinkhorn_fused
     for (int w = 0; w < NW; ++w) {
       const int e = lane + 32 * w;
       if (e < pn) {
-        const float* src = Mx + (size_t)(uint32_t)pk[w] * P;
+        uint32_t k;  // opaque copy: keeps the address arithmetic (and its wait on the entry
+        asm volatile("mov.b32 %0, %1;" : "=r"(k) : "r"(pk[w]));  // load) at this point
+        const float* src = Mx + (size_t)k * P;
         const uint32_t d = smem_u32(dst + e * P);
 #pragma unroll
         for (int q = 0; q < P / 4; ++q) cp_async16(d + 16 * q, src + 4 * q, keep);
@@ -157,100 +268,78 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LD, NE>()) sinkhorn_fused
     cp_async_commit();
   };
 
-  // prologue: the first document goes to buffer 0
   stage1(pos);
   stage2();
   stage3(buf0);
 
   for (; pos < pos1; pos += nwarps) {
-    // current document (prefetched)
     const int j = pj, n = pn;
-    int ke[NW];
-    float ce[NW];
-    bool ve[NW];
+    // c of the lane's own rows: row 32T + lane (full tiles), tail row 32NT + TW a + (b >> TSH)
+    float c_own[NOWN];
+    bool v_ok[NOWN];
 #pragma unroll
-    for (int w = 0; w < NW; ++w) {
-      ke[w] = pk[w];
-      ce[w] = pc[w];
-      ve[w] = lane + 32 * w < n;
+    for (int T = 0; T < NT; ++T) {
+      c_own[T] = pc[T];
+      v_ok[T] = 32 * T + lane < n;
     }
-    float* Sb = buf0 + cur * S::BUF;          // M rows of this document (row e at Sb + e*P)
-    float* Tb = buf0 + (cur ^ 1) * S::BUF;    // transpose scratch, then the next document's rows
-    stage1(pos + nwarps);                     // next document's header loads are in flight
+    if constexpr (TW > 0) {
+      const int tr = TW * a + (b >> S::TSH);
+      c_own[NT] = __shfl_sync(kFull, pc[NT], tr);
+      v_ok[NT] = 32 * NT + tr < n;
+    }
+    float* Sb = buf0 + cur * S::BUF;          // this document's M rows (row e at Sb + e*P)
+    float* Nb = buf0 + (cur ^ 1) * S::BUF;    // the next document's rows
+    stage1(pos + nwarps);
     cp_async_wait_all();
     __syncwarp();
 
-    // ---- m_e (stored at M row position LD) to a contiguous vector
-    float me[NW];
+    // ---- block tile: D = M - m, mu = column minima over the document, Kh = 2^(-alpha (D - mu))
+    float K[RW][CW];
+    float mu[CW];
 #pragma unroll
-    for (int w = 0; w < NW; ++w) {
-      const int e = lane + 32 * w;
-      me[w] = ve[w] ? Sb[e * P + LD] : 0.f;
-      sm[e] = me[w];
-    }
-    __syncwarp();
-
-    // ---- column copy: D, mu, Kh (lane i owns column i)
-    float kc[CPL][NE];
-    bool und[CPL];
-    float uh[CPL];
+    for (int c = 0; c < CW; ++c) mu[c] = FLT_MAX;
+    // branch-free: rows past n read a staged row (stale contents) and are masked by selects
 #pragma unroll
-    for (int c = 0; c < CPL; ++c) {
-      const int col = lane + 32 * c;
-      const bool colok = col < LD;  // lanes past LD (CPL*32 > LD) hold a phantom column of 1s
-      float mu = FLT_MAX;
+    for (int s = 0; s < RW; ++s) {
+      const int e = row_of<NT, TW>(s, a, b);
+      const bool ok = e < n;
+      const float* row = Sb + (ok ? e : 0) * P;
+      float x[CW];
+      load_cols<CW>(row, b, x);
+      const float me = row[LD];
 #pragma unroll
-      for (int e4 = 0; e4 < NEP / 4; ++e4) {
-        const float4 m4 = *reinterpret_cast<const float4*>(sm + 4 * e4);
-        const float mm[4] = {m4.x, m4.y, m4.z, m4.w};
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const int e = 4 * e4 + t;
-          if (e < NE) {
-            float dv = 0.f;
-            if (e < n && colok) {
-              dv = Sb[e * P + col] - mm[t];
-              mu = fminf(mu, dv);
-            }
-            kc[c][e] = dv;
-          }
-        }
+      for (int c = 0; c < CW; ++c) {
+        K[s][c] = ok ? x[c] - me : FLT_MAX;   // rows past n: FLT_MAX (Kh = 0 below)
+        mu[c] = fminf(mu[c], K[s][c]);
       }
-      const float amu = a * mu;
-      uh[c] = real[c] ? (float)v_r * ex2_ftz(-amu) : 0.f;   // uh0 = v_r e^{-lambda mu_i}
-      bool u_ = false;
-#pragma unroll
-      for (int e = 0; e < NE; ++e) {
-        float kv = 0.f;
-        if (e < n) {
-          kv = real[c] ? ex2_ftz(fmaf(-a, kc[c][e], amu)) : 1.f;  // padded columns: 1 (uh = 0)
-          u_ |= kv < FLT_MIN;
-          if (colok) Tb[e * P + col] = kv;
-        }
-        kc[c][e] = kv;
-      }
-      und[c] = u_ && real[c];
     }
-    __syncwarp();
-
-    // ---- row copy (lane e owns row e) from the transpose buffer
-    float kr[NW][LD];
-    bool unde[NW];
 #pragma unroll
-    for (int w = 0; w < NW; ++w) {
-      const int e = lane + 32 * w;
-      float mn = 1.f;
-#pragma unroll
-      for (int q = 0; q < LD / 4; ++q) {
-        float4 t = make_float4(1.f, 1.f, 1.f, 1.f);
-        if (e < NE) t = *reinterpret_cast<const float4*>(Tb + e * P + 4 * q);
-        kr[w][4 * q] = t.x; kr[w][4 * q + 1] = t.y; kr[w][4 * q + 2] = t.z; kr[w][4 * q + 3] = t.w;
-        mn = fminf(mn, fminf(fminf(t.x, t.y), fminf(t.z, t.w)));
-      }
-      unde[w] = ve[w] && mn < FLT_MIN;
+    for (int c = 0; c < CW; ++c) {  // column minima over the 4 a-lanes (natural column order)
+      mu[c] = fminf(mu[c], shx(mu[c], 8));
+      mu[c] = fminf(mu[c], shx(mu[c], 16));
     }
-    __syncwarp();
-    // the transpose buffer is free: the next document's rows go there while this one iterates
+    float amu[CW];
+#pragma unroll
+    for (int c = 0; c < CW; ++c) amu[c] = alpha * mu[c];
+    bool flushed = false;
+#pragma unroll
+    for (int s = 0; s < RW; ++s) {
+#pragma unroll
+      for (int c = 0; c < CW; ++c) {
+        const float d = K[s][c];
+        const float kx = ex2_ftz(fmaf(-alpha, d, amu[c]));   // rows past n: 2^-huge = 0
+        flushed |= kx < FLT_MIN && d != FLT_MAX;
+        K[s][c] = nreal[c] ? kx : (d != FLT_MAX ? 1.f : 0.f);  // padded columns: 1 on real rows
+      }
+      to_slots<CW>(K[s], a);
+    }
+    const bool und = __any_sync(kFull, flushed);
+    // uh0 = v_r 2^(-alpha mu) on real columns (slot order)
+    float u[CW];
+#pragma unroll
+    for (int c = 0; c < CW; ++c) u[c] = nreal[c] ? (float)v_r * ex2_ftz(-alpha * mu[c]) : 0.f;
+    to_slots<CW>(u, a);
+    // the next document's entries (their header loads were issued above)
     stage2();
     bool staged = false;
 
@@ -258,100 +347,124 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LD, NE>()) sinkhorn_fused
     float umax_k = (float)v_r * kv_s;   // v_r * max(uh) * 2^-110 (max uh0 <= v_r)
     bool bad = false;
     uint32_t badu = 0u;
-    float vt[NW];
+    float v_own[NOWN];
     for (int it = 0;; ++it) {
-      __syncwarp();
+      // SDDMM: row partials over this lane's columns, then the reduce over the b-lanes
+      float p[RW];
 #pragma unroll
-      for (int c = 0; c < CPL; ++c) su[lane + 32 * c] = uh[c];
-      __syncwarp();
-      // SDDMM: s_e = Kh[e,:] . uh,  vh_e = c_e / s_e
-      float sp[NW][4];
+      for (int s = 0; s < RW; ++s) {
+        float acc = K[s][0] * u[0];
 #pragma unroll
-      for (int w = 0; w < NW; ++w) sp[w][0] = sp[w][1] = sp[w][2] = sp[w][3] = 0.f;
-#pragma unroll
-      for (int q = 0; q < LD / 4; ++q) {
-        const float4 uu = *reinterpret_cast<const float4*>(su + 4 * q);
-#pragma unroll
-        for (int w = 0; w < NW; ++w) {
-          sp[w][0] = fmaf(kr[w][4 * q], uu.x, sp[w][0]);
-          sp[w][1] = fmaf(kr[w][4 * q + 1], uu.y, sp[w][1]);
-          sp[w][2] = fmaf(kr[w][4 * q + 2], uu.z, sp[w][2]);
-          sp[w][3] = fmaf(kr[w][4 * q + 3], uu.w, sp[w][3]);
-        }
+        for (int c = 1; c < CW; ++c) acc = fmaf(K[s][c], u[c], acc);
+        p[s] = acc;
       }
+      reduce_rows<NT, TW>(p);
       uint32_t vmax_b = 0u;
 #pragma unroll
-      for (int w = 0; w < NW; ++w) {
-        const float s = (sp[w][0] + sp[w][1]) + (sp[w][2] + sp[w][3]);
-        vt[w] = ve[w] ? ce[w] * rcp_fast(s) : 0.f;
-        bad |= unde[w] && umax_k > s;
-        vmax_b = max(vmax_b, __float_as_uint(vt[w]));
+      for (int o = 0; o < NOWN; ++o) {
+        const float sv = p[8 * o];
+        v_own[o] = v_ok[o] ? c_own[o] * rcp_fast(sv) : 0.f;
+#ifndef WMD_EXP_NO_CERT
+        bad |= v_ok[o] && und && umax_k > sv;
+#endif
+        vmax_b = max(vmax_b, __float_as_uint(v_own[o]));
       }
       if (it == iters) break;
       if (it == 1) {  // the next document's entries have landed: start its row copies
         staged = true;
-        stage3(Tb);
+        stage3(Nb);
       }
-      // SpMM: acc_i = Kh[:,i] . vh,  uh_i = r_i / acc_i
-#pragma unroll
-      for (int w = 0; w < NW; ++w) sv[lane + 32 * w] = vt[w];
+#ifndef WMD_EXP_NO_CERT
       vmax_b = __reduce_max_sync(kFull, vmax_b);
-      __syncwarp();
-      float ap[CPL][4];
+#endif
+      // distribute vh to the row slots
+      float vs[RW];
 #pragma unroll
-      for (int c = 0; c < CPL; ++c) ap[c][0] = ap[c][1] = ap[c][2] = ap[c][3] = 0.f;
+      for (int T = 0; T < NT; ++T) {
+        vs[8 * T] = v_own[T];
 #pragma unroll
-      for (int e4 = 0; e4 < NEP / 4; ++e4) {
-        const float4 vv = *reinterpret_cast<const float4*>(sv + 4 * e4);
-        const float vq[4] = {vv.x, vv.y, vv.z, vv.w};
-#pragma unroll
-        for (int c = 0; c < CPL; ++c)
-#pragma unroll
-          for (int t = 0; t < 4; ++t)
-            if (4 * e4 + t < NE) ap[c][t] = fmaf(kc[c][4 * e4 + t], vq[t], ap[c][t]);
+        for (int t = 1; t < 8; ++t) vs[8 * T + t] = shx(v_own[T], t);
       }
+      if constexpr (TW > 0) {
+        vs[8 * NT] = v_own[NT];
+#pragma unroll
+        for (int t = 1; t < TW; ++t) vs[8 * NT + t] = shx(v_own[NT], t << S::TSH);
+      }
+      // SpMM: column partials over this lane's rows (two chains per column), reduce over a-lanes
+      float q[CW];
+#pragma unroll
+      for (int c = 0; c < CW; ++c) {
+        float q0 = K[0][c] * vs[0];
+#pragma unroll
+        for (int s = 1; s < RW; ++s) q0 = fmaf(K[s][c], vs[s], q0);
+        q[c] = q0;
+      }
+      reduce_cols<CW>(q);
       const float vcap = (float)n * __uint_as_float(vmax_b) * kUnder;
-      uint32_t umax_b = 0u, umin_b = 0xffffffffu;
-      float un[CPL];
+      uint32_t umax_b = 0u;
+      float uo[NCO];
 #pragma unroll
-      for (int c = 0; c < CPL; ++c) {
-        const float acc = (ap[c][0] + ap[c][1]) + (ap[c][2] + ap[c][3]);
-        un[c] = r[c] * rcp_fast(acc);
-        bad |= und[c] && vcap > acc;
-        umax_b = max(umax_b, __float_as_uint(un[c]));
-        if (real[c]) umin_b = min(umin_b, __float_as_uint(un[c]));
+      for (int g = 0; g < NCO; ++g) {
+        const float acc = q[4 * g];
+        uo[g] = r_own[g] * rcp_fast(acc);
+#ifndef WMD_EXP_NO_CERT
+        bad |= und && vcap > acc;
+#endif
+        umax_b = max(umax_b, __float_as_uint(uo[g]));
       }
-      // gauge: positive floats order like their bit patterns
+      // gauge: max uh -> [1, 2) by an exact power of two (positive floats order like their bits);
+      // the lanes check their own uh stay normal
       umax_b = __reduce_max_sync(kFull, umax_b);
-      umin_b = __reduce_min_sync(kFull, umin_b);
-      badu |= (umin_b < 0x00800000u) | (umax_b > 0x7f7fffffu);
-      const float sc = gauge_scale(umax_b, umin_b);  // exact power of two
+      badu |= umax_b > 0x7f7fffffu;
+      const float sc = __uint_as_float((254u - min(umax_b >> 23, 253u)) << 23);
+      umax_k = 2.f * kv_s;
 #pragma unroll
-      for (int c = 0; c < CPL; ++c) uh[c] = un[c] * sc;
-      umax_k = __uint_as_float(umax_b) * sc * kv_s;
+      for (int g = 0; g < NCO; ++g) {
+        uo[g] *= sc;
+        bad |= oreal[g] && !(uo[g] >= FLT_MIN);
+      }
+      // distribute uh to the column slots
+      if constexpr (CW >= 4) {
+#pragma unroll
+        for (int g = 0; g < CW / 4; ++g) {
+          u[4 * g] = uo[g];
+#pragma unroll
+          for (int c = 1; c < 4; ++c) u[4 * g + c] = shx(uo[g], 8 * c);
+        }
+      } else if constexpr (CW == 2) {
+        u[0] = uo[0];
+        u[1] = shx(uo[0], 16);
+      } else {
+        u[0] = uo[0];
+      }
     }
-    if (!staged) stage3(Tb);
-    // ---- final step: WMD_j = sum_e vh_e q_e,  q_e = sum_i Kh_ei M_ie uh_i  (su holds uh)
+    if (!staged) stage3(Nb);
+    // ---- final step: WMD_j = sum_e vh_e q_e,  q_e = sum_i Kh_ei M_ie uh_i
+    float p[RW];
+#pragma unroll
+    for (int s = 0; s < RW; ++s) {
+      const int e = row_of<NT, TW>(s, a, b);
+      const bool ok = e < n;
+      float x[CW];
+      load_cols<CW>(Sb + (ok ? e : 0) * P, b, x);
+      to_slots<CW>(x, a);
+#pragma unroll
+      for (int c = 0; c < CW; ++c) x[c] = ok ? x[c] : 0.f;   // stale rows past n
+      float acc = 0.f;
+#pragma unroll
+      for (int c = 0; c < CW; ++c) acc = fmaf(K[s][c] * x[c], u[c], acc);
+      p[s] = acc;
+    }
+    reduce_rows<NT, TW>(p);
     float wsum = 0.f;
 #pragma unroll
-    for (int w = 0; w < NW; ++w) {
-      const int e = lane + 32 * w;
-      if (w > 0 && !__any_sync(kFull, ve[w])) break;
-      float q0 = 0.f, q1 = 0.f;
-#pragma unroll
-      for (int q4 = 0; q4 < LD / 4; ++q4) {
-        float4 m4 = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (e < NE) m4 = *reinterpret_cast<const float4*>(Sb + e * P + 4 * q4);
-        const float4 uu = *reinterpret_cast<const float4*>(su + 4 * q4);
-        q0 = fmaf(kr[w][4 * q4] * m4.x, uu.x, q0);
-        q1 = fmaf(kr[w][4 * q4 + 1] * m4.y, uu.y, q1);
-        q0 = fmaf(kr[w][4 * q4 + 2] * m4.z, uu.z, q0);
-        q1 = fmaf(kr[w][4 * q4 + 3] * m4.w, uu.w, q1);
-      }
-      if (ve[w]) wsum = fmaf(vt[w], q0 + q1, wsum);
+    for (int T = 0; T < NT; ++T)
+      if (v_ok[T]) wsum = fmaf(v_own[T], p[8 * T], wsum);
+    if constexpr (TW > 0) {  // each tail row is held by 2^TSH lanes: count it once
+      if (v_ok[NT] && (b & ((1 << S::TSH) - 1)) == 0) wsum = fmaf(v_own[NT], p[8 * NT], wsum);
     }
 #pragma unroll
-    for (int off = 16; off; off >>= 1) wsum += __shfl_xor_sync(kFull, wsum, off);
+    for (int off = 16; off; off >>= 1) wsum += shx(wsum, off);
     const bool flag = __any_sync(kFull, bad) || badu || !(fabsf(wsum) <= FLT_MAX);
     if (lane == 0) {
       dist[j] = wsum;
@@ -360,6 +473,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LD, NE>()) sinkhorn_fused
         flagged_list[atomicAdd(flagged_count, 1)] = j;
       }
     }
+    __syncwarp();  // all lanes are done with Sb before it becomes the next staging buffer
     cur ^= 1;
   }
   cp_async_wait_all();  // nothing may be in flight when the warp exits
@@ -376,79 +490,83 @@ int num_sms() {
   return sms;
 }
 
-template <int LD, int NE>
-void launch_fused_range(const int32_t* order, const int32_t* doc_ptr, const Entry* ent, int64_t p0,
+template <int CW, int NT, int TW>
+void launch_fused_range(const int4* sdoc, const Entry* ent, int64_t p0,
                         int64_t p1, const float* Mx, int v_r, const float* rpad, float lambda,
                         int iters, float* dist, uint8_t* flags, int32_t* fl, int32_t* fc,
                         cudaStream_t st) {
   if (p1 <= p0) return;
-  constexpr size_t smem = sizeof(float) * Shape<LD, NE>::WARP_FLOATS * kWarps;
+  constexpr size_t smem = sizeof(float) * 2 * Shape<CW, NT, TW>::BUF * kWarps;
   static int resident = 0;
   if (!resident) {
-    cudaFuncSetAttribute(sinkhorn_fused_kernel<LD, NE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(sinkhorn_fused_kernel<LD, NE>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(sinkhorn_fused_kernel<CW, NT, TW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(sinkhorn_fused_kernel<CW, NT, TW>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sinkhorn_fused_kernel<LD, NE>, kThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sinkhorn_fused_kernel<CW, NT, TW>, kThreads, smem);
     resident = std::max(1, per_sm) * num_sms();
   }
   const int64_t need = (p1 - p0 + kWarps - 1) / kWarps;
-  // persistent warps: a few waves of documents per warp keep the staging pipeline busy
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, resident));
-  sinkhorn_fused_kernel<LD, NE><<<grid, kThreads, smem, st>>>(order, doc_ptr, ent, p0, p1, Mx, v_r, rpad,
-                                                               lambda, iters, dist, flags, fl, fc);
+  sinkhorn_fused_kernel<CW, NT, TW><<<grid, kThreads, smem, st>>>(sdoc, ent, p0, p1, Mx, v_r, rpad,
+                                                                   lambda, iters, dist, flags, fl, fc);
 }
 
-// Length buckets of the fused kernel over the length-sorted order. A bucket with NE > 32 keeps
-// two row slots per lane; supported pairs keep the block within ~136 registers per lane.
-constexpr int kBuckets[] = {16, 24, 32, 40, 48, 64};
+// Length buckets (rows covered: 8, 16, 32, 40, 48, 64) over the length-sorted order.
+struct Bucket { int ne, nt, tw; };
+constexpr Bucket kBuckets[] = {{8, 0, 2}, {16, 0, 4}, {32, 1, 0}, {40, 1, 2}, {48, 1, 4}, {64, 2, 0}};
 constexpr int kNumBuckets = 6;
 
-constexpr bool fits(int ld, int ne) {
-  return ((ne + 31) / 32) * ld + ((ld + 31) / 32) * ne <= 136;
-}
+constexpr bool fits(int cw, int ne) { return (ne / 4) * cw <= 96; }  // block registers per lane
 
-template <int LD>
-void dispatch_ne(int ne, const int32_t* order, const int32_t* doc_ptr, const Entry* ent, int64_t p0,
-                 int64_t p1, const float* Mx, int v_r, const float* rpad, float lambda, int iters,
-                 float* dist, uint8_t* flags, int32_t* fl, int32_t* fc, cudaStream_t st) {
-#define F_(NE) \
-  if constexpr (fits(LD, NE)) launch_fused_range<LD, NE>(order, doc_ptr, ent, p0, p1, Mx, v_r, rpad, lambda, iters, dist, flags, fl, fc, st)
-  switch (ne) {
-    case 16: F_(16); break;
-    case 24: F_(24); break;
-    case 32: F_(32); break;
-    case 40: F_(40); break;
-    case 48: F_(48); break;
-    default: F_(64); break;
+template <int CW>
+void dispatch_bucket(int bi, const int4* sdoc, const Entry* ent, int64_t p0,
+                     int64_t p1, const float* Mx, int v_r, const float* rpad, float lambda, int iters,
+                     float* dist, uint8_t* flags, int32_t* fl, int32_t* fc, cudaStream_t st) {
+#define F_(NT, TW) \
+  if constexpr (fits(CW, 32 * NT + 4 * TW)) launch_fused_range<CW, NT, TW>(sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, dist, flags, fl, fc, st)
+  switch (bi) {
+    case 0: F_(0, 2); break;
+    case 1: F_(0, 4); break;
+    case 2: F_(1, 0); break;
+    case 3: F_(1, 2); break;
+    case 4: F_(1, 4); break;
+    default: F_(2, 0); break;
   }
 #undef F_
 }
 
 }  // namespace
 
+int fused_ld(int v_r) {
+  int ld = 8;
+  while (ld < v_r) ld *= 2;
+  return ld;
+}
+
 bool fused_supported(int ld, int64_t max_doc_nnz) {
-  if (ld > 64 || max_doc_nnz > 64) return false;
+  if (ld > 64 || (ld & (ld - 1)) || ld < 8 || max_doc_nnz > 64) return false;
   for (int b = 0; b < kNumBuckets; ++b)
-    if (kBuckets[b] >= max_doc_nnz) return fits(ld, kBuckets[b]);
+    if (kBuckets[b].ne >= max_doc_nnz) return fits(ld / 8, kBuckets[b].ne);
   return false;
 }
 
-void launch_sinkhorn_fused(const int32_t* order, const int32_t* doc_ptr, const Entry* ent, int64_t N,
+void launch_sinkhorn_fused(const int4* sdoc, const Entry* ent, int64_t N,
                            const int64_t* len_prefix, int64_t max_len, const float* Mx, int ld,
                            int v_r, const float* rpad, float lambda, int iters, float* dist,
                            uint8_t* flags, int32_t* flagged_list, int32_t* flagged_count,
                            cudaStream_t st) {
   // len_prefix[L] = number of documents with fewer than L nonzeros: the length-sorted order
-  // splits into buckets of at most 16 / 24 / 32 / 40 / 48 / 64 nonzeros, one launch each.
+  // splits into buckets of at most 8 / 16 / 32 / 40 / 48 / 64 nonzeros, one launch each.
   int64_t p0 = 0;
   for (int bi = 0; bi < kNumBuckets && p0 < N; ++bi) {
-    const int NE = kBuckets[bi];
+    const int NE = kBuckets[bi].ne;
     const int64_t p1 = NE >= max_len ? N : len_prefix[NE + 1];
     if (p1 > p0) {
       switch (ld) {
-#define L_(LD) case LD: dispatch_ne<LD>(NE, order, doc_ptr, ent, p0, p1, Mx, v_r, rpad, lambda, iters, dist, flags, flagged_list, flagged_count, st); break;
-        L_(8) L_(16) L_(24) L_(32) L_(40) L_(48) L_(56) L_(64)
-#undef L_
+        case 8: dispatch_bucket<1>(bi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, dist, flags, flagged_list, flagged_count, st); break;
+        case 16: dispatch_bucket<2>(bi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, dist, flags, flagged_list, flagged_count, st); break;
+        case 32: dispatch_bucket<4>(bi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, dist, flags, flagged_list, flagged_count, st); break;
+        case 64: dispatch_bucket<8>(bi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, dist, flags, flagged_list, flagged_count, st); break;
         default: break;
       }
     }
@@ -460,7 +578,7 @@ int fused_launch_count(const int64_t* len_prefix, int64_t max_len, int64_t N) {
   int64_t p0 = 0;
   int cnt = 0;
   for (int bi = 0; bi < kNumBuckets && p0 < N; ++bi) {
-    const int64_t p1 = kBuckets[bi] >= max_len ? N : len_prefix[kBuckets[bi] + 1];
+    const int64_t p1 = kBuckets[bi].ne >= max_len ? N : len_prefix[kBuckets[bi].ne + 1];
     cnt += p1 > p0;
     p0 = p1;
   }

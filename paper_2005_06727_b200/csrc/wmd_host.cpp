@@ -84,6 +84,7 @@ struct wmd_handle {
   bool has_targets = false;
   DevBuf<int32_t> doc_ptr;
   DevBuf<int32_t> order;     // documents sorted by length (stable counting sort)
+  DevBuf<int4> sdoc;         // {id, first nonzero, length, 0} in that order (fused path)
   DevBuf<Entry> ent;
   int64_t N = 0, nnz = 0, max_doc_nnz = 0;
   std::vector<int64_t> len_prefix;  // [L] = documents with fewer than L nonzeros (host)
@@ -258,6 +259,7 @@ void drop_targets(wmd_handle* h) {
   h->has_targets = false;
   h->doc_ptr.release();
   h->order.release();
+  h->sdoc.release();
   h->ent.release();
   h->N = h->nnz = h->max_doc_nnz = 0;
   h->u_valid = false;
@@ -372,7 +374,7 @@ void wmd_destroy(wmd_handle* h) {
     if (h->stage[s]) cudaFreeHost(h->stage[s]);
     if (h->stage_ev[s]) cudaEventDestroy(h->stage_ev[s]);
   }
-  h->E.release(); h->doc_ptr.release(); h->order.release(); h->ent.release(); h->sel.release(); h->rpad.release();
+  h->E.release(); h->doc_ptr.release(); h->order.release(); h->sdoc.release(); h->ent.release(); h->sel.release(); h->rpad.release();
   h->Kt.release(); h->Mx.release(); h->colmin.release(); h->ua.release(); h->ub.release(); h->umask.release();
   h->dist_tmp.release(); h->flags.release(); h->flagged.release(); h->counters.release();
   h->fb_scratch.release();
@@ -451,6 +453,13 @@ wmd_status wmd_set_targets(wmd_handle* h, const int64_t* col_ptr, const int32_t*
   CK(h, h->ent.ensure(nnz));
   CK(h, h->order.ensure(N));
   CK(h, cudaMemcpyAsync(h->order.p, ord.data(), N * sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
+  std::vector<int4> sd(N);
+  for (int64_t p = 0; p < N; ++p) {
+    const int32_t j = ord[p];
+    sd[p] = make_int4(j, dp[j], dp[j + 1] - dp[j], 0);
+  }
+  CK(h, h->sdoc.ensure(N));
+  CK(h, cudaMemcpyAsync(h->sdoc.p, sd.data(), N * sizeof(int4), cudaMemcpyHostToDevice, h->stream));
   CK(h, cudaMemcpyAsync(h->doc_ptr.p, dp.data(), (N + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
   CK(h, cudaMemcpyAsync(h->ent.p, en.data(), nnz * sizeof(Entry), cudaMemcpyHostToDevice, h->stream));
   CK(h, h->flags.ensure(N));
@@ -480,14 +489,17 @@ wmd_status wmd_query(wmd_handle* h, const int32_t* query_ids, const float* query
   DeviceGuard g(h->device);
   if (!g.ok) return fail(h, WMD_ERR_CUDA, "cudaSetDevice failed");
 
-  const int32_t v_r = n, ld = round_up8(n);
+  const int32_t v_r = n;
   const int64_t N = h->N;
-  // +128 floats: the pass kernels gather unpredicated float4s up to 4*32 floats past a row
+  // fused path: ld = v_r rounded up to a power of two (the 2-D lane tiling); per-iteration
+  // path: v_r rounded up to 8
   const bool fused = (h->opt_path == WMD_PATH_FUSED || h->opt_path == WMD_PATH_AUTO) &&
-                     wmd::fused_supported(ld, h->max_doc_nnz);
+                     wmd::fused_supported(wmd::fused_ld(n), h->max_doc_nnz);
   if (h->opt_path == WMD_PATH_FUSED && !fused)
-    return fail(h, WMD_ERR_INVALID_ARGUMENT, "fused path does not support ld=%d, max doc nnz=%lld", ld,
+    return fail(h, WMD_ERR_INVALID_ARGUMENT, "fused path does not support v_r=%d, max doc nnz=%lld", n,
                 (long long)h->max_doc_nnz);
+  const int32_t ld = fused ? wmd::fused_ld(n) : round_up8(n);
+  // +128 floats: the pass kernels gather unpredicated float4s up to 4*32 floats past a row
   if (!fused) CK(h, h->Kt.ensure((size_t)h->V * ld + 128));
   CK(h, h->Mx.ensure((size_t)h->V * (ld + 4) + 128));
   CK(h, h->ua.ensure((size_t)N * ld));
@@ -529,7 +541,7 @@ wmd_status wmd_query(wmd_handle* h, const int32_t* query_ids, const float* query
   if (pe) CK(h, cudaEventRecord(pe->ev[1], st));
 
   if (fused) {
-    wmd::launch_sinkhorn_fused(h->order.p, h->doc_ptr.p, h->ent.p, N, h->len_prefix.data(),
+    wmd::launch_sinkhorn_fused(h->sdoc.p, h->ent.p, N, h->len_prefix.data(),
                                h->max_doc_nnz, h->Mx.p, ld, v_r, h->rpad.p, lambda, iters, dist,
                                h->flags.p, h->flagged.p, h->counters.p, st);
     const int64_t nl = wmd::fused_launch_count(h->len_prefix.data(), h->max_doc_nnz, N);

@@ -52,8 +52,10 @@ void launch_final_wmd(const int32_t* order, const int32_t* doc_ptr, const Entry*
 // Returns false if the shape is not supported by the fused kernel (the caller then uses the
 // per-iteration path). `len_prefix` (host, max_len + 2 entries): len_prefix[L] = number of
 // documents with fewer than L nonzeros, i.e. bucket boundaries in the length-sorted `order`.
+int fused_ld(int v_r);  // row width of the fused path's tables: v_r rounded up to 8, 16, 32, 64
 bool fused_supported(int ld, int64_t max_doc_nnz);
-void launch_sinkhorn_fused(const int32_t* order, const int32_t* doc_ptr, const Entry* ent, int64_t N,
+// sdoc[p] = {document id, first nonzero, length, 0} of the p-th document in length order.
+void launch_sinkhorn_fused(const int4* sdoc, const Entry* ent, int64_t N,
                            const int64_t* len_prefix, int64_t max_len, const float* Mx, int ld,
                            int v_r, const float* rpad, float lambda, int iters, float* dist,
                            uint8_t* flags, int32_t* flagged_list, int32_t* flagged_count,
