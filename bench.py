@@ -311,7 +311,7 @@ def main():
                 "algorithmic_flops_per_step": flops,
                 "phase_ms": t_phase * 1e3,
                 "launches_per_step": st["iter_launches"] / args.steps,
-                "l2_gather_bytes_per_step": 2 * 4 * v_r * nnz_l,  # K~ and M rows, once
+                "l2_gather_bytes_per_step": 4 * (st["last_ld"] + 4) * nnz_l,  # one M row (+ m_k) per nonzero, once
                 "traffic": None,
                 "share_of_step": st["iter_ms"] / max(st["query_ms"], 1e-9),
             }

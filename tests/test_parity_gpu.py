@@ -474,3 +474,47 @@ def test_auto_path_selection_and_cross_path_agreement(W):
         assert W.wmd_get_stats(h)["last_path"] == W.WMD_PATH_PER_ITER
     finally:
         W.wmd_destroy(h)
+
+
+# ------------------------------------------------------------------ fused-kernel shape grid
+
+def _docs_with_lengths(V, lengths, seed, p=0.6, lo_id=0):
+    rng = np.random.default_rng(seed)
+    cdf = synth.zipf_cdf(V, 1.07)
+    docs = []
+    for L in lengths:
+        ids = set()
+        while len(ids) < L:  # Zipf ids (hot words shared across documents), distinct
+            ids.update(int(x) for x in np.searchsorted(cdf, rng.random(L - len(ids))))
+        ids = np.array(sorted(ids)[:L])
+        cnt = rng.geometric(p, L).astype(np.float64)
+        docs.append({int(k): float(x) for k, x in zip(ids, (cnt / cnt.sum()).astype(np.float32))})
+    return synth.csc_from_lists(docs, V)
+
+
+@pytest.mark.parametrize("v_r", [1, 5, 8, 9, 16, 17, 30, 32, 33, 64])
+def test_fused_bucket_and_width_grid(W, v_r):
+    """Every fused-kernel instance: ld in {8, 16, 32, 64} x length buckets {8, 16, 32, 40, 48, 64}
+    (documents at and next to each boundary, ragged counts per bucket); AUTO must pick the fused
+    path, and the distances must match the FP64 oracle."""
+    wl = synth.make_workload("tweet", n_queries=0, N=10)
+    V = wl.cfg.V
+    lengths = [1, 2, 7, 8, 9, 15, 16, 17, 31, 32, 33, 39, 40, 41, 47, 48, 49, 63, 64] * 3
+    if v_r > 32:  # the 64-wide tables keep documents of up to 48 words in registers
+        lengths = [L for L in lengths if L <= 48]
+    cp, ri, va = _docs_with_lengths(V, lengths, seed=v_r)
+    rng = np.random.default_rng(100 + v_r)
+    q = np.sort(rng.choice(2000, v_r, replace=False)).astype(np.int32)  # frequent words
+    cnt = rng.geometric(0.6, v_r).astype(np.float64)
+    w = (cnt / cnt.sum()).astype(np.float32)
+    h = W.wmd_create(wl.E)
+    try:
+        W.wmd_set_targets(h, cp, ri, va)
+        d = np.empty(cp.shape[0] - 1, np.float32)
+        W.wmd_query(h, q, w, 10.0, 15, d)
+        W.wmd_sync(h)
+        assert W.wmd_get_stats(h)["last_path"] == W.WMD_PATH_FUSED
+    finally:
+        W.wmd_destroy(h)
+    o = oracle.sinkhorn_wmd(wl.E, cp, ri, va, q, w, 10.0, 15)
+    assert_parity(d, o, f"fused grid v_r={v_r}")
