@@ -79,7 +79,7 @@ struct wmd_handle {
   // embeddings
   DevBuf<float> E;
   int64_t V = 0;
-  int32_t d = 0;
+  int32_t d = 0, dp = 0;     // dp: padded row stride of E (multiple of 32)
   // targets
   bool has_targets = false;
   DevBuf<int32_t> doc_ptr;
@@ -332,14 +332,20 @@ wmd_status wmd_create(const float* vocab_emb, int64_t V, int32_t d, int32_t devi
   auto bail = [&](wmd_status s) { wmd_destroy(h); return s; };
   if (cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking) != cudaSuccess) return bail(WMD_ERR_CUDA);
   h->stream = h->own_stream;
+  // E is kept with rows padded to dp = d rounded up to 32 floats (zeros add nothing to a
+  // distance): the build kernel streams whole 32-float chunks with 16-byte async copies.
+  const int32_t dp = (d + 31) / 32 * 32;
+  h->dp = dp;
   const size_t n = (size_t)V * d;
-  if (h->E.ensure(n) != cudaSuccess) return bail(WMD_ERR_OUT_OF_MEMORY);
+  if (h->E.ensure((size_t)V * dp) != cudaSuccess) return bail(WMD_ERR_OUT_OF_MEMORY);
+  if (cudaMemsetAsync(h->E.p, 0, (size_t)V * dp * sizeof(float), h->stream) != cudaSuccess) return bail(WMD_ERR_CUDA);
+  if (h->counters.ensure(4) != cudaSuccess) return bail(WMD_ERR_OUT_OF_MEMORY);
   if (is_device_ptr(vocab_emb)) {
-    if (cudaMemcpyAsync(h->E.p, vocab_emb, n * sizeof(float), cudaMemcpyDeviceToDevice, h->stream) != cudaSuccess)
+    if (cudaMemcpy2DAsync(h->E.p, dp * sizeof(float), vocab_emb, d * sizeof(float), d * sizeof(float), V,
+                          cudaMemcpyDeviceToDevice, h->stream) != cudaSuccess)
       return bail(WMD_ERR_CUDA);
-    if (h->counters.ensure(4) != cudaSuccess) return bail(WMD_ERR_OUT_OF_MEMORY);
     cudaMemsetAsync(h->counters.p, 0, 4 * sizeof(int32_t), h->stream);
-    wmd::launch_check_finite(h->E.p, (int64_t)n, h->counters.p + 3, h->stream);
+    wmd::launch_check_finite(h->E.p, (int64_t)V * dp, h->counters.p + 3, h->stream);
     int32_t bad = 0;
     if (cudaMemcpyAsync(&bad, h->counters.p + 3, sizeof bad, cudaMemcpyDeviceToHost, h->stream) != cudaSuccess ||
         cudaStreamSynchronize(h->stream) != cudaSuccess)
@@ -348,7 +354,9 @@ wmd_status wmd_create(const float* vocab_emb, int64_t V, int32_t d, int32_t devi
   } else {
     for (size_t i = 0; i < n; ++i)
       if (!std::isfinite(vocab_emb[i])) return bail(WMD_ERR_NONFINITE_EMBEDDING);
-    if (cudaMemcpy(h->E.p, vocab_emb, n * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess)
+    if (cudaMemcpy2DAsync(h->E.p, dp * sizeof(float), vocab_emb, d * sizeof(float), d * sizeof(float), V,
+                          cudaMemcpyHostToDevice, h->stream) != cudaSuccess ||
+        cudaStreamSynchronize(h->stream) != cudaSuccess)
       return bail(WMD_ERR_CUDA);
   }
   if (h->sel.ensure(WMD_MAX_VR) != cudaSuccess || h->rpad.ensure(WMD_MAX_VR) != cudaSuccess ||
@@ -534,7 +542,7 @@ wmd_status wmd_query(wmd_handle* h, const int32_t* query_ids, const float* query
   }
   int64_t launches = 0;
   // a2: M, K~
-  wmd::launch_build_ktilde(h->E.p, h->V, h->d, h->sel.p, v_r, ld, lambda, fused ? nullptr : h->Kt.p,
+  wmd::launch_build_ktilde(h->E.p, h->V, h->dp, h->sel.p, v_r, ld, lambda, fused ? nullptr : h->Kt.p,
                            h->Mx.p, h->colmin.p, st);
   h->kt_valid = !fused;
   ++launches;

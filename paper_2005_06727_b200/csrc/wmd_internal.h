@@ -32,7 +32,8 @@ struct QueryDev {
 // --- a2: distance + column-rescaled kernel build -------
 // Mx: V rows of ld + 4 floats [M_k0 .. M_k,ld-1 (zero beyond v_r), m_k = min_i M_ik, 0, 0, 0].
 // Kt (V x ld, K~ = exp(-lambda (M - m))) is written only when non-null (per-iteration path).
-void launch_build_ktilde(const float* E, int64_t V, int d, const int32_t* sel, int v_r, int ld,
+// E: V rows of dp floats (d padded with zeros to a multiple of 32).
+void launch_build_ktilde(const float* E, int64_t V, int dp, const int32_t* sel, int v_r, int ld,
                          float lambda, float* Kt, float* Mx, float* colmin, cudaStream_t st);
 
 // --- a4: one fused SDDMM_SpMM iteration for all documents ------------

@@ -3,7 +3,7 @@
 // All arithmetic is FP32 SIMT (no tensor cores in the sparse steps: they are gathers, not
 // contractions), except the FP64 fallback. See DESIGN.md §5 for each kernel's roofline.
 //
-//   build_ktilde      a2: M and the column-rescaled K~ = exp(-lambda (M - min_i M)) (vocab-major tables)
+//   (a2, the distance build, is in wmd_build.cu; NEXT-1, the fused kernel, in wmd_fused.cu)
 //   sddmm_spmm_iter   a4: one fused SDDMM_SpMM iteration over all documents
 //   final_wmd         a5: u/v/WMD final step
 //   fallback_fp64     a6: FP64 re-run of documents whose FP32 iterates left the normal range
@@ -26,11 +26,6 @@ __device__ __forceinline__ float dot4(float4 a, float4 b) {
 __device__ __forceinline__ void axpy4(float4& acc, float4 x, float s) {
   acc.x = fmaf(x.x, s, acc.x); acc.y = fmaf(x.y, s, acc.y);
   acc.z = fmaf(x.z, s, acc.z); acc.w = fmaf(x.w, s, acc.w);
-}
-__device__ __forceinline__ float4 shfl_xor4(float4 v, int off) {
-  v.x = __shfl_xor_sync(kFull, v.x, off); v.y = __shfl_xor_sync(kFull, v.y, off);
-  v.z = __shfl_xor_sync(kFull, v.z, off); v.w = __shfl_xor_sync(kFull, v.w, off);
-  return v;
 }
 __device__ __forceinline__ bool normal_pos(float x) { return x >= FLT_MIN && x <= FLT_MAX; }
 
@@ -60,7 +55,6 @@ __device__ __forceinline__ float4 ldg4_keep(const float4* p, uint64_t pol) {
 #define WMD_LDS(p) __ldg(p)
 #define WMD_STS(p, v) (*(p) = (v))
 #endif
-__device__ __forceinline__ float max4(float4 v) { return fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)); }
 
 // FP32 range certificate (R21). A K~ entry below FLT_MIN = 2^-126 is subnormal or
 // flushed to 0 and carries an absolute error of up to 2^-149 (a normal entry only its relative
@@ -71,108 +65,6 @@ __device__ __forceinline__ float max4(float4 v) { return fmaxf(fmaxf(v.x, v.y), 
 // a and v~, acc by 1/a) and only fires when underflowed entries could matter: the FP32 error of
 // a certified sum stays ~1e-6 relative (measured: DESIGN.md §4).
 constexpr float kUnderScale = 0x1p-133f;  // 2^-149 / 2^-16
-
-// ============================================================================================
-// a2. build_ktilde: per vocabulary word k and query row i
-//        M_ik  = sqrt(sum_t (E[sel_i,t] - E[k,t])^2)        (direct difference so
-//                                                             M_{i,sel_i} == 0 exactly)
-//        m_k   = min_i M_ik
-//        K~_ki = expf(-lambda (M_ik - m_k))   (vocab-major, ld floats; per-iteration path only)
-//        Mx_k  = [M_k0 .. M_k,ld-1, m_k, 0, 0, 0] (vocab-major, ld + 4 floats; zero beyond v_r)
-// Block: 256 threads, 64 vocabulary words x all query rows (32-row tiles), d staged through
-// shared memory in chunks of 32. Thread micro-tile: 2 rows x 4 words, float4 smem reads.
-// Bound: FP32 issue (2 flops per (i,k,t) triple, PAPER.md:260 counts 3) vs reading E once.
-// ============================================================================================
-constexpr int BK_TW = 64, BK_TI = 32, BK_DC = 32, BK_STR = BK_DC + 4, BK_LDM = 129;
-
-__global__ void __launch_bounds__(256) build_ktilde_kernel(const float* __restrict__ E, int64_t V,
-                                                           int d, const int32_t* __restrict__ sel,
-                                                           int v_r, int ld, float lambda,
-                                                           float* __restrict__ Kt,
-                                                           float* __restrict__ Mx,
-                                                           float* __restrict__ colmin) {
-  extern __shared__ __align__(16) float smem[];
-  float* Qs = smem;                          // [BK_TI][BK_STR]
-  float* Es = Qs + BK_TI * BK_STR;           // [BK_TW][BK_STR]
-  float* Ms = Es + BK_TW * BK_STR;           // [BK_TW][BK_LDM]  (word-major, row i)
-  const int tid = threadIdx.x;
-  const int tw = tid & 15, ti = tid >> 4;
-  const int64_t k0 = (int64_t)blockIdx.x * BK_TW;
-
-  for (int it0 = 0; it0 < v_r; it0 += BK_TI) {
-    float acc[2][4];
-#pragma unroll
-    for (int a = 0; a < 2; ++a)
-#pragma unroll
-      for (int s = 0; s < 4; ++s) acc[a][s] = 0.f;
-    for (int d0 = 0; d0 < d; d0 += BK_DC) {
-      for (int idx = tid; idx < BK_TI * BK_DC; idx += 256) {
-        const int r = idx / BK_DC, c = idx % BK_DC;
-        float x = 0.f;
-        if (it0 + r < v_r && d0 + c < d) x = __ldg(E + (int64_t)sel[it0 + r] * d + d0 + c);
-        Qs[r * BK_STR + c] = x;
-      }
-      for (int idx = tid; idx < BK_TW * BK_DC; idx += 256) {
-        const int w = idx / BK_DC, c = idx % BK_DC;
-        float x = 0.f;
-        if (k0 + w < V && d0 + c < d) x = __ldg(E + (k0 + w) * d + d0 + c);
-        Es[w * BK_STR + c] = x;
-      }
-      __syncthreads();
-      const int tmax = min(BK_DC, d - d0);   // padded columns are 0-0 = 0: harmless, skip anyway
-#pragma unroll 2
-      for (int t4 = 0; t4 < BK_DC; t4 += 4) {
-        if (t4 >= tmax) break;
-        const float4 q0 = *reinterpret_cast<const float4*>(Qs + ti * BK_STR + t4);
-        const float4 q1 = *reinterpret_cast<const float4*>(Qs + (ti + 16) * BK_STR + t4);
-#pragma unroll
-        for (int s = 0; s < 4; ++s) {
-          const float4 e = *reinterpret_cast<const float4*>(Es + (tw + 16 * s) * BK_STR + t4);
-          float df;
-          df = q0.x - e.x; acc[0][s] = fmaf(df, df, acc[0][s]);
-          df = q0.y - e.y; acc[0][s] = fmaf(df, df, acc[0][s]);
-          df = q0.z - e.z; acc[0][s] = fmaf(df, df, acc[0][s]);
-          df = q0.w - e.w; acc[0][s] = fmaf(df, df, acc[0][s]);
-          df = q1.x - e.x; acc[1][s] = fmaf(df, df, acc[1][s]);
-          df = q1.y - e.y; acc[1][s] = fmaf(df, df, acc[1][s]);
-          df = q1.z - e.z; acc[1][s] = fmaf(df, df, acc[1][s]);
-          df = q1.w - e.w; acc[1][s] = fmaf(df, df, acc[1][s]);
-        }
-      }
-      __syncthreads();
-    }
-#pragma unroll
-    for (int a = 0; a < 2; ++a) {
-      const int i = it0 + ti + 16 * a;
-      if (i < v_r) {
-#pragma unroll
-        for (int s = 0; s < 4; ++s) Ms[(tw + 16 * s) * BK_LDM + i] = sqrtf(acc[a][s]);
-      }
-    }
-  }
-  __syncthreads();
-
-  // Epilogue: one warp per word; lanes over query rows (coalesced row writes).
-  const int warp = tid >> 5, lane = tid & 31;
-  for (int w = warp; w < BK_TW; w += 8) {
-    const int64_t k = k0 + w;
-    if (k >= V) break;
-    const float* mrow = Ms + w * BK_LDM;
-    float mn = FLT_MAX;
-    for (int i = lane; i < v_r; i += 32) mn = fminf(mn, mrow[i]);
-#pragma unroll
-    for (int off = 16; off; off >>= 1) mn = fminf(mn, __shfl_xor_sync(kFull, mn, off));
-    const int ldx = ld + 4;  // Mx row: M_k0..M_k,ld-1 (zero beyond v_r), m_k, 3 zeros
-    for (int i = lane; i < ldx; i += 32) {
-      float m = 0.f;
-      if (i < v_r) m = mrow[i];
-      else if (i == ld) m = mn;
-      Mx[k * ldx + i] = m;
-      if (Kt && i < ld) Kt[k * ld + i] = i < v_r ? expf(-lambda * (m - mn)) : 0.f;
-    }
-    if (lane == 0) colmin[k] = mn;
-  }
-}
 
 // ============================================================================================
 // a4 + a5. sinkhorn_pass<G, U, FINAL>: one pass over all target documents.
@@ -515,18 +407,6 @@ int lanes_per_row(int ld) {
 }  // namespace
 
 // ------------------------------------------------------------------------------ launchers
-void launch_build_ktilde(const float* E, int64_t V, int d, const int32_t* sel, int v_r, int ld,
-                         float lambda, float* Kt, float* Mt, float* colmin, cudaStream_t st) {
-  const size_t smem = sizeof(float) * (BK_TI * BK_STR + BK_TW * BK_STR + BK_TW * BK_LDM);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(build_ktilde_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
-  const int64_t grid = (V + BK_TW - 1) / BK_TW;
-  build_ktilde_kernel<<<(unsigned)grid, 256, smem, st>>>(E, V, d, sel, v_r, ld, lambda, Kt, Mt, colmin);
-}
-
 // U = nonzeros per group per step: U = G up to 8 so that the transpose-reduce leaves exactly one
 // nonzero per lane (fewer lanes idle); (32/G) documents per warp.
 #define WMD_DISPATCH_G(ld, MACRO) \
