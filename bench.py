@@ -169,6 +169,102 @@ def config_dict(cfg, wl, args, **extra):
     return d
 
 
+def run_many(args, wl):
+    """BASELINE config "Many queries": 256 queries (v_r 15..40) against 200k tweet-like documents,
+    K rebuilt per query; one step = the whole batch. Query-parallel across ranks (NEXT-2 (i):
+    every rank holds all documents, queries g, g+P, ...; one all-gather of the distance rows)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2005_06727_b200 import wmd
+    from paper_2005_06727_b200.sharded import QueryParallelEngine
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+    cfg = wl.cfg
+    queries = wl.queries
+    nq = len(queries)
+    path = {"auto": wmd.WMD_PATH_AUTO, "iter": wmd.WMD_PATH_PER_ITER, "fused": wmd.WMD_PATH_FUSED}[args.path]
+    E = torch.from_numpy(wl.E).cuda()
+    eng = QueryParallelEngine(E, wl.col_ptr, wl.row_idx, wl.val, rank, world, local_rank, path=path)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        out = eng.query_batch(queries, cfg.lam, cfg.iters)
+    torch.cuda.synchronize()
+    eng.engine.sync()
+    wmd.wmd_reset_stats(eng.engine.h)
+    flush = torch.empty(256 * 2 ** 20 // 4, dtype=torch.float32, device="cuda")
+    t_ms = 0.0
+    with ClockSampler(local_rank) as clk:
+        for s in range(args.steps):
+            flush.fill_(float(s))
+            barrier()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            out = eng.query_batch(queries, cfg.lam, cfg.iters)
+            b.record(stream)
+            torch.cuda.synchronize()
+            t_ms += a.elapsed_time(b)
+    barrier()
+    eng.engine.sync()
+    launches = int(wmd.wmd_get_stats(eng.engine.h)["kernel_launches"])
+    t = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    T = float(t.item()) / 1e3
+    units = sum(wl.nnz * len(q) * cfg.iters for q, _ in queries) * args.steps
+    assert bool(torch.isfinite(out).all()), "non-finite distances"
+    # e2e: the same batch through the C ABI from host query arrays into pinned host rows
+    # (rank-local rows; the all-gather is device-side and already in `value`)
+    pin = torch.empty((len(range(rank, nq, world)), wl.N), dtype=torch.float32, pin_memory=True)
+    mine = [queries[q] for q in range(rank, nq, world)]
+    e2e_ms = 0.0
+    for s in range(args.warmup + args.steps):
+        barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        if mine:
+            wmd.wmd_query_batch(eng.engine.h, mine, cfg.lam, cfg.iters, pin)
+        b.record(stream)
+        torch.cuda.synchronize()
+        if s >= args.warmup:
+            e2e_ms += a.elapsed_time(b)
+    e = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(e, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": units / T, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded Zipf bag-of-words, N(0,1) embeddings; BASELINE.json config)",
+            "config": dict(config_dict(cfg, wl, args, path=args.path), queries=nq,
+                           v_r=f"{min(len(q) for q, _ in queries)}-{max(len(q) for q, _ in queries)}",
+                           parallelism=f"query-parallel x{world}" if world > 1 else "1 GPU"),
+            "queries_per_s": nq * args.steps / T,
+            "e2e": {"value": units / (float(e.item()) / 1e3), "unit": UNIT,
+                    "h2d_bytes_per_step": int(sum(8 * len(q) for q, _ in mine)),
+                    "d2h_bytes_per_step": int(4 * len(mine) * wl.N)},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -184,6 +280,8 @@ def main():
     wl = synth.make_workload(args.config)
     if args.impl == "reference":
         return run_reference(args, wl)
+    if args.config == "many":
+        return run_many(args, wl)
 
     import torch
     import torch.distributed as dist

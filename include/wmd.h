@@ -132,6 +132,20 @@ WMD_API wmd_status wmd_set_targets(wmd_handle* h, const int64_t* col_ptr, const 
 WMD_API wmd_status wmd_query(wmd_handle* h, const int32_t* query_ids, const float* query_weights,
                      int32_t n, float lambda, int32_t iters, float* out_dist);
 
+/* A batch of nq queries against the same targets in one call (many
+ * queries, PAPER.md:12 "one tweet vs a day of tweets", :255 per-query runs). Query q is
+ * query_ids[q_ptr[q] .. q_ptr[q+1]) with weights at the same positions (HOST arrays, each query
+ * as in wmd_query); q_ptr: nq+1 int64 offsets, q_ptr[0] == 0, non-decreasing.
+ * out_dist: nq x N floats row-major (row q = query q), host or device as in wmd_query.
+ * Every query is validated before any work is enqueued (all-or-nothing; the message names the
+ * first bad query). The rows of all queries go to the device in one copy; the queries then run
+ * back to back on the handle's stream (each: build, Sinkhorn, final, FP64 fallback), with no
+ * host round trip between them. Results equal nq separate wmd_query calls bit for bit.
+ * Errors: as wmd_query, plus INVALID_ARGUMENT for nq < 1 or bad q_ptr. */
+WMD_API wmd_status wmd_query_batch(wmd_handle* h, const int32_t* query_ids, const float* query_weights,
+                           const int64_t* q_ptr, int32_t nq, float lambda, int32_t iters,
+                           float* out_dist);
+
 /* Wait for the handle's stream; return a latched deferred status (then clear it). */
 WMD_API wmd_status wmd_sync(wmd_handle* h);
 

@@ -106,8 +106,16 @@ struct wmd_handle {
   void* stage[2] = {nullptr, nullptr};
   cudaEvent_t stage_ev[2] = {nullptr, nullptr};
   int stage_slot = 0;
+  // batched queries (wmd_query_batch): device rows, pinned staging, host-output buffer
+  DevBuf<int32_t> bsel;
+  DevBuf<float> brpad, batch_dist;
+  void* batch_stage = nullptr;
+  size_t batch_stage_bytes = 0;
+  cudaEvent_t batch_ev = nullptr;
   // last query
   int32_t v_r = 0, ld = 0, path_used = 0;
+  const int32_t* last_sel = nullptr;
+  const float* last_r = nullptr;
   bool u_valid = false;
   const float* u_last = nullptr;
   std::vector<int32_t> h_sel;
@@ -362,6 +370,7 @@ wmd_status wmd_create(const float* vocab_emb, int64_t V, int32_t d, int32_t devi
   if (h->sel.ensure(WMD_MAX_VR) != cudaSuccess || h->rpad.ensure(WMD_MAX_VR) != cudaSuccess ||
       h->colmin.ensure((size_t)V) != cudaSuccess || h->counters.ensure(4) != cudaSuccess)
     return bail(WMD_ERR_OUT_OF_MEMORY);
+  if (cudaEventCreateWithFlags(&h->batch_ev, cudaEventDisableTiming) != cudaSuccess) return bail(WMD_ERR_CUDA);
   for (int s = 0; s < 2; ++s) {
     if (cudaMallocHost(&h->stage[s], WMD_MAX_VR * 8) != cudaSuccess) return bail(WMD_ERR_OUT_OF_MEMORY);
     if (cudaEventCreateWithFlags(&h->stage_ev[s], cudaEventDisableTiming) != cudaSuccess) return bail(WMD_ERR_CUDA);
@@ -378,6 +387,9 @@ void wmd_destroy(wmd_handle* h) {
   if (h->stream && h->stream != h->own_stream) cudaStreamSynchronize(h->stream);
   for (auto& pe : h->events)
     for (auto& e : pe.ev) cudaEventDestroy(e);
+  if (h->batch_stage) cudaFreeHost(h->batch_stage);
+  if (h->batch_ev) cudaEventDestroy(h->batch_ev);
+  h->bsel.release(); h->brpad.release(); h->batch_dist.release();
   for (int s = 0; s < 2; ++s) {
     if (h->stage[s]) cudaFreeHost(h->stage[s]);
     if (h->stage_ev[s]) cudaEventDestroy(h->stage_ev[s]);
@@ -483,54 +495,35 @@ wmd_status wmd_set_targets(wmd_handle* h, const int64_t* col_ptr, const int32_t*
   return WMD_OK;
 }
 
-wmd_status wmd_query(wmd_handle* h, const int32_t* query_ids, const float* query_weights,
-                     int32_t n, float lambda, int32_t iters, float* out_dist) {
-  if (!h) return WMD_ERR_INVALID_ARGUMENT;
-  h->err.clear();
-  if (!h->has_targets) return fail(h, WMD_ERR_STATE, "wmd_query before wmd_set_targets");
-  if (!out_dist || !(lambda > 0.f) || !std::isfinite(lambda) || iters < 0)
-    return fail(h, WMD_ERR_INVALID_ARGUMENT, "out_dist NULL, lambda not finite > 0, or iters < 0");
-  int64_t bad = -1;
-  std::string msg;
-  wmd_status s = validate_query(query_ids, query_weights, n, h->V, &bad, &msg, &h->h_sel, &h->h_r);
-  if (s != WMD_OK) return fail(h, s, "%s", msg.c_str());
-  DeviceGuard g(h->device);
-  if (!g.ok) return fail(h, WMD_ERR_CUDA, "cudaSetDevice failed");
+}  // extern "C"
 
-  const int32_t v_r = n;
+namespace {
+
+// Enqueue one validated query whose sorted rows sel (device, v_r ids) and r (device, zero padded
+// to WMD_MAX_VR) are already on the device: a2 build, a4/a5 (fused or per iteration), a6.
+// dist: device, N floats. Asynchronous on the handle's stream.
+wmd_status enqueue_query(wmd_handle* h, const int32_t* d_sel, const float* d_r, int32_t v_r,
+                         float lambda, int32_t iters, float* dist) {
   const int64_t N = h->N;
   // fused path: ld = v_r rounded up to a power of two (the 2-D lane tiling); per-iteration
   // path: v_r rounded up to 8
   const bool fused = (h->opt_path == WMD_PATH_FUSED || h->opt_path == WMD_PATH_AUTO) &&
-                     wmd::fused_supported(wmd::fused_ld(n), h->max_doc_nnz);
+                     wmd::fused_supported(wmd::fused_ld(v_r), h->max_doc_nnz);
   if (h->opt_path == WMD_PATH_FUSED && !fused)
-    return fail(h, WMD_ERR_INVALID_ARGUMENT, "fused path does not support v_r=%d, max doc nnz=%lld", n,
+    return fail(h, WMD_ERR_INVALID_ARGUMENT, "fused path does not support v_r=%d, max doc nnz=%lld", v_r,
                 (long long)h->max_doc_nnz);
-  const int32_t ld = fused ? wmd::fused_ld(n) : round_up8(n);
+  const int32_t ld = fused ? wmd::fused_ld(v_r) : round_up8(v_r);
   // +128 floats: the pass kernels gather unpredicated float4s up to 4*32 floats past a row
   if (!fused) CK(h, h->Kt.ensure((size_t)h->V * ld + 128));
   CK(h, h->Mx.ensure((size_t)h->V * (ld + 4) + 128));
-  CK(h, h->ua.ensure((size_t)N * ld));
-  CK(h, h->ub.ensure((size_t)N * ld));
-  CK(h, h->umask.ensure((size_t)N * ((ld + 31) / 32)));
+  if (!fused) {
+    CK(h, h->ua.ensure((size_t)N * ld));
+    CK(h, h->ub.ensure((size_t)N * ld));
+    CK(h, h->umask.ensure((size_t)N * ((ld + 31) / 32)));
+  }
   cudaStream_t st = h->stream;
-
-  // Upload (sel, r padded with zeros to ld) from pinned staging, double-buffered.
-  const int slot = h->stage_slot;
-  h->stage_slot ^= 1;
-  CK(h, cudaEventSynchronize(h->stage_ev[slot]));
-  int32_t* ssel = (int32_t*)h->stage[slot];
-  float* sr = (float*)((char*)h->stage[slot] + WMD_MAX_VR * 4);
-  std::memset(h->stage[slot], 0, WMD_MAX_VR * 8);
-  for (int32_t i = 0; i < v_r; ++i) { ssel[i] = h->h_sel[i]; sr[i] = h->h_r[i]; }
-  CK(h, cudaMemcpyAsync(h->sel.p, ssel, WMD_MAX_VR * 4, cudaMemcpyHostToDevice, st));
-  CK(h, cudaMemcpyAsync(h->rpad.p, sr, WMD_MAX_VR * 4, cudaMemcpyHostToDevice, st));
-  CK(h, cudaEventRecord(h->stage_ev[slot], st));
   CK(h, cudaMemsetAsync(h->flags.p, 0, N, st));
   CK(h, cudaMemsetAsync(h->counters.p, 0, sizeof(int32_t), st));  // flagged-list length
-
-  const bool dev_out = is_device_ptr(out_dist);
-  float* dist = dev_out ? out_dist : h->dist_tmp.p;
 
   PhaseEvents* pe = nullptr;
   if (h->opt_timing) {
@@ -541,8 +534,8 @@ wmd_status wmd_query(wmd_handle* h, const int32_t* query_ids, const float* query
     CK(h, cudaEventRecord(pe->ev[0], st));
   }
   int64_t launches = 0;
-  // a2: M, K~
-  wmd::launch_build_ktilde(h->E.p, h->V, h->dp, h->sel.p, v_r, ld, lambda, fused ? nullptr : h->Kt.p,
+  // a2: M (+ m), and K~ for the per-iteration path
+  wmd::launch_build_ktilde(h->E.p, h->V, h->dp, d_sel, v_r, ld, lambda, fused ? nullptr : h->Kt.p,
                            h->Mx.p, h->colmin.p, st);
   h->kt_valid = !fused;
   ++launches;
@@ -550,7 +543,7 @@ wmd_status wmd_query(wmd_handle* h, const int32_t* query_ids, const float* query
 
   if (fused) {
     wmd::launch_sinkhorn_fused(h->sdoc.p, h->ent.p, N, h->len_prefix.data(),
-                               h->max_doc_nnz, h->Mx.p, ld, v_r, h->rpad.p, lambda, iters, dist,
+                               h->max_doc_nnz, h->Mx.p, ld, v_r, d_r, lambda, iters, dist,
                                h->flags.p, h->flagged.p, h->counters.p, st);
     const int64_t nl = wmd::fused_launch_count(h->len_prefix.data(), h->max_doc_nnz, N);
     launches += nl;
@@ -564,7 +557,7 @@ wmd_status wmd_query(wmd_handle* h, const int32_t* query_ids, const float* query
     float* bufs[2] = {h->ua.p, h->ub.p};
     for (int32_t t = 0; t < iters; ++t) {
       float* u_out = bufs[t & 1];
-      wmd::launch_sddmm_spmm_iter(h->order.p, h->doc_ptr.p, h->ent.p, N, h->Kt.p, ld, v_r, h->rpad.p, u_in, u_out,
+      wmd::launch_sddmm_spmm_iter(h->order.p, h->doc_ptr.p, h->ent.p, N, h->Kt.p, ld, v_r, d_r, u_in, u_out,
                                   h->umask.p, h->flags.p, st);
       u_in = u_out;
     }
@@ -572,7 +565,7 @@ wmd_status wmd_query(wmd_handle* h, const int32_t* query_ids, const float* query
     h->st.iter_launches += iters;
     if (pe) CK(h, cudaEventRecord(pe->ev[2], st));
     // a5
-    wmd::launch_final_wmd(h->order.p, h->doc_ptr.p, h->ent.p, N, h->Kt.p, h->Mx.p, ld, v_r, h->rpad.p, u_in,
+    wmd::launch_final_wmd(h->order.p, h->doc_ptr.p, h->ent.p, N, h->Kt.p, h->Mx.p, ld, v_r, d_r, u_in,
                           h->umask.p, dist, h->flags.p, h->flagged.p, h->counters.p, st);
     ++launches;
     if (pe) CK(h, cudaEventRecord(pe->ev[3], st));
@@ -582,7 +575,7 @@ wmd_status wmd_query(wmd_handle* h, const int32_t* query_ids, const float* query
   }
   // a6: FP64 re-run of flagged documents (device-side list; zero-cost when empty)
   if (h->opt_fallback) {
-    wmd::launch_fallback_fp64(h->Mx.p, h->colmin.p, ld, h->rpad.p, v_r, (double)lambda, iters, h->doc_ptr.p,
+    wmd::launch_fallback_fp64(h->Mx.p, h->colmin.p, ld, d_r, v_r, (double)lambda, iters, h->doc_ptr.p,
                               h->ent.p, h->flagged.p, h->counters.p, h->fb_scratch.p, h->max_doc_nnz, dist,
                               h->flags.p, h->counters.p + 1, h->counters.p + 2, st);
     ++launches;
@@ -591,13 +584,120 @@ wmd_status wmd_query(wmd_handle* h, const int32_t* query_ids, const float* query
   CK(h, cudaGetLastError());
   h->v_r = v_r;
   h->ld = ld;
+  h->last_sel = d_sel;
+  h->last_r = d_r;
   h->st.queries += 1;
   h->st.kernel_launches += launches;
   h->st.last_v_r = v_r;
   h->st.last_ld = ld;
   h->st.last_path = h->path_used;
+  return WMD_OK;
+}
+
+wmd_status check_query_args(wmd_handle* h, const void* out_dist, float lambda, int32_t iters) {
+  if (!h->has_targets) return fail(h, WMD_ERR_STATE, "query before wmd_set_targets");
+  if (!out_dist || !(lambda > 0.f) || !std::isfinite(lambda) || iters < 0)
+    return fail(h, WMD_ERR_INVALID_ARGUMENT, "out_dist NULL, lambda not finite > 0, or iters < 0");
+  return WMD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+wmd_status wmd_query(wmd_handle* h, const int32_t* query_ids, const float* query_weights,
+                     int32_t n, float lambda, int32_t iters, float* out_dist) {
+  if (!h) return WMD_ERR_INVALID_ARGUMENT;
+  h->err.clear();
+  wmd_status s = check_query_args(h, out_dist, lambda, iters);
+  if (s != WMD_OK) return s;
+  int64_t bad = -1;
+  std::string msg;
+  s = validate_query(query_ids, query_weights, n, h->V, &bad, &msg, &h->h_sel, &h->h_r);
+  if (s != WMD_OK) return fail(h, s, "%s", msg.c_str());
+  DeviceGuard g(h->device);
+  if (!g.ok) return fail(h, WMD_ERR_CUDA, "cudaSetDevice failed");
+  cudaStream_t st = h->stream;
+
+  // Upload (sel, r padded with zeros) from pinned staging, double-buffered.
+  const int slot = h->stage_slot;
+  h->stage_slot ^= 1;
+  CK(h, cudaEventSynchronize(h->stage_ev[slot]));
+  int32_t* ssel = (int32_t*)h->stage[slot];
+  float* sr = (float*)((char*)h->stage[slot] + WMD_MAX_VR * 4);
+  std::memset(h->stage[slot], 0, WMD_MAX_VR * 8);
+  for (int32_t i = 0; i < n; ++i) { ssel[i] = h->h_sel[i]; sr[i] = h->h_r[i]; }
+  CK(h, cudaMemcpyAsync(h->sel.p, ssel, WMD_MAX_VR * 4, cudaMemcpyHostToDevice, st));
+  CK(h, cudaMemcpyAsync(h->rpad.p, sr, WMD_MAX_VR * 4, cudaMemcpyHostToDevice, st));
+  CK(h, cudaEventRecord(h->stage_ev[slot], st));
+
+  const bool dev_out = is_device_ptr(out_dist);
+  float* dist = dev_out ? out_dist : h->dist_tmp.p;
+  s = enqueue_query(h, h->sel.p, h->rpad.p, n, lambda, iters, dist);
+  if (s != WMD_OK) return s;
   if (!dev_out) {
-    CK(h, cudaMemcpyAsync(out_dist, dist, N * sizeof(float), cudaMemcpyDeviceToHost, st));
+    CK(h, cudaMemcpyAsync(out_dist, dist, h->N * sizeof(float), cudaMemcpyDeviceToHost, st));
+    CK(h, cudaStreamSynchronize(st));
+  }
+  return WMD_OK;
+}
+
+wmd_status wmd_query_batch(wmd_handle* h, const int32_t* query_ids, const float* query_weights,
+                           const int64_t* q_ptr, int32_t nq, float lambda, int32_t iters,
+                           float* out_dist) {
+  if (!h) return WMD_ERR_INVALID_ARGUMENT;
+  h->err.clear();
+  wmd_status s = check_query_args(h, out_dist, lambda, iters);
+  if (s != WMD_OK) return s;
+  if (nq < 1 || !q_ptr || q_ptr[0] != 0) return fail(h, WMD_ERR_INVALID_ARGUMENT, "nq < 1 or q_ptr[0] != 0");
+  for (int32_t q = 0; q < nq; ++q)
+    if (q_ptr[q + 1] < q_ptr[q]) return fail(h, WMD_ERR_INVALID_ARGUMENT, "q_ptr decreases at query %d", q);
+  DeviceGuard g(h->device);
+  if (!g.ok) return fail(h, WMD_ERR_CUDA, "cudaSetDevice failed");
+  cudaStream_t st = h->stream;
+  // validate and sort every query before any work is enqueued (all-or-nothing)
+  CK(h, cudaEventSynchronize(h->batch_ev));  // the previous batch's upload has left the staging
+  const size_t need = (size_t)nq * WMD_MAX_VR * 8;
+  if (h->batch_stage_bytes < need) {
+    if (h->batch_stage) cudaFreeHost(h->batch_stage);
+    h->batch_stage = nullptr;
+    h->batch_stage_bytes = 0;
+    CK(h, cudaMallocHost(&h->batch_stage, need));
+    h->batch_stage_bytes = need;
+  }
+  int32_t* ssel = (int32_t*)h->batch_stage;
+  float* sr = (float*)((char*)h->batch_stage + (size_t)nq * WMD_MAX_VR * 4);
+  std::memset(h->batch_stage, 0, need);
+  std::vector<int32_t> nrow(nq);
+  for (int32_t q = 0; q < nq; ++q) {
+    int64_t bad = -1;
+    std::string msg;
+    const int64_t n = q_ptr[q + 1] - q_ptr[q];
+    if (n > WMD_MAX_VR) return fail(h, WMD_ERR_INVALID_ARGUMENT, "query %d: v_r > WMD_MAX_VR", q);
+    s = validate_query(query_ids + q_ptr[q], query_weights + q_ptr[q], (int32_t)n, h->V, &bad, &msg,
+                       &h->h_sel, &h->h_r);
+    if (s != WMD_OK) return fail(h, s, "query %d: %s", q, msg.c_str());
+    nrow[q] = (int32_t)n;
+    for (int64_t i = 0; i < n; ++i) {
+      ssel[(size_t)q * WMD_MAX_VR + i] = h->h_sel[i];
+      sr[(size_t)q * WMD_MAX_VR + i] = h->h_r[i];
+    }
+  }
+  CK(h, h->bsel.ensure((size_t)nq * WMD_MAX_VR));
+  CK(h, h->brpad.ensure((size_t)nq * WMD_MAX_VR));
+  CK(h, cudaMemcpyAsync(h->bsel.p, ssel, (size_t)nq * WMD_MAX_VR * 4, cudaMemcpyHostToDevice, st));
+  CK(h, cudaMemcpyAsync(h->brpad.p, sr, (size_t)nq * WMD_MAX_VR * 4, cudaMemcpyHostToDevice, st));
+  CK(h, cudaEventRecord(h->batch_ev, st));
+  const bool dev_out = is_device_ptr(out_dist);
+  if (!dev_out) CK(h, h->batch_dist.ensure((size_t)nq * h->N));
+  float* dist = dev_out ? out_dist : h->batch_dist.p;
+  for (int32_t q = 0; q < nq; ++q) {
+    s = enqueue_query(h, h->bsel.p + (size_t)q * WMD_MAX_VR, h->brpad.p + (size_t)q * WMD_MAX_VR, nrow[q],
+                      lambda, iters, dist + (size_t)q * h->N);
+    if (s != WMD_OK) return s;
+  }
+  if (!dev_out) {
+    CK(h, cudaMemcpyAsync(out_dist, dist, (size_t)nq * h->N * sizeof(float), cudaMemcpyDeviceToHost, st));
     CK(h, cudaStreamSynchronize(st));
   }
   return WMD_OK;
@@ -656,8 +756,8 @@ wmd_status wmd_get_query_rows(wmd_handle* h, int32_t* sel, float* r) {
   if (h->st.queries == 0) return fail(h, WMD_ERR_STATE, "no query yet");
   DeviceGuard g(h->device);
   CK(h, cudaStreamSynchronize(h->stream));
-  CK(h, cudaMemcpy(sel, h->sel.p, h->v_r * sizeof(int32_t), cudaMemcpyDeviceToHost));
-  CK(h, cudaMemcpy(r, h->rpad.p, h->v_r * sizeof(float), cudaMemcpyDeviceToHost));
+  CK(h, cudaMemcpy(sel, h->last_sel, h->v_r * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  CK(h, cudaMemcpy(r, h->last_r, h->v_r * sizeof(float), cudaMemcpyDeviceToHost));
   return WMD_OK;
 }
 

@@ -10,6 +10,11 @@ The one exchange step is the output: a padded all_gather_into_tensor of the FP32
 The embeddings and the per-query K~ table are replicated (each rank builds its own K~: no
 traffic). Per-document arithmetic does not depend on shard membership, so the distances are
 bitwise identical for every world size.
+
+QueryParallelEngine is the other decomposition, for many queries
+against the same corpus: every rank holds all documents and runs whole queries (q = rank,
+rank + P, ...), so there is neither a replicated distance build nor a per-query exchange; one
+all-gather of the finished distance rows at the end of a batch.
 """
 from __future__ import annotations
 
@@ -99,3 +104,53 @@ class ShardedEngine:
     def close(self):
         if self.engine is not None:
             self.engine.close()
+
+
+def query_assignment(nq: int, world: int, rank: int) -> np.ndarray:
+    """Queries of one rank in the query-parallel decomposition: q = rank, rank + P, ..."""
+    return np.arange(rank, nq, world, dtype=np.int64)
+
+
+def gather_query_rows(local, nq: int, world: int, group=None):
+    """All-gather the ranks' query rows (local: (len(query_assignment(nq, P, rank)), N) tensor)
+    into the (nq, N) result in query order: one padded all_gather_into_tensor, then the
+    row interleave out[q] = buf[q % P][q // P]."""
+    import torch
+    import torch.distributed as dist
+
+    per = (nq + world - 1) // world
+    N = local.shape[1]
+    send = torch.zeros((per, N), dtype=local.dtype, device=local.device)
+    send[: local.shape[0]] = local
+    buf = torch.empty((world * per, N), dtype=local.dtype, device=local.device)
+    dist.all_gather_into_tensor(buf, send, group=group)
+    q = np.arange(nq)
+    idx = torch.from_numpy(((q % world) * per + q // world).astype(np.int64)).to(local.device)
+    return torch.index_select(buf, 0, idx)
+
+
+class QueryParallelEngine:
+    """One rank's view of the query-parallel decomposition: all documents, a share of queries."""
+
+    def __init__(self, vocab_emb, col_ptr, row_idx, val, rank: int, world: int, device: int,
+                 group=None, path: int = wmd.WMD_PATH_AUTO, timing: bool = False):
+        self.rank, self.world, self.group = rank, world, group
+        self.N = int(np.shape(col_ptr)[0]) - 1
+        self.engine = wmd.Engine(vocab_emb, device=device, path=path, timing=timing)
+        self.engine.set_targets(col_ptr, row_idx, val)
+
+    def query_batch(self, queries, lam: float, iters: int, gather: bool = True):
+        """Distances (len(queries), N) in query order on every rank (gather=True), else this
+        rank's rows (queries rank, rank + P, ...)."""
+        import torch
+        mine = query_assignment(len(queries), self.world, self.rank)
+        if mine.shape[0]:
+            local = self.engine.query_batch([queries[q] for q in mine], lam, iters)
+        else:
+            local = torch.empty((0, self.N), dtype=torch.float32, device=f"cuda:{self.engine.device}")
+        if not gather or self.world == 1:
+            return local
+        return gather_query_rows(local, len(queries), self.world, self.group)
+
+    def close(self):
+        self.engine.close()

@@ -38,7 +38,8 @@ WMD_PATH_AUTO, WMD_PATH_PER_ITER, WMD_PATH_FUSED = 0, 1, 2
 WMD_OPT_PATH, WMD_OPT_TIMING, WMD_OPT_FALLBACK, WMD_OPT_GRAPH = 1, 2, 3, 4
 
 EXPORTED = (
-    "wmd_create", "wmd_set_stream", "wmd_set_option", "wmd_set_targets", "wmd_query", "wmd_sync",
+    "wmd_create", "wmd_set_stream", "wmd_set_option", "wmd_set_targets", "wmd_query",
+    "wmd_query_batch", "wmd_sync",
     "wmd_partition", "wmd_validate_csc", "wmd_validate_query", "wmd_get_stats", "wmd_reset_stats",
     "wmd_get_query_rows", "wmd_read_kernel", "wmd_read_scaling", "wmd_read_flags",
     "wmd_status_string", "wmd_last_error", "wmd_version", "wmd_destroy",
@@ -71,6 +72,7 @@ def _load():
         "wmd_set_option": [P, I32, I64],
         "wmd_set_targets": [P, P, P, P, I64, I64],
         "wmd_query": [P, P, P, I32, ctypes.c_float, I32, P],
+        "wmd_query_batch": [P, P, P, P, I32, ctypes.c_float, I32, P],
         "wmd_sync": [P],
         "wmd_partition": [P, I64, I32, P],
         "wmd_validate_csc": [P, P, P, I64, I64, I64, P],
@@ -188,6 +190,19 @@ def wmd_query(h, query_ids, query_weights, lam: float, iters: int, out_dist) -> 
     _check(lib.wmd_query(h, pi, pw, n, float(lam), int(iters), po), h)
 
 
+def wmd_query_batch(h, queries, lam: float, iters: int, out_dist) -> None:
+    """queries: list of (ids, weights) host arrays. out_dist: (nq, N) floats, host or device."""
+    ids = np.concatenate([np.asarray(q, np.int32) for q, _ in queries]) if queries else np.empty(0, np.int32)
+    ws = np.concatenate([np.asarray(w, np.float32) for _, w in queries]) if queries else np.empty(0, np.float32)
+    qp = np.zeros(len(queries) + 1, np.int64)
+    qp[1:] = np.cumsum([np.asarray(q).shape[0] for q, _ in queries])
+    pi, k1 = _ptr(ids, np.int32)
+    pw, k2 = _ptr(ws, np.float32)
+    pq, k3 = _ptr(qp, np.int64)
+    po, k4 = _ptr(out_dist, np.float32)
+    _check(lib.wmd_query_batch(h, pi, pw, pq, len(queries), float(lam), int(iters), po), h)
+
+
 def wmd_sync(h) -> None:
     _check(lib.wmd_sync(h), h)
 
@@ -299,6 +314,14 @@ class Engine:
         if out is None:
             out = torch.empty(self.N, dtype=torch.float32, device=f"cuda:{self.device}")
         wmd_query(self.h, ids, weights, lam, iters, out)
+        return out
+
+    def query_batch(self, queries, lam: float, iters: int, out=None):
+        """queries: list of (ids, weights); returns a CUDA (len(queries), N) float32 tensor."""
+        torch = self._torch
+        if out is None:
+            out = torch.empty((len(queries), self.N), dtype=torch.float32, device=f"cuda:{self.device}")
+        wmd_query_batch(self.h, queries, lam, iters, out)
         return out
 
     def sync(self):

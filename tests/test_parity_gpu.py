@@ -518,3 +518,50 @@ def test_fused_bucket_and_width_grid(W, v_r):
         W.wmd_destroy(h)
     o = oracle.sinkhorn_wmd(wl.E, cp, ri, va, q, w, 10.0, 15)
     assert_parity(d, o, f"fused grid v_r={v_r}")
+
+
+# ------------------------------------------------------------------ NEXT-2: query batches
+
+def test_query_batch_equals_single_queries_and_oracle(W):
+    """wmd_query_batch (host and device outputs) == back-to-back wmd_query bit for bit, and
+    within tolerance of the oracle; varying v_r (15..40, the Many config's range) per query."""
+    import torch
+    wl = synth.make_workload("many", n_queries=6, N=3000)
+    qs = wl.queries
+    h = W.wmd_create(wl.E)
+    try:
+        W.wmd_set_targets(h, wl.col_ptr, wl.row_idx, wl.val)
+        single = np.empty((len(qs), wl.N), np.float32)
+        for i, (q, w) in enumerate(qs):
+            W.wmd_query(h, q, w, 10.0, 15, single[i])
+        host = np.empty((len(qs), wl.N), np.float32)
+        W.wmd_query_batch(h, qs, 10.0, 15, host)
+        dev = torch.empty((len(qs), wl.N), dtype=torch.float32, device="cuda:0")
+        W.wmd_set_stream(h, torch.cuda.current_stream())
+        W.wmd_query_batch(h, qs, 10.0, 15, dev)
+        torch.cuda.synchronize()
+        W.wmd_sync(h)
+        assert W.wmd_get_stats(h)["queries"] == 3 * len(qs)
+    finally:
+        W.wmd_destroy(h)
+    assert np.array_equal(host, single)
+    assert np.array_equal(dev.cpu().numpy(), single)
+    for i in (0, len(qs) - 1):
+        o = oracle.sinkhorn_wmd(wl.E, wl.col_ptr, wl.row_idx, wl.val, *qs[i], 10.0, 15)
+        assert_parity(single[i], o, f"batch query {i}")
+
+
+def test_query_batch_validates_all_before_enqueueing(W):
+    wl = synth.make_workload("tiny", n_queries=3)
+    qs = list(wl.queries)
+    bad = (np.array([1, 1], np.int32), np.array([0.5, 0.5], np.float32))  # duplicate id
+    h = W.wmd_create(wl.E)
+    try:
+        W.wmd_set_targets(h, wl.col_ptr, wl.row_idx, wl.val)
+        out = np.zeros((4, wl.N), np.float32)
+        with pytest.raises(W.WmdError) as e:
+            W.wmd_query_batch(h, qs + [bad], 10.0, 15, out)
+        assert e.value.status == W.WMD_ERR_BAD_WEIGHTS and "query 3" in str(e.value)
+        assert W.wmd_get_stats(h)["queries"] == 0 and not out.any()
+    finally:
+        W.wmd_destroy(h)
