@@ -51,6 +51,10 @@ def _load():
                                         ctypes.c_double, ctypes.c_int32, ctypes.c_double,
                                         P, P, P, P]
         lib.oracle_partition.argtypes = [P, ctypes.c_int64, ctypes.c_int32, P]
+        lib.oracle_sinkhorn_per_doc.argtypes = [P, ctypes.c_int64, ctypes.c_int32, P, P, P, ctypes.c_int64,
+                                                P, P, ctypes.c_int32, ctypes.c_double, ctypes.c_int32,
+                                                ctypes.c_double, P, P]
+        lib.oracle_sinkhorn_per_doc.restype = ctypes.c_int
         for f in (lib.oracle_euclidean_rows, lib.oracle_select_nonzero, lib.oracle_sinkhorn,
                   lib.oracle_partition):
             f.restype = ctypes.c_int
@@ -126,6 +130,27 @@ def sinkhorn_wmd(E, col_ptr, row_idx, val, q_ids, q_w, lam, iters, *, dense=Fals
     v_r = sel.shape[0]
     uu = u.reshape(-1)[: N * v_r].reshape(N, v_r).copy()
     return out, dict(u=uu, v=v[:nnz].copy(), iters_run=it.value, sel=sel, r=r)
+
+
+def sinkhorn_wmd_per_doc(E, col_ptr, row_idx, val, q_ids, q_w, lam, max_iter, tol_rel):
+    """Algorithm 1 with a per-document "while x changes" stop (oracle_sinkhorn_per_doc):
+    doc j stops after the first x-update with max_i |x_new/x - 1| <= tol_rel (tol_rel < 0:
+    never), capped at max_iter. Returns (float64[N] distances, int32[N] x-updates per doc)."""
+    E = _c(E, np.float32)
+    col_ptr = _c(col_ptr, np.int64)
+    row_idx = _c(row_idx, np.int32)
+    val = _c(val, np.float32)
+    q_ids = _c(q_ids, np.int32)
+    q_w = _c(q_w, np.float32)
+    N = col_ptr.shape[0] - 1
+    out = np.empty(N, np.float64)
+    its = np.empty(N, np.int32)
+    rc = _load().oracle_sinkhorn_per_doc(_ptr(E), E.shape[0], E.shape[1], _ptr(col_ptr), _ptr(row_idx),
+                                         _ptr(val), N, _ptr(q_ids), _ptr(q_w), q_ids.shape[0], float(lam),
+                                         int(max_iter), float(tol_rel), _ptr(out), _ptr(its))
+    if rc:
+        raise OracleError(rc)
+    return out, its
 
 
 def partition(col_ptr, P):

@@ -218,6 +218,90 @@ done:
   return rc;
 }
 
+/* "While x changes" per document (Algorithm 1 l.3).
+ * The same sparse Algorithm 1 as oracle_sinkhorn (dense = 0), but each document j stops on its
+ * own: after the first x-update t (1 <= t <= max_iter) with
+ *        max_i | xnew_ij / x_ij - 1 |  <= tol_rel,
+ * i.e. x no longer changes relative to itself (reading R31: the paper gives no
+ * tolerance; a relative test is scale free, so the GPU can evaluate it on gauged iterates),
+ * or after max_iter updates. tol_rel < 0 never stops early (= oracle_sinkhorn, fixed iters).
+ * Then the final step of l.6-7. Documents are independent, so the loop runs
+ * document by document. iters_doc[j] (optional) receives the number of x-updates of doc j. */
+int oracle_sinkhorn_per_doc(const float* E, int64_t V, int32_t d, const int64_t* col_ptr,
+                            const int32_t* row_idx, const float* val, int64_t N,
+                            const int32_t* q_ids, const float* q_w, int32_t nq, double lambda,
+                            int32_t max_iter, double tol_rel, double* wmd, int32_t* iters_doc) {
+  if (!E || !col_ptr || !row_idx || !val || !q_ids || !q_w || !wmd) return ORC_ERR_ARG;
+  if (V < 1 || d < 1 || N < 1 || nq < 1 || max_iter < 0 || !(lambda > 0.0)) return ORC_ERR_ARG;
+  const int64_t nnz = col_ptr[N];
+  for (int64_t e = 0; e < nnz; ++e)
+    if (row_idx[e] < 0 || row_idx[e] >= V) return ORC_ERR_INDEX;
+  int rc = ORC_OK;
+  int32_t* sel = (int32_t*)malloc(sizeof(int32_t) * (size_t)nq);
+  double* r = (double*)malloc(sizeof(double) * (size_t)nq);
+  int32_t v_r = 0;
+  if (!sel || !r) { free(sel); free(r); return ORC_ERR_OOM; }
+  rc = oracle_select_nonzero(V, q_ids, q_w, nq, sel, r, &v_r);
+  if (rc != ORC_OK || v_r < 1) { free(sel); free(r); return rc != ORC_OK ? rc : ORC_ERR_ARG; }
+  int64_t maxlen = 1;
+  for (int64_t j = 0; j < N; ++j)
+    if (col_ptr[j + 1] - col_ptr[j] > maxlen) maxlen = col_ptr[j + 1] - col_ptr[j];
+  double* M = (double*)malloc(sizeof(double) * (size_t)v_r * (size_t)maxlen);  /* doc block */
+  double* K = (double*)malloc(sizeof(double) * (size_t)v_r * (size_t)maxlen);
+  double* x = (double*)malloc(sizeof(double) * (size_t)v_r);
+  double* xn = (double*)malloc(sizeof(double) * (size_t)v_r);
+  double* u = (double*)malloc(sizeof(double) * (size_t)v_r);
+  double* v = (double*)malloc(sizeof(double) * (size_t)maxlen);
+  if (!M || !K || !x || !xn || !u || !v) { rc = ORC_ERR_OOM; goto done2; }
+  for (int64_t j = 0; j < N; ++j) {
+    const int64_t b = col_ptr[j], n = col_ptr[j + 1] - b;
+    for (int32_t i = 0; i < v_r; ++i)                    /* M(I, words of j), K = exp(-lambda M) */
+      for (int64_t e = 0; e < n; ++e) {
+        const double m = euclid(E + (int64_t)sel[i] * d, E + (int64_t)row_idx[b + e] * d, d);
+        M[(int64_t)i * n + e] = m;
+        K[(int64_t)i * n + e] = exp(-lambda * m);
+      }
+    for (int32_t i = 0; i < v_r; ++i) x[i] = 1.0 / (double)v_r;             /* :121 */
+    int32_t it = 0;
+    while (it < max_iter) {
+      for (int32_t i = 0; i < v_r; ++i) u[i] = 1.0 / x[i];                   /* u = 1.0 / x */
+      for (int64_t e = 0; e < n; ++e) {                                       /* SDDMM */
+        double s = 0.0;
+        for (int32_t i = 0; i < v_r; ++i) s += K[(int64_t)i * n + e] * u[i];
+        v[e] = (double)val[b + e] * (1.0 / s);
+      }
+      double change = 0.0;
+      for (int32_t i = 0; i < v_r; ++i) {                                     /* x = diag(1/r) K v */
+        double s = 0.0;
+        for (int64_t e = 0; e < n; ++e) s += ((1.0 / r[i]) * K[(int64_t)i * n + e]) * v[e];
+        xn[i] = s;
+        const double rc_ = fabs(s / x[i] - 1.0);
+        change = (rc_ > change || isnan(rc_)) ? (isnan(rc_) ? INFINITY : rc_) : change;
+      }
+      for (int32_t i = 0; i < v_r; ++i) x[i] = xn[i];
+      ++it;
+      if (tol_rel >= 0.0 && change <= tol_rel) break;
+    }
+    if (iters_doc) iters_doc[j] = it;
+    for (int32_t i = 0; i < v_r; ++i) u[i] = 1.0 / x[i];                     /* final step */
+    for (int64_t e = 0; e < n; ++e) {
+      double s = 0.0;
+      for (int32_t i = 0; i < v_r; ++i) s += K[(int64_t)i * n + e] * u[i];
+      v[e] = (double)val[b + e] * (1.0 / s);
+    }
+    double w = 0.0;
+    for (int32_t i = 0; i < v_r; ++i) {
+      double s = 0.0;
+      for (int64_t e = 0; e < n; ++e) s += (K[(int64_t)i * n + e] * M[(int64_t)i * n + e]) * v[e];
+      w += u[i] * s;
+    }
+    wmd[j] = w;
+  }
+done2:
+  free(M); free(K); free(x); free(xn); free(u); free(v); free(sel); free(r);
+  return rc;
+}
+
 /* nnz-balanced document partition ("divided the number of non-zeros in c evenly
  * among the threads and each thread ... determines its starting exploration point inside the
  * CSR using a binary search"), snapped to document boundaries: worker g starts

@@ -336,3 +336,46 @@ def test_P14_partition_bisect_and_balance():
         assert np.all(np.diff(b) >= 0)
         for g in range(P):
             assert cp[b[g + 1]] - cp[b[g]] <= -(-nnz // P) + lens.max()
+
+
+# ---------------------------------------------------------------- P16: per-document "while x changes"
+
+def test_P16_per_doc_tol_negative_is_the_fixed_iteration_oracle():
+    """tol_rel < 0 never stops early: bitwise the fixed-iteration oracle (same sums, same order)."""
+    wl = synth.make_workload("tiny")
+    q, w = wl.queries[0]
+    for iters in (0, 1, 15):
+        d, its = oracle.sinkhorn_wmd_per_doc(wl.E, wl.col_ptr, wl.row_idx, wl.val, q, w, 10.0, iters, -1.0)
+        ref = oracle.sinkhorn_wmd(wl.E, wl.col_ptr, wl.row_idx, wl.val, q, w, 10.0, iters)
+        assert np.array_equal(d, ref)
+        assert np.all(its == iters)
+
+
+def test_P16_per_doc_stop_equals_fixed_run_of_that_length_and_criterion():
+    """Each document's result equals the fixed-iteration oracle run for exactly iters_doc[j]
+    updates, and the stopping rule holds at that update and not before: with x_t = 1/u after t
+    updates (from the fixed oracle's final state), max_i |x_t/x_{t-1} - 1| <= tol < the same
+    quantity at t-1."""
+    wl = synth.make_workload("tiny")
+    q, w = wl.queries[0]
+    tol = 1e-3
+    d, its = oracle.sinkhorn_wmd_per_doc(wl.E, wl.col_ptr, wl.row_idx, wl.val, q, w, 1.0, 500, tol)
+    assert its.min() >= 1 and its.max() < 500 and len(set(its.tolist())) > 1
+    for j in range(0, wl.N, 7):
+        cp, ri, va = synth.subset_docs(wl.col_ptr, wl.row_idx, wl.val, np.array([j]))
+        ref = oracle.sinkhorn_wmd(wl.E, cp, ri, va, q, w, 1.0, int(its[j]))
+        assert d[j] == ref[0]
+        x = [1.0 / oracle.sinkhorn_wmd(wl.E, cp, ri, va, q, w, 1.0, t, return_state=True)[1]["u"][0]
+             for t in range(max(0, its[j] - 2), its[j] + 1)]
+        change = [np.max(np.abs(x[k + 1] / x[k] - 1.0)) for k in range(len(x) - 1)]
+        assert change[-1] <= tol
+        if its[j] >= 2:
+            assert change[-2] > tol
+
+
+def test_P16_per_doc_huge_tol_stops_after_one_update():
+    wl = synth.make_workload("tiny")
+    q, w = wl.queries[0]
+    d, its = oracle.sinkhorn_wmd_per_doc(wl.E, wl.col_ptr, wl.row_idx, wl.val, q, w, 10.0, 15, 1e300)
+    assert np.all(its == 1)
+    assert np.array_equal(d, oracle.sinkhorn_wmd(wl.E, wl.col_ptr, wl.row_idx, wl.val, q, w, 10.0, 1))
