@@ -108,6 +108,14 @@ WMD_API wmd_status wmd_set_stream(wmd_handle* h, void* cuda_stream);
 
 WMD_API wmd_status wmd_set_option(wmd_handle* h, int32_t option, int64_t value);
 
+/* "While x changes" (Algorithm 1 l.3). tol < 0 (default):
+ * every query runs exactly `iters` x-updates. tol >= 0: each document stops on its own after
+ * the first x-update with max_i |x_new_ij / x_ij - 1| <= tol (a relative, scale-free reading of
+ * the paper's untoleranced rule, R31), at most `iters` updates; then the final step.
+ * The per-document update counts of the last query are read with wmd_read_iterations.
+ * Errors: INVALID_ARGUMENT (NaN). */
+WMD_API wmd_status wmd_set_tolerance(wmd_handle* h, double tol);
+
 /* Install the target documents c ("c is a sparse vocabulary_size x num_docs
  * matrix ... columns of c are normalized"). CSC: col_ptr[N+1] int64 (col_ptr[0]==0,
  * non-decreasing, col_ptr[N]==nnz), row_idx[nnz] int32 word ids strictly increasing within
@@ -179,6 +187,9 @@ WMD_API wmd_status wmd_read_kernel(wmd_handle* h, int64_t k0, int64_t count, flo
                            float* colmin);
 WMD_API wmd_status wmd_read_scaling(wmd_handle* h, int64_t j0, int64_t count, float* u);
 WMD_API wmd_status wmd_read_flags(wmd_handle* h, uint8_t* flags);
+/* iters_out[N]: x-updates each document of the last query ran (== iters unless a tolerance is
+ * set; for wmd_query_batch: the last query of the batch). */
+WMD_API wmd_status wmd_read_iterations(wmd_handle* h, int32_t* iters_out);
 
 WMD_API const char* wmd_status_string(wmd_status s);
 WMD_API const char* wmd_last_error(const wmd_handle* h); /* detail of the last error on h ("" if none) */

@@ -196,10 +196,12 @@ constexpr int min_blocks() {
   return b < 1 ? 1 : (b > 8 ? 8 : b);
 }
 
-template <int CW, int NT, int TW>
+// CONV: "while x changes" mode (per-document relative-change stop, NEXT-3) compiled in.
+template <int CW, int NT, int TW, bool CONV>
 __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW>()) sinkhorn_fused_kernel(
     const int4* __restrict__ sdoc, const Entry* __restrict__ ent, int64_t pos0, int64_t pos1,
-    const float* __restrict__ Mx, int v_r, const float* __restrict__ rpad, float lambda, int iters, float* __restrict__ dist,
+    const float* __restrict__ Mx, int v_r, const float* __restrict__ rpad, float lambda, int iters,
+    float tol, int32_t* __restrict__ iters_doc, float* __restrict__ dist,
     uint8_t* __restrict__ flags, int32_t* __restrict__ flagged_list,
     int32_t* __restrict__ flagged_count) {
   using S = Shape<CW, NT, TW>;
@@ -345,10 +347,11 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW>()) sinkhorn_f
 
     // ---- iterations, then the final step
     float umax_k = (float)v_r * kv_s;   // v_r * max(uh) * 2^-110 (max uh0 <= v_r)
-    bool bad = false;
+    bool bad = false, done = false;
     uint32_t badu = 0u;
     float v_own[NOWN];
-    for (int it = 0;; ++it) {
+    int it = 0;
+    for (;; ++it) {
       // SDDMM: row partials over this lane's columns, then the reduce over the b-lanes
       float p[RW];
 #pragma unroll
@@ -369,7 +372,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW>()) sinkhorn_f
 #endif
         vmax_b = max(vmax_b, __float_as_uint(v_own[o]));
       }
-      if (it == iters) break;
+      if (it == iters || (CONV && done)) break;
       if (it == 1) {  // the next document's entries have landed: start its row copies
         staged = true;
         stage3(Nb);
@@ -401,12 +404,15 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW>()) sinkhorn_f
       }
       reduce_cols<CW>(q);
       const float vcap = (float)n * __uint_as_float(vmax_b) * kUnder;
-      uint32_t umax_b = 0u;
+      uint32_t umax_b = 0u, chg_b = 0u;
       float uo[NCO];
 #pragma unroll
       for (int g = 0; g < NCO; ++g) {
         const float acc = q[4 * g];
         uo[g] = r_own[g] * rcp_fast(acc);
+        // "while x changes" (NEXT-3): |x_new/x - 1| = |uh/uh_new - 1| (gauge invariant; the
+        // own column's current uh sits in column slot 4g); NaN compares above every float
+        if (CONV && oreal[g]) chg_b = max(chg_b, __float_as_uint(fabsf(u[4 * g] / uo[g] - 1.f)));
 #ifndef WMD_EXP_NO_CERT
         bad |= und && vcap > acc;
 #endif
@@ -416,6 +422,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW>()) sinkhorn_f
       // the lanes check their own uh stay normal
       umax_b = __reduce_max_sync(kFull, umax_b);
       badu |= umax_b > 0x7f7fffffu;
+      if (CONV) done = __uint_as_float(__reduce_max_sync(kFull, chg_b)) <= tol;
       const float sc = __uint_as_float((254u - min(umax_b >> 23, 253u)) << 23);
       umax_k = 2.f * kv_s;
 #pragma unroll
@@ -468,6 +475,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW>()) sinkhorn_f
     const bool flag = __any_sync(kFull, bad) || badu || !(fabsf(wsum) <= FLT_MAX);
     if (lane == 0) {
       dist[j] = wsum;
+      if (iters_doc) iters_doc[j] = it;
       if (flag) {
         flags[j] |= kFlagFp32Range;
         flagged_list[atomicAdd(flagged_count, 1)] = j;
@@ -490,25 +498,35 @@ int num_sms() {
   return sms;
 }
 
-template <int CW, int NT, int TW>
-void launch_fused_range(const int4* sdoc, const Entry* ent, int64_t p0,
+template <int CW, int NT, int TW, bool CONV>
+void launch_fused_range_t(const int4* sdoc, const Entry* ent, int64_t p0,
                         int64_t p1, const float* Mx, int v_r, const float* rpad, float lambda,
-                        int iters, float* dist, uint8_t* flags, int32_t* fl, int32_t* fc,
-                        cudaStream_t st) {
+                        int iters, float tol, int32_t* itd, float* dist, uint8_t* flags, int32_t* fl,
+                        int32_t* fc, cudaStream_t st) {
   if (p1 <= p0) return;
   constexpr size_t smem = sizeof(float) * 2 * Shape<CW, NT, TW>::BUF * kWarps;
   static int resident = 0;
   if (!resident) {
-    cudaFuncSetAttribute(sinkhorn_fused_kernel<CW, NT, TW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(sinkhorn_fused_kernel<CW, NT, TW>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(sinkhorn_fused_kernel<CW, NT, TW, CONV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(sinkhorn_fused_kernel<CW, NT, TW, CONV>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sinkhorn_fused_kernel<CW, NT, TW>, kThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sinkhorn_fused_kernel<CW, NT, TW, CONV>, kThreads, smem);
     resident = std::max(1, per_sm) * num_sms();
   }
   const int64_t need = (p1 - p0 + kWarps - 1) / kWarps;
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, resident));
-  sinkhorn_fused_kernel<CW, NT, TW><<<grid, kThreads, smem, st>>>(sdoc, ent, p0, p1, Mx, v_r, rpad,
-                                                                   lambda, iters, dist, flags, fl, fc);
+  sinkhorn_fused_kernel<CW, NT, TW, CONV><<<grid, kThreads, smem, st>>>(sdoc, ent, p0, p1, Mx, v_r, rpad,
+                                                                   lambda, iters, tol, itd, dist, flags, fl, fc);
+}
+
+template <int CW, int NT, int TW>
+void launch_fused_range(const int4* sdoc, const Entry* ent, int64_t p0, int64_t p1, const float* Mx, int v_r,
+                        const float* rpad, float lambda, int iters, float tol, int32_t* itd, float* dist,
+                        uint8_t* flags, int32_t* fl, int32_t* fc, cudaStream_t st) {
+  if (tol >= 0.f)
+    launch_fused_range_t<CW, NT, TW, true>(sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, tol, itd, dist, flags, fl, fc, st);
+  else
+    launch_fused_range_t<CW, NT, TW, false>(sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, tol, itd, dist, flags, fl, fc, st);
 }
 
 // Length buckets (rows covered: 8, 16, 32, 40, 48, 64) over the length-sorted order.
@@ -521,9 +539,10 @@ constexpr bool fits(int cw, int ne) { return (ne / 4) * cw <= 96; }  // block re
 template <int CW>
 void dispatch_bucket(int bi, const int4* sdoc, const Entry* ent, int64_t p0,
                      int64_t p1, const float* Mx, int v_r, const float* rpad, float lambda, int iters,
-                     float* dist, uint8_t* flags, int32_t* fl, int32_t* fc, cudaStream_t st) {
+                     float tol, int32_t* itd, float* dist, uint8_t* flags, int32_t* fl, int32_t* fc,
+                     cudaStream_t st) {
 #define F_(NT, TW) \
-  if constexpr (fits(CW, 32 * NT + 4 * TW)) launch_fused_range<CW, NT, TW>(sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, dist, flags, fl, fc, st)
+  if constexpr (fits(CW, 32 * NT + 4 * TW)) launch_fused_range<CW, NT, TW>(sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, tol, itd, dist, flags, fl, fc, st)
   switch (bi) {
     case 0: F_(0, 2); break;
     case 1: F_(0, 4); break;
@@ -552,9 +571,9 @@ bool fused_supported(int ld, int64_t max_doc_nnz) {
 
 void launch_sinkhorn_fused(const int4* sdoc, const Entry* ent, int64_t N,
                            const int64_t* len_prefix, int64_t max_len, const float* Mx, int ld,
-                           int v_r, const float* rpad, float lambda, int iters, float* dist,
-                           uint8_t* flags, int32_t* flagged_list, int32_t* flagged_count,
-                           cudaStream_t st) {
+                           int v_r, const float* rpad, float lambda, int iters, float tol,
+                           int32_t* iters_doc, float* dist, uint8_t* flags, int32_t* flagged_list,
+                           int32_t* flagged_count, cudaStream_t st) {
   // len_prefix[L] = number of documents with fewer than L nonzeros: the length-sorted order
   // splits into buckets of at most 8 / 16 / 32 / 40 / 48 / 64 nonzeros, one launch each.
   int64_t p0 = 0;
@@ -563,10 +582,10 @@ void launch_sinkhorn_fused(const int4* sdoc, const Entry* ent, int64_t N,
     const int64_t p1 = NE >= max_len ? N : len_prefix[NE + 1];
     if (p1 > p0) {
       switch (ld) {
-        case 8: dispatch_bucket<1>(bi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, dist, flags, flagged_list, flagged_count, st); break;
-        case 16: dispatch_bucket<2>(bi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, dist, flags, flagged_list, flagged_count, st); break;
-        case 32: dispatch_bucket<4>(bi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, dist, flags, flagged_list, flagged_count, st); break;
-        case 64: dispatch_bucket<8>(bi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, dist, flags, flagged_list, flagged_count, st); break;
+        case 8: dispatch_bucket<1>(bi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, tol, iters_doc, dist, flags, flagged_list, flagged_count, st); break;
+        case 16: dispatch_bucket<2>(bi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, tol, iters_doc, dist, flags, flagged_list, flagged_count, st); break;
+        case 32: dispatch_bucket<4>(bi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, tol, iters_doc, dist, flags, flagged_list, flagged_count, st); break;
+        case 64: dispatch_bucket<8>(bi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, tol, iters_doc, dist, flags, flagged_list, flagged_count, st); break;
         default: break;
       }
     }

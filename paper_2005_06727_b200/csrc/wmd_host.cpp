@@ -100,6 +100,9 @@ struct wmd_handle {
   DevBuf<float> dist_tmp;    // N (host-output queries)
   DevBuf<uint8_t> flags;     // N
   DevBuf<int32_t> flagged;   // N
+  DevBuf<int32_t> iters_doc; // N: x-updates per document of the last query
+  DevBuf<uint8_t> conv;      // N: converged flags ("while x changes", per-iteration path)
+  double tol = -1.0;         // "while x changes" relative tolerance; < 0: fixed iterations
   DevBuf<int32_t> counters;  // [0] flagged count, [1] breakdown, [2] fallback count, [3] scratch
   DevBuf<double> fb_scratch;
   // pinned staging for the query upload (double buffered)
@@ -397,6 +400,7 @@ void wmd_destroy(wmd_handle* h) {
   h->E.release(); h->doc_ptr.release(); h->order.release(); h->sdoc.release(); h->ent.release(); h->sel.release(); h->rpad.release();
   h->Kt.release(); h->Mx.release(); h->colmin.release(); h->ua.release(); h->ub.release(); h->umask.release();
   h->dist_tmp.release(); h->flags.release(); h->flagged.release(); h->counters.release();
+  h->iters_doc.release(); h->conv.release();
   h->fb_scratch.release();
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
   delete h;
@@ -484,6 +488,8 @@ wmd_status wmd_set_targets(wmd_handle* h, const int64_t* col_ptr, const int32_t*
   CK(h, cudaMemcpyAsync(h->ent.p, en.data(), nnz * sizeof(Entry), cudaMemcpyHostToDevice, h->stream));
   CK(h, h->flags.ensure(N));
   CK(h, h->flagged.ensure(N));
+  CK(h, h->iters_doc.ensure(N));
+  CK(h, h->conv.ensure(N));
   CK(h, h->dist_tmp.ensure(N));
   CK(h, h->fb_scratch.ensure(wmd::fallback_scratch_bytes(mx) / sizeof(double)));
   CK(h, cudaStreamSynchronize(h->stream));
@@ -541,10 +547,11 @@ wmd_status enqueue_query(wmd_handle* h, const int32_t* d_sel, const float* d_r, 
   ++launches;
   if (pe) CK(h, cudaEventRecord(pe->ev[1], st));
 
+  const float tol = h->tol >= 0.0 ? (float)h->tol : -1.f;
   if (fused) {
     wmd::launch_sinkhorn_fused(h->sdoc.p, h->ent.p, N, h->len_prefix.data(),
-                               h->max_doc_nnz, h->Mx.p, ld, v_r, d_r, lambda, iters, dist,
-                               h->flags.p, h->flagged.p, h->counters.p, st);
+                               h->max_doc_nnz, h->Mx.p, ld, v_r, d_r, lambda, iters, tol, h->iters_doc.p,
+                               dist, h->flags.p, h->flagged.p, h->counters.p, st);
     const int64_t nl = wmd::fused_launch_count(h->len_prefix.data(), h->max_doc_nnz, N);
     launches += nl;
     h->st.iter_launches += nl;
@@ -555,10 +562,13 @@ wmd_status enqueue_query(wmd_handle* h, const int32_t* d_sel, const float* d_r, 
     // a4: iters fused SDDMM_SpMM launches, u ping-pong
     const float* u_in = nullptr;
     float* bufs[2] = {h->ua.p, h->ub.p};
+    wmd::launch_fill_i32(h->iters_doc.p, N, iters, st);
+    if (tol >= 0.f) CK(h, cudaMemsetAsync(h->conv.p, 0, N, st));
     for (int32_t t = 0; t < iters; ++t) {
       float* u_out = bufs[t & 1];
       wmd::launch_sddmm_spmm_iter(h->order.p, h->doc_ptr.p, h->ent.p, N, h->Kt.p, ld, v_r, d_r, u_in, u_out,
-                                  h->umask.p, h->flags.p, st);
+                                  h->umask.p, h->flags.p, wmd::ConvParams{tol, h->conv.p, h->iters_doc.p, t},
+                                  st);
       u_in = u_out;
     }
     launches += iters;
@@ -783,6 +793,22 @@ wmd_status wmd_read_scaling(wmd_handle* h, int64_t j0, int64_t count, float* u) 
   DeviceGuard g(h->device);
   CK(h, cudaStreamSynchronize(h->stream));
   CK(h, cudaMemcpy(u, h->u_last + j0 * h->ld, count * h->ld * 4, cudaMemcpyDeviceToHost));
+  return WMD_OK;
+}
+
+wmd_status wmd_set_tolerance(wmd_handle* h, double tol) {
+  if (!h) return WMD_ERR_INVALID_ARGUMENT;
+  if (std::isnan(tol)) return fail(h, WMD_ERR_INVALID_ARGUMENT, "tolerance is NaN");
+  h->tol = tol;
+  return WMD_OK;
+}
+
+wmd_status wmd_read_iterations(wmd_handle* h, int32_t* iters_out) {
+  if (!h || !iters_out) return WMD_ERR_INVALID_ARGUMENT;
+  if (!h->has_targets || h->st.queries == 0) return fail(h, WMD_ERR_STATE, "no query yet");
+  DeviceGuard g(h->device);
+  CK(h, cudaStreamSynchronize(h->stream));
+  CK(h, cudaMemcpy(iters_out, h->iters_doc.p, h->N * sizeof(int32_t), cudaMemcpyDeviceToHost));
   return WMD_OK;
 }
 

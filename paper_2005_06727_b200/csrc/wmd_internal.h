@@ -36,12 +36,23 @@ struct QueryDev {
 void launch_build_ktilde(const float* E, int64_t V, int dp, const int32_t* sel, int v_r, int ld,
                          float lambda, float* Kt, float* Mx, float* colmin, cudaStream_t st);
 
+// "While x changes" (NEXT-3): tol < 0 runs the fixed iteration count. Otherwise a
+// document stops after the first x-update with max_i |x_new/x - 1| <= tol (R31);
+// conv[j] marks it (per-iteration path), iters_doc[j] receives its number of x-updates.
+struct ConvParams {
+  float tol;
+  uint8_t* conv;
+  int32_t* iters_doc;
+  int it_index;  // index of this x-update (per-iteration path)
+};
+
 // --- a4: one fused SDDMM_SpMM iteration for all documents ------------
 // u_in == nullptr: first iteration with the constant u0 = 1/x0 = v_r.
 // `order` lists the documents sorted by length (processing order only; results are per document).
 void launch_sddmm_spmm_iter(const int32_t* order, const int32_t* doc_ptr, const Entry* ent, int64_t N,
                             const float* Kt, int ld, int v_r, const float* rpad, const float* u_in,
-                            float* u_out, uint32_t* umask, uint8_t* flags, cudaStream_t st);
+                            float* u_out, uint32_t* umask, uint8_t* flags, ConvParams cv,
+                            cudaStream_t st);
 
 // --- a5: final u/v/WMD step -----------------------------------
 void launch_final_wmd(const int32_t* order, const int32_t* doc_ptr, const Entry* ent, int64_t N,
@@ -58,9 +69,9 @@ bool fused_supported(int ld, int64_t max_doc_nnz);
 // sdoc[p] = {document id, first nonzero, length, 0} of the p-th document in length order.
 void launch_sinkhorn_fused(const int4* sdoc, const Entry* ent, int64_t N,
                            const int64_t* len_prefix, int64_t max_len, const float* Mx, int ld,
-                           int v_r, const float* rpad, float lambda, int iters, float* dist,
-                           uint8_t* flags, int32_t* flagged_list, int32_t* flagged_count,
-                           cudaStream_t st);
+                           int v_r, const float* rpad, float lambda, int iters, float tol,
+                           int32_t* iters_doc, float* dist, uint8_t* flags, int32_t* flagged_list,
+                           int32_t* flagged_count, cudaStream_t st);
 int fused_launch_count(const int64_t* len_prefix, int64_t max_len, int64_t N);
 
 // --- a6: FP64 re-run of flagged documents (no CPU fallback) --------------------------------
@@ -74,5 +85,6 @@ void launch_fallback_fp64(const float* Mx, const float* colmin, int ld, const fl
 
 // --- validation helpers (device-resident inputs) -------------------------------------------
 void launch_check_finite(const float* x, int64_t n, int32_t* bad, cudaStream_t st);
+void launch_fill_i32(int32_t* p, int64_t n, int32_t v, cudaStream_t st);
 
 }  // namespace wmd

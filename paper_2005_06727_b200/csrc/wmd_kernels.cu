@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(256, FINAL ? 2 : PASS_BLOCKS_PER_SM) sinkhorn_
     const float* __restrict__ Mt, int ld, int v_r, const float* __restrict__ rpad,
     const float* __restrict__ u_in, float* __restrict__ u_out, uint32_t* __restrict__ umask,
     int mask_words, float* __restrict__ dist, uint8_t* __restrict__ flags,
-    int32_t* __restrict__ flagged_list, int32_t* __restrict__ flagged_count) {
+    int32_t* __restrict__ flagged_list, int32_t* __restrict__ flagged_count, ConvParams cv) {
   constexpr int NG = 32 / G;
   constexpr int SHIFT = Log2<G>::value - Log2<U>::value;
   static_assert(U <= G, "at most one nonzero per lane per step");
@@ -287,6 +287,18 @@ __global__ void __launch_bounds__(256, FINAL ? 2 : PASS_BLOCKS_PER_SM) sinkhorn_
       un.c = (r.c > 0.f ? r.c : 1.f) / (r.c > 0.f ? acc.c : 1.f); if (!(r.c > 0.f)) un.c = 0.f;
       WMD_UDIV(x) WMD_UDIV(y) WMD_UDIV(z) WMD_UDIV(w)
 #undef WMD_UDIV
+      // "while x changes" (NEXT-3): a converged document keeps its u (x is frozen); otherwise
+      // the relative change max_i |x_new/x - 1| = max_i |u/u_new - 1| (gauge invariant)
+      const bool frozen = cv.tol >= 0.f && j >= 0 && cv.conv[j];
+      float chg = 0.f;
+      if (cv.tol >= 0.f) {
+#define WMD_CHG(c) if (r.c > 0.f) chg = fmaxf(chg, fabsf(u.c / un.c - 1.f));
+        WMD_CHG(x) WMD_CHG(y) WMD_CHG(z) WMD_CHG(w)
+#undef WMD_CHG
+        if (!(chg <= FLT_MAX)) chg = FLT_MAX;  // NaN: not converged
+#pragma unroll
+        for (int off = G / 2; off; off >>= 1) chg = fmaxf(chg, __shfl_xor_sync(kFull, chg, off));
+      }
       const float vcap = (float)n * vmax * kUnderScale;  // bound on the underflowed terms
       float mx = 0.f, mn = FLT_MAX;
 #define WMD_ROW(c, bit)                                                   \
@@ -302,12 +314,18 @@ __global__ void __launch_bounds__(256, FINAL ? 2 : PASS_BLOCKS_PER_SM) sinkhorn_
         mn = fminf(mn, __shfl_xor_sync(kFull, mn, off));
         bad |= __shfl_xor_sync(kFull, bad, off);
       }
-      if (!bad) {
+      if (frozen) {
+        un = u;
+      } else if (!bad) {
         const int g = (ilogbf(mx) + ilogbf(mn)) >> 1;  // floor((e_max + e_min) / 2)
         const float sc = ldexpf(1.0f, -g);             // |g| <= 126 when all u are normal
         un.x *= sc; un.y *= sc; un.z *= sc; un.w *= sc;
       } else if (sub == 0 && j >= 0) {
         flags[j] |= kFlagFp32Range;
+      }
+      if (!frozen && cv.tol >= 0.f && chg <= cv.tol && sub == 0 && j >= 0) {
+        cv.conv[j] = 1;
+        cv.iters_doc[j] = cv.it_index + 1;
       }
       if (act && j >= 0) WMD_STS(reinterpret_cast<float4*>(u_out + j * ld) + sub, un);
     }
@@ -438,16 +456,17 @@ int mask_words_for(int ld) { return (ld + 31) / 32; }
 
 void launch_sddmm_spmm_iter(const int32_t* order, const int32_t* doc_ptr, const Entry* ent, int64_t N,
                             const float* Kt, int ld, int v_r, const float* rpad, const float* u_in,
-                            float* u_out, uint32_t* umask, uint8_t* flags, cudaStream_t st) {
+                            float* u_out, uint32_t* umask, uint8_t* flags, ConvParams cv,
+                            cudaStream_t st) {
   const unsigned grid = pass_grid(N, ld, PASS_BLOCKS_PER_SM);
   const int mw = mask_words_for(ld);
   // the first iteration records the underflow row masks, later ones read them
   if (u_in == nullptr) {
-#define L_(G, U) sinkhorn_pass_kernel<G, U, false, true><<<grid, 256, 0, st>>>(order, doc_ptr, ent, N, Kt, nullptr, ld, v_r, rpad, u_in, u_out, umask, mw, nullptr, flags, nullptr, nullptr)
+#define L_(G, U) sinkhorn_pass_kernel<G, U, false, true><<<grid, 256, 0, st>>>(order, doc_ptr, ent, N, Kt, nullptr, ld, v_r, rpad, u_in, u_out, umask, mw, nullptr, flags, nullptr, nullptr, cv)
     WMD_DISPATCH_G(ld, L_)
 #undef L_
   } else {
-#define L_(G, U) sinkhorn_pass_kernel<G, U, false, false><<<grid, 256, 0, st>>>(order, doc_ptr, ent, N, Kt, nullptr, ld, v_r, rpad, u_in, u_out, umask, mw, nullptr, flags, nullptr, nullptr)
+#define L_(G, U) sinkhorn_pass_kernel<G, U, false, false><<<grid, 256, 0, st>>>(order, doc_ptr, ent, N, Kt, nullptr, ld, v_r, rpad, u_in, u_out, umask, mw, nullptr, flags, nullptr, nullptr, cv)
     WMD_DISPATCH_G(ld, L_)
 #undef L_
   }
@@ -461,11 +480,11 @@ void launch_final_wmd(const int32_t* order, const int32_t* doc_ptr, const Entry*
   const int mw = mask_words_for(ld);
   uint32_t* um = const_cast<uint32_t*>(umask);
   if (u_in == nullptr) {  // iters == 0: no iteration recorded the masks
-#define L_(G, U) sinkhorn_pass_kernel<G, U, true, true><<<grid, 256, 0, st>>>(order, doc_ptr, ent, N, Kt, Mt, ld, v_r, rpad, u_in, nullptr, um, mw, dist, flags, flagged_list, flagged_count)
+#define L_(G, U) sinkhorn_pass_kernel<G, U, true, true><<<grid, 256, 0, st>>>(order, doc_ptr, ent, N, Kt, Mt, ld, v_r, rpad, u_in, nullptr, um, mw, dist, flags, flagged_list, flagged_count, ConvParams{-1.f, nullptr, nullptr, 0})
     WMD_DISPATCH_G(ld, L_)
 #undef L_
   } else {
-#define L_(G, U) sinkhorn_pass_kernel<G, U, true, false><<<grid, 256, 0, st>>>(order, doc_ptr, ent, N, Kt, Mt, ld, v_r, rpad, u_in, nullptr, um, mw, dist, flags, flagged_list, flagged_count)
+#define L_(G, U) sinkhorn_pass_kernel<G, U, true, false><<<grid, 256, 0, st>>>(order, doc_ptr, ent, N, Kt, Mt, ld, v_r, rpad, u_in, nullptr, um, mw, dist, flags, flagged_list, flagged_count, ConvParams{-1.f, nullptr, nullptr, 0})
     WMD_DISPATCH_G(ld, L_)
 #undef L_
   }
@@ -484,6 +503,15 @@ void launch_fallback_fp64(const float* Mt, const float* colmin, int ld, const fl
                                                         ent, flagged_list, flagged_count, scratch,
                                                         max_doc_nnz, dist, flags, breakdown,
                                                         fallback_count);
+}
+
+__global__ void fill_i32_kernel(int32_t* p, int64_t n, int32_t v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+void launch_fill_i32(int32_t* p, int64_t n, int32_t v, cudaStream_t st) {
+  fill_i32_kernel<<<(unsigned)std::min<int64_t>(1184, (n + 255) / 256 + 1), 256, 0, st>>>(p, n, v);
 }
 
 void launch_check_finite(const float* x, int64_t n, int32_t* bad, cudaStream_t st) {

@@ -42,6 +42,7 @@ EXPORTED = (
     "wmd_query_batch", "wmd_sync",
     "wmd_partition", "wmd_validate_csc", "wmd_validate_query", "wmd_get_stats", "wmd_reset_stats",
     "wmd_get_query_rows", "wmd_read_kernel", "wmd_read_scaling", "wmd_read_flags",
+    "wmd_set_tolerance", "wmd_read_iterations",
     "wmd_status_string", "wmd_last_error", "wmd_version", "wmd_destroy",
 )
 
@@ -83,6 +84,8 @@ def _load():
         "wmd_read_kernel": [P, I64, I64, P, P, P],
         "wmd_read_scaling": [P, I64, I64, P],
         "wmd_read_flags": [P, P],
+        "wmd_set_tolerance": [P, ctypes.c_double],
+        "wmd_read_iterations": [P, P],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -265,6 +268,16 @@ def wmd_read_scaling(h, j0: int, count: int, ld: int):
     u = np.empty((count, ld), np.float32)
     _check(lib.wmd_read_scaling(h, j0, count, u.ctypes.data_as(ctypes.c_void_p)), h)
     return u
+
+
+def wmd_set_tolerance(h, tol: float) -> None:
+    _check(lib.wmd_set_tolerance(h, float(tol)), h)
+
+
+def wmd_read_iterations(h, N: int) -> np.ndarray:
+    it = np.empty(N, np.int32)
+    _check(lib.wmd_read_iterations(h, it.ctypes.data_as(ctypes.c_void_p)), h)
+    return it
 
 
 def wmd_read_flags(h, N: int):

@@ -565,3 +565,35 @@ def test_query_batch_validates_all_before_enqueueing(W):
         assert W.wmd_get_stats(h)["queries"] == 0 and not out.any()
     finally:
         W.wmd_destroy(h)
+
+
+# ------------------------------------------------------------------ NEXT-3: while x changes
+
+@pytest.mark.parametrize("path", PATHS)
+def test_while_x_changes_per_document(W, path):
+    """wmd_set_tolerance: each document stops after the first x-update with
+    max_i |x_new/x - 1| <= tol (the oracle's sinkhorn_wmd_per_doc). Distances within the parity
+    tolerance; per-document update counts equal the oracle's up to +-1 (FP32 vs FP64 evaluation
+    of a change that sits at the threshold) and exactly for the large majority."""
+    wl = synth.make_workload("tiny")
+    q, w = wl.queries[0]
+    tol, lam, cap = 1e-5, 1.0, 800  # tol well above the FP32 noise of the change (~1e-6)
+    o, o_its = oracle.sinkhorn_wmd_per_doc(wl.E, wl.col_ptr, wl.row_idx, wl.val, q, w, lam, cap, tol)
+    assert o_its.max() < cap
+    h = W.wmd_create(wl.E)
+    try:
+        W.wmd_set_option(h, W.WMD_OPT_PATH, path)
+        W.wmd_set_targets(h, wl.col_ptr, wl.row_idx, wl.val)
+        W.wmd_set_tolerance(h, tol)
+        d = np.empty(wl.N, np.float32)
+        W.wmd_query(h, q, w, lam, cap, d)
+        W.wmd_sync(h)
+        its = W.wmd_read_iterations(h, wl.N)
+        W.wmd_set_tolerance(h, -1.0)          # back to fixed iterations
+        W.wmd_query(h, q, w, lam, 15, np.empty(wl.N, np.float32))
+        assert np.all(W.wmd_read_iterations(h, wl.N) == 15)
+    finally:
+        W.wmd_destroy(h)
+    assert_parity(d, o, f"while-x-changes path {path}")
+    assert np.abs(its - o_its).max() <= 1
+    assert np.mean(its == o_its) >= 0.9
