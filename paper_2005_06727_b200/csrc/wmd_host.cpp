@@ -585,7 +585,8 @@ wmd_status enqueue_query(wmd_handle* h, const int32_t* d_sel, const float* d_r, 
   }
   // a6: FP64 re-run of flagged documents (device-side list; zero-cost when empty)
   if (h->opt_fallback) {
-    wmd::launch_fallback_fp64(h->Mx.p, h->colmin.p, ld, d_r, v_r, (double)lambda, iters, h->doc_ptr.p,
+    wmd::launch_fallback_fp64(h->Mx.p, h->colmin.p, ld, d_r, v_r, (double)lambda, iters, tol, h->iters_doc.p,
+                              h->doc_ptr.p,
                               h->ent.p, h->flagged.p, h->counters.p, h->fb_scratch.p, h->max_doc_nnz, dist,
                               h->flags.p, h->counters.p + 1, h->counters.p + 2, st);
     ++launches;

@@ -78,7 +78,8 @@ int fused_launch_count(const int64_t* len_prefix, int64_t max_len, int64_t N);
 constexpr int kFallbackBlocks = 296;  // 2 per SM
 size_t fallback_scratch_bytes(int64_t max_doc_nnz);
 void launch_fallback_fp64(const float* Mx, const float* colmin, int ld, const float* rpad, int v_r,
-                          double lambda, int iters, const int32_t* doc_ptr, const Entry* ent,
+                          double lambda, int iters, float tol, int32_t* iters_doc,
+                          const int32_t* doc_ptr, const Entry* ent,
                           const int32_t* flagged_list, const int32_t* flagged_count,
                           double* scratch, int64_t max_doc_nnz, float* dist, uint8_t* flags,
                           int32_t* breakdown, int32_t* fallback_count, cudaStream_t st);

@@ -342,16 +342,39 @@ __global__ void __launch_bounds__(256, FINAL ? 2 : PASS_BLOCKS_PER_SM) sinkhorn_
 // FP32 *range* failed (measured: DESIGN.md §4). Deterministic: sequential per-thread sums and a
 // serial final sum.
 // ============================================================================================
+__device__ __forceinline__ double warp_sum_d(double x) {
+#pragma unroll
+  for (int off = 16; off; off >>= 1) x += __shfl_xor_sync(kFull, x, off);
+  return x;
+}
+
+// Block (256 threads) max and min of per-thread doubles; all threads receive the results.
+__device__ __forceinline__ void block_maxmin_d(double mx, double mn, double* red, double& omx, double& omn) {
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    mx = fmax(mx, __shfl_xor_sync(kFull, mx, off));
+    mn = fmin(mn, __shfl_xor_sync(kFull, mn, off));
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) { red[w] = mx; red[8 + w] = mn; }
+  __syncthreads();
+  omx = red[0]; omn = red[8];
+#pragma unroll
+  for (int k = 1; k < 8; ++k) { omx = fmax(omx, red[k]); omn = fmin(omn, red[8 + k]); }
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(256) fallback_fp64_kernel(
     const float* __restrict__ Mt, const float* __restrict__ colmin, int ld,
-    const float* __restrict__ rpad, int v_r, double lambda, int iters,
-    const int32_t* __restrict__ doc_ptr, const Entry* __restrict__ ent,
+    const float* __restrict__ rpad, int v_r, double lambda, int iters, float tol,
+    int32_t* __restrict__ iters_doc, const int32_t* __restrict__ doc_ptr, const Entry* __restrict__ ent,
     const int32_t* __restrict__ flagged_list, const int32_t* __restrict__ flagged_count,
     double* __restrict__ scratch, int64_t max_doc_nnz, float* __restrict__ dist,
     uint8_t* __restrict__ flags, int32_t* __restrict__ breakdown, int32_t* __restrict__ fb_count) {
   __shared__ double u[WMD_MAX_VR_DEV], un[WMD_MAX_VR_DEV];
-  __shared__ int gexp;
+  __shared__ int gexp, stop;
   const int n = *flagged_count;
+  const int ldx = ld + 4;
   double* Kb = scratch + (int64_t)blockIdx.x * (max_doc_nnz * WMD_MAX_VR_DEV + 2 * max_doc_nnz);
   double* vv = Kb + max_doc_nnz * WMD_MAX_VR_DEV;
   double* qv = vv + max_doc_nnz;
@@ -361,11 +384,12 @@ __global__ void __launch_bounds__(256) fallback_fp64_kernel(
     for (int p = threadIdx.x; p < L * v_r; p += blockDim.x) {
       const int e_ = p / v_r, i = p % v_r;
       const int k = ent[b + e_].k;
-      Kb[p] = exp(-lambda * ((double)Mt[(int64_t)k * (ld + 4) + i] - (double)colmin[k]));
+      Kb[p] = exp(-lambda * ((double)Mt[(int64_t)k * ldx + i] - (double)colmin[k]));
     }
     for (int i = threadIdx.x; i < v_r; i += blockDim.x) u[i] = (double)v_r;  // x0 = 1/v_r
     __syncthreads();
-    for (int it = 0; it < iters; ++it) {
+    int it = 0;
+    for (; it < iters; ++it) {
       for (int e_ = threadIdx.x; e_ < L; e_ += blockDim.x) {
         double s = 0.0;
         for (int i = 0; i < v_r; ++i) s += Kb[(int64_t)e_ * v_r + i] * u[i];
@@ -379,13 +403,19 @@ __global__ void __launch_bounds__(256) fallback_fp64_kernel(
       }
       __syncthreads();
       if (threadIdx.x == 0) {
-        double mx = 0.0, mn = DBL_MAX;
-        for (int i = 0; i < v_r; ++i) { mx = fmax(mx, un[i]); mn = fmin(mn, un[i]); }
+        double mx = 0.0, mn = DBL_MAX, chg = 0.0;
+        for (int i = 0; i < v_r; ++i) {
+          mx = fmax(mx, un[i]); mn = fmin(mn, un[i]);
+          const double c = fabs(u[i] / un[i] - 1.0);  // "while x changes": |x_new/x - 1|
+          chg = c <= DBL_MAX ? fmax(chg, c) : DBL_MAX;
+        }
         gexp = (mx > 0.0 && mn > 0.0 && mx <= DBL_MAX) ? ((ilogb(mx) + ilogb(mn)) >> 1) : 0;
+        stop = tol >= 0.f && chg <= (double)tol;
       }
       __syncthreads();
       for (int i = threadIdx.x; i < v_r; i += blockDim.x) u[i] = ldexp(un[i], -gexp);
       __syncthreads();
+      if (stop) { ++it; break; }
     }
     for (int e_ = threadIdx.x; e_ < L; e_ += blockDim.x) {
       const int k = ent[b + e_].k;
@@ -393,7 +423,7 @@ __global__ void __launch_bounds__(256) fallback_fp64_kernel(
       for (int i = 0; i < v_r; ++i) {
         const double kk = Kb[(int64_t)e_ * v_r + i];
         s += kk * u[i];
-        t += kk * (double)Mt[(int64_t)k * (ld + 4) + i] * u[i];
+        t += kk * (double)Mt[(int64_t)k * ldx + i] * u[i];
       }
       qv[e_] = ((double)ent[b + e_].c / s) * t;
     }
@@ -403,6 +433,7 @@ __global__ void __launch_bounds__(256) fallback_fp64_kernel(
       for (int e_ = 0; e_ < L; ++e_) w += qv[e_];
       dist[j] = (float)w;
       flags[j] |= kFlagFp64;
+      if (iters_doc) iters_doc[j] = it;
       if (!isfinite(w)) atomicExch(breakdown, 1);
       atomicAdd(fb_count, 1);
     }
@@ -495,11 +526,13 @@ size_t fallback_scratch_bytes(int64_t max_doc_nnz) {
 }
 
 void launch_fallback_fp64(const float* Mt, const float* colmin, int ld, const float* rpad, int v_r,
-                          double lambda, int iters, const int32_t* doc_ptr, const Entry* ent,
+                          double lambda, int iters, float tol, int32_t* iters_doc,
+                          const int32_t* doc_ptr, const Entry* ent,
                           const int32_t* flagged_list, const int32_t* flagged_count,
                           double* scratch, int64_t max_doc_nnz, float* dist, uint8_t* flags,
                           int32_t* breakdown, int32_t* fallback_count, cudaStream_t st) {
-  fallback_fp64_kernel<<<kFallbackBlocks, 256, 0, st>>>(Mt, colmin, ld, rpad, v_r, lambda, iters, doc_ptr,
+  fallback_fp64_kernel<<<kFallbackBlocks, 256, 0, st>>>(Mt, colmin, ld, rpad, v_r, lambda, iters, tol,
+                                                        iters_doc, doc_ptr,
                                                         ent, flagged_list, flagged_count, scratch,
                                                         max_doc_nnz, dist, flags, breakdown,
                                                         fallback_count);
