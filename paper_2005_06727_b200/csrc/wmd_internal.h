@@ -75,7 +75,7 @@ void launch_sinkhorn_fused(const int4* sdoc, const Entry* ent, int64_t N,
 int fused_launch_count(const int64_t* len_prefix, int64_t max_len, int64_t N);
 
 // --- a6: FP64 re-run of flagged documents (no CPU fallback) --------------------------------
-constexpr int kFallbackBlocks = 296;  // 2 per SM
+constexpr int kFallbackBlocks = 148;  // 1 per SM (200 KB of shared memory each)
 size_t fallback_scratch_bytes(int64_t max_doc_nnz);
 void launch_fallback_fp64(const float* Mx, const float* colmin, int ld, const float* rpad, int v_r,
                           double lambda, int iters, float tol, int32_t* iters_doc,

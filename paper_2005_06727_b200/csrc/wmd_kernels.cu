@@ -66,6 +66,11 @@ __device__ __forceinline__ float4 ldg4_keep(const float4* p, uint64_t pol) {
 // a certified sum stays ~1e-6 relative (measured: DESIGN.md §4).
 constexpr float kUnderScale = 0x1p-133f;  // 2^-149 / 2^-16
 
+// FP64 fallback scratch per block: K (documents too long for shared memory) + v + final terms.
+__host__ __device__ constexpr int64_t fallback_block_doubles(int64_t max_doc_nnz) {
+  return max_doc_nnz * (WMD_MAX_VR_DEV + 1) + 2 * max_doc_nnz;
+}
+
 // ============================================================================================
 // a4 + a5. sinkhorn_pass<G, U, FINAL>: one pass over all target documents.
 //
@@ -364,6 +369,13 @@ __device__ __forceinline__ void block_maxmin_d(double mx, double mn, double* red
   __syncthreads();
 }
 
+// One block per flagged document (grid-stride over the device-side list). K = exp(-lambda
+// (M - m)) in FP64 lives in shared memory (row pitch v_r + 1 doubles: the SDDMM reads it with
+// threads over rows, the SpMM with threads over columns) when the document fits
+// (kFallbackSmem), else in a per-block global scratch with the same layout. The SpMM splits
+// the rows over two thread halves; gauge and change test are block reductions.
+constexpr int kFallbackSmem = 200 * 1024;
+
 __global__ void __launch_bounds__(256) fallback_fp64_kernel(
     const float* __restrict__ Mt, const float* __restrict__ colmin, int ld,
     const float* __restrict__ rpad, int v_r, double lambda, int iters, float tol,
@@ -371,64 +383,91 @@ __global__ void __launch_bounds__(256) fallback_fp64_kernel(
     const int32_t* __restrict__ flagged_list, const int32_t* __restrict__ flagged_count,
     double* __restrict__ scratch, int64_t max_doc_nnz, float* __restrict__ dist,
     uint8_t* __restrict__ flags, int32_t* __restrict__ breakdown, int32_t* __restrict__ fb_count) {
-  __shared__ double u[WMD_MAX_VR_DEV], un[WMD_MAX_VR_DEV];
-  __shared__ int gexp, stop;
+  extern __shared__ double ksm[];
+  __shared__ double u[WMD_MAX_VR_DEV], part[2][WMD_MAX_VR_DEV], red[3][8];
   const int n = *flagged_count;
-  const int ldx = ld + 4;
-  double* Kb = scratch + (int64_t)blockIdx.x * (max_doc_nnz * WMD_MAX_VR_DEV + 2 * max_doc_nnz);
-  double* vv = Kb + max_doc_nnz * WMD_MAX_VR_DEV;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ci = tid & 127, half = tid >> 7;
+  const int ldx = ld + 4, pitch = v_r + 1;
+  double* gK = scratch + (int64_t)blockIdx.x * fallback_block_doubles(max_doc_nnz);
+  double* vv = gK + max_doc_nnz * (WMD_MAX_VR_DEV + 1);
   double* qv = vv + max_doc_nnz;
   for (int idx = blockIdx.x; idx < n; idx += gridDim.x) {
     const int j = flagged_list[idx];
     const int b = doc_ptr[j], L = doc_ptr[j + 1] - b;
-    for (int p = threadIdx.x; p < L * v_r; p += blockDim.x) {
+    double* K = (int64_t)L * pitch * 8 <= kFallbackSmem ? ksm : gK;
+    for (int p = tid; p < L * v_r; p += blockDim.x) {  // K = exp(-lambda (M - m)), FP64
       const int e_ = p / v_r, i = p % v_r;
       const int k = ent[b + e_].k;
-      Kb[p] = exp(-lambda * ((double)Mt[(int64_t)k * ldx + i] - (double)colmin[k]));
+      K[(int64_t)e_ * pitch + i] = exp(-lambda * ((double)Mt[(int64_t)k * ldx + i] - (double)colmin[k]));
     }
-    for (int i = threadIdx.x; i < v_r; i += blockDim.x) u[i] = (double)v_r;  // x0 = 1/v_r
+    for (int i = tid; i < v_r; i += blockDim.x) u[i] = (double)v_r;  // x0 = 1/v_r
     __syncthreads();
     int it = 0;
     for (; it < iters; ++it) {
-      for (int e_ = threadIdx.x; e_ < L; e_ += blockDim.x) {
-        double s = 0.0;
-        for (int i = 0; i < v_r; ++i) s += Kb[(int64_t)e_ * v_r + i] * u[i];
-        vv[e_] = (double)ent[b + e_].c / s;
-      }
-      __syncthreads();
-      for (int i = threadIdx.x; i < v_r; i += blockDim.x) {
-        double a = 0.0;
-        for (int e_ = 0; e_ < L; ++e_) a += Kb[(int64_t)e_ * v_r + i] * vv[e_];
-        un[i] = (double)rpad[i] / a;
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        double mx = 0.0, mn = DBL_MAX, chg = 0.0;
-        for (int i = 0; i < v_r; ++i) {
-          mx = fmax(mx, un[i]); mn = fmin(mn, un[i]);
-          const double c = fabs(u[i] / un[i] - 1.0);  // "while x changes": |x_new/x - 1|
-          chg = c <= DBL_MAX ? fmax(chg, c) : DBL_MAX;
+      for (int e_ = tid; e_ < L; e_ += blockDim.x) {  // SDDMM (4 partial sums: pipelined loads)
+        const double* Ke = K + (int64_t)e_ * pitch;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int i = 0;
+        for (; i + 4 <= v_r; i += 4) {
+          s0 = fma(Ke[i], u[i], s0); s1 = fma(Ke[i + 1], u[i + 1], s1);
+          s2 = fma(Ke[i + 2], u[i + 2], s2); s3 = fma(Ke[i + 3], u[i + 3], s3);
         }
-        gexp = (mx > 0.0 && mn > 0.0 && mx <= DBL_MAX) ? ((ilogb(mx) + ilogb(mn)) >> 1) : 0;
-        stop = tol >= 0.f && chg <= (double)tol;
+        for (; i < v_r; ++i) s0 = fma(Ke[i], u[i], s0);
+        vv[e_] = (double)ent[b + e_].c / ((s0 + s1) + (s2 + s3));
       }
       __syncthreads();
-      for (int i = threadIdx.x; i < v_r; i += blockDim.x) u[i] = ldexp(un[i], -gexp);
+      for (int i0 = 0; i0 < v_r; i0 += 128) {  // SpMM, two row halves
+        const int i = i0 + ci;
+        if (i < v_r) {
+          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+          int e_ = half;
+          for (; e_ + 6 < L; e_ += 8) {
+            a0 = fma(K[(int64_t)e_ * pitch + i], vv[e_], a0);
+            a1 = fma(K[(int64_t)(e_ + 2) * pitch + i], vv[e_ + 2], a1);
+            a2 = fma(K[(int64_t)(e_ + 4) * pitch + i], vv[e_ + 4], a2);
+            a3 = fma(K[(int64_t)(e_ + 6) * pitch + i], vv[e_ + 6], a3);
+          }
+          for (; e_ < L; e_ += 2) a0 = fma(K[(int64_t)e_ * pitch + i], vv[e_], a0);
+          part[half][i] = (a0 + a1) + (a2 + a3);
+        }
+      }
       __syncthreads();
-      if (stop) { ++it; break; }
+      double mx = 0.0, mn = DBL_MAX, chg = 0.0, un = 0.0;
+      if (tid < v_r) {  // v_r <= WMD_MAX_VR <= blockDim
+        un = (double)rpad[tid] / (part[0][tid] + part[1][tid]);
+        mx = un; mn = un;
+        const double c = fabs(u[tid] / un - 1.0);  // "while x changes": |x_new/x - 1|
+        chg = c <= DBL_MAX ? c : DBL_MAX;
+      }
+#pragma unroll
+      for (int off = 16; off; off >>= 1) {
+        mx = fmax(mx, __shfl_xor_sync(kFull, mx, off));
+        mn = fmin(mn, __shfl_xor_sync(kFull, mn, off));
+        chg = fmax(chg, __shfl_xor_sync(kFull, chg, off));
+      }
+      if (lane == 0) { red[0][warp] = mx; red[1][warp] = mn; red[2][warp] = chg; }
+      __syncthreads();
+      mx = red[0][0]; mn = red[1][0]; chg = red[2][0];
+#pragma unroll
+      for (int w = 1; w < 8; ++w) { mx = fmax(mx, red[0][w]); mn = fmin(mn, red[1][w]); chg = fmax(chg, red[2][w]); }
+      const int gexp = (mx > 0.0 && mn > 0.0 && mx <= DBL_MAX) ? ((ilogb(mx) + ilogb(mn)) >> 1) : 0;
+      if (tid < v_r) u[tid] = ldexp(un, -gexp);
+      __syncthreads();
+      if (tol >= 0.f && chg <= (double)tol) { ++it; break; }
     }
-    for (int e_ = threadIdx.x; e_ < L; e_ += blockDim.x) {
+    for (int e_ = tid; e_ < L; e_ += blockDim.x) {  // final step
       const int k = ent[b + e_].k;
       double s = 0.0, t = 0.0;
       for (int i = 0; i < v_r; ++i) {
-        const double kk = Kb[(int64_t)e_ * v_r + i];
+        const double kk = K[(int64_t)e_ * pitch + i];
         s += kk * u[i];
         t += kk * (double)Mt[(int64_t)k * ldx + i] * u[i];
       }
       qv[e_] = ((double)ent[b + e_].c / s) * t;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
       double w = 0.0;
       for (int e_ = 0; e_ < L; ++e_) w += qv[e_];
       dist[j] = (float)w;
@@ -522,7 +561,7 @@ void launch_final_wmd(const int32_t* order, const int32_t* doc_ptr, const Entry*
 }
 
 size_t fallback_scratch_bytes(int64_t max_doc_nnz) {
-  return sizeof(double) * (size_t)kFallbackBlocks * (size_t)(max_doc_nnz * WMD_MAX_VR_DEV + 2 * max_doc_nnz);
+  return sizeof(double) * (size_t)kFallbackBlocks * (size_t)fallback_block_doubles(max_doc_nnz);
 }
 
 void launch_fallback_fp64(const float* Mt, const float* colmin, int ld, const float* rpad, int v_r,
@@ -531,7 +570,12 @@ void launch_fallback_fp64(const float* Mt, const float* colmin, int ld, const fl
                           const int32_t* flagged_list, const int32_t* flagged_count,
                           double* scratch, int64_t max_doc_nnz, float* dist, uint8_t* flags,
                           int32_t* breakdown, int32_t* fallback_count, cudaStream_t st) {
-  fallback_fp64_kernel<<<kFallbackBlocks, 256, 0, st>>>(Mt, colmin, ld, rpad, v_r, lambda, iters, tol,
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(fallback_fp64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFallbackSmem);
+    attr = true;
+  }
+  fallback_fp64_kernel<<<kFallbackBlocks, 256, kFallbackSmem, st>>>(Mt, colmin, ld, rpad, v_r, lambda, iters, tol,
                                                         iters_doc, doc_ptr,
                                                         ent, flagged_list, flagged_count, scratch,
                                                         max_doc_nnz, dist, flags, breakdown,

@@ -53,6 +53,16 @@ K_BEGIN(k_ffma2)
   float s = 0; for (int i = 0; i < 8; ++i) s += a[i].x + a[i].y;
 K_END(s)
 
+K_BEGIN(k_dfma)
+  double a[8], bb[8];
+  for (int i = 0; i < 8; ++i) { a[i] = lane * 0.1 + i; bb[i] = 1.0 + i * 1e-9; }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = fma(a[i], bb[i], bb[(i + 1) & 7]);
+  }
+  double s = 0; for (int i = 0; i < 8; ++i) s += a[i];
+K_END((float)s)
+
 K_BEGIN(k_shfl)
   float a[8];
   for (int i = 0; i < 8; ++i) a[i] = lane * 0.1f + i;
@@ -135,7 +145,7 @@ int main() {
   float* out; long long* clk;
   cudaMalloc(&out, 1 << 20); cudaMalloc(&clk, 8);
   struct { const char* name; KF f; } ks[] = {
-    {"ffma_imm", k_ffma}, {"ffma3", k_ffma3}, {"ffma2", k_ffma2}, {"shfl", k_shfl}, {"lds128_bcast", k_lds128b},
+    {"ffma_imm", k_ffma}, {"ffma3", k_ffma3}, {"ffma2", k_ffma2}, {"dfma", k_dfma}, {"shfl", k_shfl}, {"lds128_bcast", k_lds128b},
     {"lds128", k_lds128}, {"lds32", k_lds32}, {"redux", k_redux}, {"mufu_rcp", k_mufu}};
   int sms = 0; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   for (auto& k : ks) {
