@@ -65,6 +65,11 @@ struct Shape {
   static constexpr int REGS = RW * CW;
 };
 
+__device__ __forceinline__ float lg2_approx(float x) {
+  float y;
+  asm("lg2.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ float ex2_ftz(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -211,7 +216,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW>()) sinkhorn_f
   extern __shared__ __align__(16) float smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int a = lane >> 3, b = lane & 7;
-  float* buf0 = smem + wib * 2 * S::BUF;
+  float* buf = smem + wib * S::BUF;        // the staged M rows of one document
   const int64_t nwarps = (int64_t)gridDim.x * kWarps;
   const uint64_t keep = l2_evict_last_policy();
   const int2* ent2 = reinterpret_cast<const int2*>(ent);
@@ -236,7 +241,6 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW>()) sinkhorn_f
   int pj = -1, pb = 0, pn = 0;
   int pk[NW];
   float pc[NW];
-  int cur = 0;
   auto stage1 = [&](int64_t p) {
     pj = -1; pn = 0;
     if (p < pos1) {
@@ -272,7 +276,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW>()) sinkhorn_f
 
   stage1(pos);
   stage2();
-  stage3(buf0);
+  stage3(buf);
 
   for (; pos < pos1; pos += nwarps) {
     const int j = pj, n = pn;
@@ -289,8 +293,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW>()) sinkhorn_f
       c_own[NT] = __shfl_sync(kFull, pc[NT], tr);
       v_ok[NT] = 32 * NT + tr < n;
     }
-    float* Sb = buf0 + cur * S::BUF;          // this document's M rows (row e at Sb + e*P)
-    float* Nb = buf0 + (cur ^ 1) * S::BUF;    // the next document's rows
+    const float* Sb = buf;                    // this document's M rows (row e at Sb + e*P)
     stage1(pos + nwarps);
     cp_async_wait_all();
     __syncwarp();
@@ -336,6 +339,16 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW>()) sinkhorn_f
       to_slots<CW>(K[s], a);
     }
     const bool und = __any_sync(kFull, flushed);
+    // for the final step (which then needs no M): m of the own rows, mu in slot order
+    float m_own[NOWN];
+#pragma unroll
+    for (int T = 0; T < NT; ++T) m_own[T] = v_ok[T] ? Sb[(32 * T + lane) * P + LD] : 0.f;
+    if constexpr (TW > 0) m_own[NT] = v_ok[NT] ? Sb[(32 * NT + TW * a + (b >> S::TSH)) * P + LD] : 0.f;
+    float mu_s[CW];
+#pragma unroll
+    for (int c = 0; c < CW; ++c) mu_s[c] = mu[c];
+    to_slots<CW>(mu_s, a);
+    __syncwarp();  // every lane is done with the staged rows: the buffer takes the next document
     // uh0 = v_r 2^(-alpha mu) on real columns (slot order)
     float u[CW];
 #pragma unroll
@@ -349,7 +362,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW>()) sinkhorn_f
     float umax_k = (float)v_r * kv_s;   // v_r * max(uh) * 2^-110 (max uh0 <= v_r)
     bool bad = false, done = false;
     uint32_t badu = 0u;
-    float v_own[NOWN];
+    float v_own[NOWN], s_own[NOWN];
     int it = 0;
     for (;; ++it) {
       // SDDMM: row partials over this lane's columns, then the reduce over the b-lanes
@@ -366,6 +379,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW>()) sinkhorn_f
 #pragma unroll
       for (int o = 0; o < NOWN; ++o) {
         const float sv = p[8 * o];
+        s_own[o] = sv;
         v_own[o] = v_ok[o] ? c_own[o] * rcp_fast(sv) : 0.f;
 #ifndef WMD_EXP_NO_CERT
         bad |= v_ok[o] && und && umax_k > sv;
@@ -375,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW>()) sinkhorn_f
       if (it == iters || (CONV && done)) break;
       if (it == 1) {  // the next document's entries have landed: start its row copies
         staged = true;
-        stage3(Nb);
+        stage3(buf);
       }
 #ifndef WMD_EXP_NO_CERT
       vmax_b = __reduce_max_sync(kFull, vmax_b);
@@ -445,30 +459,33 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW>()) sinkhorn_f
         u[0] = uo[0];
       }
     }
-    if (!staged) stage3(Nb);
-    // ---- final step: WMD_j = sum_e vh_e q_e,  q_e = sum_i Kh_ei M_ie uh_i
+    if (!staged) stage3(buf);
+    // ---- final step: WMD_j = sum_e vh_e q_e,  q_e = sum_i Kh_ei M_ie uh_i  (PAPER.md:66)
+    // M is recovered from the block itself: Kh = 2^(-alpha (D - mu)) gives
+    //   M_ie = D_ei + m_e = mu_i + m_e - log2(Kh_ei) / alpha,
+    // so q_e = sum_i Kh_ei uh_i (mu_i - log2(Kh_ei)/alpha) + m_e s_e with s_e = Kh uh from the
+    // last SDDMM. Entries flushed to 0 contribute 0 (Kh log2 Kh -> 0).
+    const float ia = -1.f / alpha;
     float p[RW];
 #pragma unroll
     for (int s = 0; s < RW; ++s) {
-      const int e = row_of<NT, TW>(s, a, b);
-      const bool ok = e < n;
-      float x[CW];
-      load_cols<CW>(Sb + (ok ? e : 0) * P, b, x);
-      to_slots<CW>(x, a);
-#pragma unroll
-      for (int c = 0; c < CW; ++c) x[c] = ok ? x[c] : 0.f;   // stale rows past n
       float acc = 0.f;
 #pragma unroll
-      for (int c = 0; c < CW; ++c) acc = fmaf(K[s][c] * x[c], u[c], acc);
+      for (int c = 0; c < CW; ++c) {
+        const float k = K[s][c];
+        const float kl = k > 0.f ? k * lg2_approx(k) : 0.f;
+        acc = fmaf(fmaf(kl, ia, k * mu_s[c]), u[c], acc);
+      }
       p[s] = acc;
     }
     reduce_rows<NT, TW>(p);
     float wsum = 0.f;
 #pragma unroll
     for (int T = 0; T < NT; ++T)
-      if (v_ok[T]) wsum = fmaf(v_own[T], p[8 * T], wsum);
+      if (v_ok[T]) wsum = fmaf(v_own[T], fmaf(m_own[T], s_own[T], p[8 * T]), wsum);
     if constexpr (TW > 0) {  // each tail row is held by 2^TSH lanes: count it once
-      if (v_ok[NT] && (b & ((1 << S::TSH) - 1)) == 0) wsum = fmaf(v_own[NT], p[8 * NT], wsum);
+      if (v_ok[NT] && (b & ((1 << S::TSH) - 1)) == 0)
+        wsum = fmaf(v_own[NT], fmaf(m_own[NT], s_own[NT], p[8 * NT]), wsum);
     }
 #pragma unroll
     for (int off = 16; off; off >>= 1) wsum += shx(wsum, off);
@@ -481,8 +498,6 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW>()) sinkhorn_f
         flagged_list[atomicAdd(flagged_count, 1)] = j;
       }
     }
-    __syncwarp();  // all lanes are done with Sb before it becomes the next staging buffer
-    cur ^= 1;
   }
   cp_async_wait_all();  // nothing may be in flight when the warp exits
 }
@@ -504,7 +519,7 @@ void launch_fused_range_t(const int4* sdoc, const Entry* ent, int64_t p0,
                         int iters, float tol, int32_t* itd, float* dist, uint8_t* flags, int32_t* fl,
                         int32_t* fc, cudaStream_t st) {
   if (p1 <= p0) return;
-  constexpr size_t smem = sizeof(float) * 2 * Shape<CW, NT, TW>::BUF * kWarps;
+  constexpr size_t smem = sizeof(float) * Shape<CW, NT, TW>::BUF * kWarps;
   static int resident = 0;
   if (!resident) {
     cudaFuncSetAttribute(sinkhorn_fused_kernel<CW, NT, TW, CONV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -1,3 +1,3 @@
 python -m paper_2005_06727_b200.build > /dev/null 2>&1
-python tools/pass_timing.py long auto 1 > gpurun_out/plain_fb.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:fallback -s 2 -c 1 -o gpurun_out/prof_fallback python tools/pass_timing.py long auto 1 > gpurun_out/ncu_fb.log 2>&1; echo ncu=$?
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?; tail -3 gpurun_out/pytest_gpu.log
+for c in scaling tweet many; do python tools/pass_timing.py $c auto 5; done
