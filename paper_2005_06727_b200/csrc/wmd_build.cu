@@ -147,10 +147,269 @@ __global__ void __launch_bounds__(kThreads, 2) build_mx_kernel(
   }
 }
 
+// ============================================================================================
+// Tensor-core variant (NEXT-4, "GEMM-like" distance): the cross term of
+//     M_ik^2 = |E_k|^2 + |q_i|^2 - 2 E_k . q_i
+// on the 5th-generation tensor cores in 3xTF32 (exact-FP32 emulation: x = hi + lo with hi the
+// TF32 truncation; E.q ~ hi.hi + hi.lo + lo.hi, the lo.lo term below FP32 rounding), FP32
+// accumulation in TMEM. The norms are FP32 sums of the same staged values. Cancellation: where
+// M^2 < kNearFrac (|E_k|^2 + |q_i|^2) the distance is recomputed by direct difference (and
+// M_{i,sel_i} = 0 exactly), so near-duplicate words keep the direct-difference accuracy that
+// exp(-lambda M) needs.
+//
+// Block: 128 threads, 128 vocabulary rows (TMEM lanes) x NP query rows (TMEM columns, NP = v_r
+// rounded up to 32, <= 128). d streams in 32-float chunks, double buffered with cp.async
+// straight into the K-major no-swizzle core-matrix layout the MMA descriptors read (8 rows x
+// 16 B per core matrix); the threads add the lo parts and the squared norms; one elected thread
+// issues 12 tcgen05.mma (M=128, N=NP, K=8) per chunk and commits them to the stage's mbarrier.
+// Epilogue: tcgen05.ld of each thread's accumulator row (row = TMEM lane), sqrt, column minimum,
+// Mx / K~ rows. Bound: reading E once from HBM (the MMAs need ~2 % of the tensor peak).
+// ============================================================================================
+constexpr int TC_M = 128;             // vocabulary rows per block (MMA M, TMEM lanes)
+#ifndef WMD_TC_CHUNK
+#define WMD_TC_CHUNK 16
+#endif
+constexpr int TC_K = WMD_TC_CHUNK;    // d chunk (floats)
+#ifndef WMD_TC_STAGES
+#define WMD_TC_STAGES 3
+#endif
+constexpr int TC_NS = WMD_TC_STAGES;  // pipeline stages
+constexpr float kNearFrac = 1.0f / 64.f;
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+// byte offset of element (r, k) (k < 32) in a K-major no-swizzle tile of R rows: core matrices
+// of 8 rows x 4 floats; SBO = 128 B between 8-row groups, LBO = R/8 * 128 B between K quads
+__device__ __forceinline__ uint32_t km_off(int r, int k, int R) {
+  return (uint32_t)((k >> 2) * (R / 8 * 128) + (r >> 3) * 128 + (r & 7) * 16 + (k & 3) * 4);
+}
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);  // version 1, no swizzle
+}
+__device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n"
+      ::"r"(tmem), "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+                 "selp.b32 %0, 1, 0, P1;\n\t}\n" : "=r"(done) : "r"(bar), "r"(parity));
+  }
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int c = 0; c < 32; ++c) v[c] = __uint_as_float(r[c]);
+}
+
+template <int NP>
+__global__ void __launch_bounds__(128, NP <= 32 ? 2 : 1) build_mx_tc_kernel(
+    const float* __restrict__ E, int64_t V, int dp, const int32_t* __restrict__ sel, int v_r,
+    int ld, float lambda, float* __restrict__ Kt, float* __restrict__ Mx,
+    float* __restrict__ colmin) {
+  constexpr int A_BYTES = TC_M * TC_K * 4, B_BYTES = NP * TC_K * 4;
+  constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;          // raw (= hi) and lo, A and B
+  constexpr uint32_t TMEM_COLS = NP <= 32 ? 32 : (NP <= 64 ? 64 : 128);
+  constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NP >> 3) << 17) |
+                             ((uint32_t)(TC_M >> 4) << 24);   // F32 += TF32 x TF32, K-major both
+  extern __shared__ __align__(1024) uint8_t tc_smem[];
+  uint8_t* smem = tc_smem;
+  __shared__ uint32_t tmem_base;
+  __shared__ __align__(8) uint64_t mbar[TC_NS];
+  __shared__ float qn[NP];
+  __shared__ int32_t qsel[NP];
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int64_t k0 = (int64_t)blockIdx.x * TC_M;
+  const int nchunk = dp / TC_K;
+  const int ldx = ld + 4;
+  if (tid < NP) qsel[tid] = tid < v_r ? sel[tid] : -1;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_base)), "n"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < TC_NS; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&mbar[i])), "r"(1));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tm = tmem_base;
+
+  // raw chunk copies: A rows k0 + r (zero past V), B rows = the query rows (zero past v_r)
+  auto issue = [&](int c, int st) {
+    uint8_t* base = smem + st * STAGE;
+    for (int p = tid; p < TC_M * (TC_K / 4); p += 128) {
+      const int r = p / (TC_K / 4), q = p % (TC_K / 4);
+      const bool ok = k0 + r < V;
+      const float* src = E + (ok ? k0 + r : 0) * (int64_t)dp + c * TC_K + 4 * q;
+      const uint32_t dst = su32(base + km_off(r, 4 * q, TC_M));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0) : "memory");
+    }
+    for (int p = tid; p < NP * (TC_K / 4); p += 128) {
+      const int r = p / (TC_K / 4), q = p % (TC_K / 4);
+      const int row = qsel[r];
+      const float* src = E + (row >= 0 ? row : 0) * (int64_t)dp + c * TC_K + 4 * q;
+      const uint32_t dst = su32(base + 2 * A_BYTES + km_off(r, 4 * q, NP));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(row >= 0 ? 16 : 0) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  __syncthreads();  // qsel
+  float en = 0.f, qq = 0.f;   // |E_row|^2 of this thread's vocabulary row; |q|^2 (tid < NP)
+  // copies run TC_NS - 2 chunks ahead: the stage being refilled was read by the MMAs of chunk
+  // c - 2, which have had a whole chunk step to complete
+  constexpr int AHEAD = TC_NS - 2;
+  for (int c = 0; c < AHEAD; ++c) {
+    if (c < nchunk) issue(c, c);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  for (int c = 0; c < nchunk; ++c) {
+    const int st = c % TC_NS;
+    const int cn = c + AHEAD;
+    if (cn < nchunk) {
+      if (cn >= TC_NS) mbar_wait(su32(&mbar[cn % TC_NS]), ((cn - TC_NS) / TC_NS) & 1);
+      issue(cn, cn % TC_NS);
+    } else {
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    asm volatile("cp.async.wait_group %0;" ::"n"(AHEAD) : "memory");  // chunk c has landed
+    __syncthreads();
+    uint8_t* base = smem + st * STAGE;
+    // lo parts and norms: thread tid owns vocabulary row tid (and query row tid < NP)
+#pragma unroll
+    for (int q = 0; q < TC_K / 4; ++q) {
+      const uint32_t off = km_off(tid, 4 * q, TC_M);
+      const float4 x = *reinterpret_cast<const float4*>(base + off);
+      en = fmaf(x.x, x.x, en); en = fmaf(x.y, x.y, en); en = fmaf(x.z, x.z, en); en = fmaf(x.w, x.w, en);
+      float4 lo;
+      lo.x = x.x - __uint_as_float(__float_as_uint(x.x) & 0xffffe000u);
+      lo.y = x.y - __uint_as_float(__float_as_uint(x.y) & 0xffffe000u);
+      lo.z = x.z - __uint_as_float(__float_as_uint(x.z) & 0xffffe000u);
+      lo.w = x.w - __uint_as_float(__float_as_uint(x.w) & 0xffffe000u);
+      *reinterpret_cast<float4*>(base + A_BYTES + off) = lo;
+    }
+    if (tid < NP) {
+#pragma unroll
+      for (int q = 0; q < TC_K / 4; ++q) {
+        const uint32_t off = 2 * A_BYTES + km_off(tid, 4 * q, NP);
+        const float4 x = *reinterpret_cast<const float4*>(base + off);
+        qq = fmaf(x.x, x.x, qq); qq = fmaf(x.y, x.y, qq); qq = fmaf(x.z, x.z, qq); qq = fmaf(x.w, x.w, qq);
+        float4 lo;
+        lo.x = x.x - __uint_as_float(__float_as_uint(x.x) & 0xffffe000u);
+        lo.y = x.y - __uint_as_float(__float_as_uint(x.y) & 0xffffe000u);
+        lo.z = x.z - __uint_as_float(__float_as_uint(x.z) & 0xffffe000u);
+        lo.w = x.w - __uint_as_float(__float_as_uint(x.w) & 0xffffe000u);
+        *reinterpret_cast<float4*>(base + 2 * A_BYTES + B_BYTES + (off - 2 * A_BYTES)) = lo;
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t a_hi = su32(base), a_lo = a_hi + A_BYTES;
+      const uint32_t b_hi = su32(base + 2 * A_BYTES), b_lo = b_hi + B_BYTES;
+#pragma unroll
+      for (int pass = 0; pass < 3; ++pass) {          // hi.hi + hi.lo + lo.hi
+        const uint32_t a = pass == 2 ? a_lo : a_hi, b = pass == 1 ? b_lo : b_hi;
+#pragma unroll
+        for (int kk = 0; kk < TC_K; kk += 8) {
+          const uint64_t da = umma_desc(a + (kk >> 2) * (TC_M / 8 * 128), TC_M / 8 * 128, 128);
+          const uint64_t db = umma_desc(b + (kk >> 2) * (NP / 8 * 128), NP / 8 * 128, 128);
+          mma_tf32(tm, da, db, IDESC, (c | pass | kk) ? 1u : 0u);
+        }
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&mbar[st])));
+    }
+  }
+  if (tid < NP) qn[tid] = qq;
+  // the last chunk's commit also covers every earlier MMA
+  mbar_wait(su32(&mbar[(nchunk - 1) % TC_NS]), ((nchunk - 1) / TC_NS) & 1);
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  __syncthreads();  // qn
+
+  // ---- epilogue: thread tid = vocabulary row k0 + tid = TMEM lane tid
+  const int64_t k = k0 + tid;
+  const bool kok = k < V;
+  float Mrow[NP];
+  uint32_t near[(NP + 31) / 32];
+#pragma unroll
+  for (int c0 = 0; c0 < NP; c0 += 32) {
+    float dot[32];
+    tmem_ld32(tm + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, dot);
+    uint32_t nb = 0u;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      const float m2 = fmaxf(en + qn[c0 + c] - 2.f * dot[c], 0.f);
+      Mrow[c0 + c] = sqrtf(m2);
+      if (c0 + c < v_r && m2 < kNearFrac * (en + qn[c0 + c])) nb |= 1u << c;
+    }
+    near[c0 / 32] = nb;
+  }
+  if (kok) {
+    // cancellation-prone pairs (rare; M_{i,sel_i} among them): direct difference
+#pragma unroll
+    for (int w = 0; w < (NP + 31) / 32; ++w) {
+      for (uint32_t nb = near[w]; nb; nb &= nb - 1) {
+        const int i = 32 * w + __ffs(nb) - 1;
+        const float* er = E + k * (int64_t)dp;
+        const float* qr = E + (int64_t)qsel[i] * dp;
+        float s2 = 0.f;
+        for (int t = 0; t < dp; ++t) { const float df = qr[t] - er[t]; s2 = fmaf(df, df, s2); }
+        const float m = sqrtf(s2);  // == 0 exactly for k == sel_i
+#pragma unroll
+        for (int ii = 0; ii < NP; ++ii) if (ii == i) Mrow[ii] = m;
+      }
+    }
+    float mn = FLT_MAX;
+#pragma unroll
+    for (int i = 0; i < NP; ++i) if (i < v_r) mn = fminf(mn, Mrow[i]);
+    float* row = reinterpret_cast<float*>(smem) + tid * (ldx + 1);  // staging buffers are idle
+#pragma unroll
+    for (int i = 0; i < NP; ++i)
+      if (i < ldx) row[i] = i < v_r ? Mrow[i] : (i == ld ? mn : 0.f);
+    for (int x = NP; x < ldx; ++x) row[x] = x == ld ? mn : 0.f;
+    colmin[k] = mn;
+  }
+  __syncthreads();
+  // the block's rows are contiguous in Mx (and K~): coalesced copies out of shared memory
+  const int rows = (int)(V - k0 < TC_M ? V - k0 : TC_M);
+  {
+    const float* tile = reinterpret_cast<const float*>(smem);
+    float* dst = Mx + k0 * ldx;
+    for (int g = tid; g < rows * ldx; g += 128) dst[g] = tile[(g / ldx) * (ldx + 1) + g % ldx];
+    if (Kt) {
+      float* kd = Kt + k0 * ld;
+      for (int g = tid; g < rows * ld; g += 128) {
+        const int r = g / ld, x = g % ld;
+        const float mv = tile[r * (ldx + 1) + x], mn = tile[r * (ldx + 1) + ld];
+        kd[g] = x < v_r ? expf(-lambda * (mv - mn)) : 0.f;
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "n"(TMEM_COLS));
+}
+
 }  // namespace
 
 void launch_build_ktilde(const float* E, int64_t V, int dp, const int32_t* sel, int v_r, int ld,
-                         float lambda, float* Kt, float* Mx, float* colmin, cudaStream_t st) {
+                         float lambda, float* Kt, float* Mx, float* colmin, bool use_tc, cudaStream_t st) {
   constexpr size_t smem = sizeof(float) * 2 * kStageFloats;
   static_assert(BW * kMsPitch <= 2 * kStageFloats, "M tile must fit in the staging buffers");
   static bool attr = false;
@@ -158,8 +417,24 @@ void launch_build_ktilde(const float* E, int64_t V, int dp, const int32_t* sel, 
     cudaFuncSetAttribute(build_mx_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  const int64_t grid = (V + BW - 1) / BW;
-  build_mx_kernel<<<(unsigned)grid, kThreads, smem, st>>>(E, V, dp, sel, v_r, ld, lambda, Kt, Mx, colmin);
+  if (!use_tc) {
+    const int64_t grid = (V + BW - 1) / BW;
+    build_mx_kernel<<<(unsigned)grid, kThreads, smem, st>>>(E, V, dp, sel, v_r, ld, lambda, Kt, Mx, colmin);
+    return;
+  }
+  const unsigned grid = (unsigned)((V + TC_M - 1) / TC_M);
+#define TC_(NP)                                                                                       \
+  {                                                                                                   \
+    constexpr size_t sm = TC_NS * (2 * TC_M * TC_K * 4 + 2 * NP * TC_K * 4);                              \
+    static bool a = false;                                                                            \
+    if (!a) { cudaFuncSetAttribute(build_mx_tc_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); a = true; } \
+    build_mx_tc_kernel<NP><<<grid, 128, sm, st>>>(E, V, dp, sel, v_r, ld, lambda, Kt, Mx, colmin);   \
+  }
+  if (v_r <= 32) TC_(32)
+  else if (v_r <= 64) TC_(64)
+  else if (v_r <= 96) TC_(96)
+  else TC_(128)
+#undef TC_
 }
 
 }  // namespace wmd

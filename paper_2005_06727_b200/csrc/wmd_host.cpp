@@ -124,7 +124,7 @@ struct wmd_handle {
   std::vector<int32_t> h_sel;
   std::vector<float> h_r;
   // options
-  int64_t opt_path = WMD_PATH_AUTO, opt_timing = 0, opt_fallback = 1, opt_graph = 0;
+  int64_t opt_path = WMD_PATH_AUTO, opt_timing = 0, opt_fallback = 1, opt_graph = 0, opt_build = 0;
   // stats
   wmd_stats st{};
   std::vector<PhaseEvents> events;
@@ -422,6 +422,10 @@ wmd_status wmd_set_option(wmd_handle* h, int32_t option, int64_t value) {
     case WMD_OPT_TIMING: h->opt_timing = value != 0; return WMD_OK;
     case WMD_OPT_FALLBACK: h->opt_fallback = value != 0; return WMD_OK;
     case WMD_OPT_GRAPH: h->opt_graph = value != 0; return WMD_OK;
+    case WMD_OPT_BUILD:
+      if (value < 0 || value > 1) return fail(h, WMD_ERR_INVALID_ARGUMENT, "bad build kernel");
+      h->opt_build = value;
+      return WMD_OK;
   }
   return fail(h, WMD_ERR_INVALID_ARGUMENT, "unknown option %d", option);
 }
@@ -542,7 +546,7 @@ wmd_status enqueue_query(wmd_handle* h, const int32_t* d_sel, const float* d_r, 
   int64_t launches = 0;
   // a2: M (+ m), and K~ for the per-iteration path
   wmd::launch_build_ktilde(h->E.p, h->V, h->dp, d_sel, v_r, ld, lambda, fused ? nullptr : h->Kt.p,
-                           h->Mx.p, h->colmin.p, st);
+                           h->Mx.p, h->colmin.p, h->opt_build == 0, st);
   h->kt_valid = !fused;
   ++launches;
   if (pe) CK(h, cudaEventRecord(pe->ev[1], st));

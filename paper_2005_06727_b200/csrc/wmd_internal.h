@@ -34,7 +34,7 @@ struct QueryDev {
 // Kt (V x ld, K~ = exp(-lambda (M - m))) is written only when non-null (per-iteration path).
 // E: V rows of dp floats (d padded with zeros to a multiple of 32).
 void launch_build_ktilde(const float* E, int64_t V, int dp, const int32_t* sel, int v_r, int ld,
-                         float lambda, float* Kt, float* Mx, float* colmin, cudaStream_t st);
+                         float lambda, float* Kt, float* Mx, float* colmin, bool use_tc, cudaStream_t st);
 
 // "While x changes" (NEXT-3): tol < 0 runs the fixed iteration count. Otherwise a
 // document stops after the first x-update with max_i |x_new/x - 1| <= tol (R31);

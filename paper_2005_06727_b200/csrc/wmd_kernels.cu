@@ -347,28 +347,6 @@ __global__ void __launch_bounds__(256, FINAL ? 2 : PASS_BLOCKS_PER_SM) sinkhorn_
 // FP32 *range* failed (measured: DESIGN.md §4). Deterministic: sequential per-thread sums and a
 // serial final sum.
 // ============================================================================================
-__device__ __forceinline__ double warp_sum_d(double x) {
-#pragma unroll
-  for (int off = 16; off; off >>= 1) x += __shfl_xor_sync(kFull, x, off);
-  return x;
-}
-
-// Block (256 threads) max and min of per-thread doubles; all threads receive the results.
-__device__ __forceinline__ void block_maxmin_d(double mx, double mn, double* red, double& omx, double& omn) {
-#pragma unroll
-  for (int off = 16; off; off >>= 1) {
-    mx = fmax(mx, __shfl_xor_sync(kFull, mx, off));
-    mn = fmin(mn, __shfl_xor_sync(kFull, mn, off));
-  }
-  const int w = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0) { red[w] = mx; red[8 + w] = mn; }
-  __syncthreads();
-  omx = red[0]; omn = red[8];
-#pragma unroll
-  for (int k = 1; k < 8; ++k) { omx = fmax(omx, red[k]); omn = fmin(omn, red[8 + k]); }
-  __syncthreads();
-}
-
 // One block per flagged document (grid-stride over the device-side list). K = exp(-lambda
 // (M - m)) in FP64 lives in shared memory (row pitch v_r + 1 doubles: the SDDMM reads it with
 // threads over rows, the SpMM with threads over columns) when the document fits

@@ -143,6 +143,39 @@ def test_query_compaction_bit_exact(W):
         W.wmd_destroy(h)
 
 
+@pytest.mark.parametrize("v_r", [1, 7, 30, 33, 64, 65, 100, 128])
+def test_build_tensor_core_equals_simt_and_oracle(W, v_r):
+    """a2 on the tensor cores (3xTF32 GEMM form, default) against the SIMT direct-difference
+    build and the FP64 oracle's M: every query width class (N = 32/64/96/128 MMA tiles), a
+    vocabulary that is not a multiple of the 128-row tile, exact zeros at the query words."""
+    wl = synth.make_workload("tiny")
+    V = 1000 + 77
+    E = wl.E[:V]
+    rng = np.random.default_rng(v_r)
+    q = np.sort(rng.choice(V, v_r, replace=False)).astype(np.int32)
+    w = np.full(v_r, 1.0 / v_r, np.float32)
+    cp, ri, va = synth.csc_from_lists([{int(k): 1.0} for k in (0, 5, V - 1)], V)
+    out = {}
+    for build in (0, 1):
+        h = W.wmd_create(E)
+        try:
+            W.wmd_set_option(h, W.WMD_OPT_BUILD, build)
+            W.wmd_set_option(h, W.WMD_OPT_PATH, W.WMD_PATH_PER_ITER)
+            W.wmd_set_targets(h, cp, ri, va)
+            W.wmd_query(h, q, w, 10.0, 2, np.empty(3, np.float32))
+            ld = W.wmd_get_stats(h)["last_ld"]
+            out[build] = W.wmd_read_kernel(h, 0, V, ld)
+        finally:
+            W.wmd_destroy(h)
+    M = oracle.euclidean_rows(E, q).T                      # (V, v_r) FP64
+    for build in (0, 1):
+        kt, km, cm = out[build]
+        np.testing.assert_allclose(km[:, :v_r], M, rtol=2e-6, atol=2e-5)
+        assert np.all(km[q, np.arange(v_r)] == 0.0)
+        np.testing.assert_allclose(cm, M.min(axis=1), rtol=2e-6, atol=2e-5)
+    np.testing.assert_allclose(out[0][1], out[1][1], rtol=2e-6, atol=2e-5)
+
+
 @pytest.mark.parametrize("name", ["tiny", "tweet"])
 def test_kernel_build_parity(W, name):
     """a2: M and K~ = exp(-lambda (M - min_i M)) against the FP64 oracle's M."""
