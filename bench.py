@@ -275,6 +275,7 @@ def main():
     ap.add_argument("--path", default="auto", choices=["auto", "iter", "fused"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--graph", action="store_true", help="replay each query as a CUDA graph (WMD_OPT_GRAPH)")
     args = ap.parse_args()
 
     wl = synth.make_workload(args.config)
@@ -305,8 +306,11 @@ def main():
     v_r = len(q)
     path = {"auto": wmd.WMD_PATH_AUTO, "iter": wmd.WMD_PATH_PER_ITER, "fused": wmd.WMD_PATH_FUSED}[args.path]
     E = torch.from_numpy(wl.E).cuda()
-    eng = ShardedEngine(E, wl.col_ptr, wl.row_idx, wl.val, rank, world, local_rank, path=path, timing=True)
+    eng = ShardedEngine(E, wl.col_ptr, wl.row_idx, wl.val, rank, world, local_rank, path=path,
+                        timing=not args.graph)
     h = eng.engine.h
+    if args.graph:
+        wmd.wmd_set_option(h, wmd.WMD_OPT_GRAPH, 1)
     stream = torch.cuda.current_stream()
     small = (cfg.V * cfg.d * 4 + wl.nnz * 8) <= 2 * L2_BYTES
     flush = torch.empty(256 * 2 ** 20 // 4, dtype=torch.float32, device="cuda") if small else None
@@ -375,7 +379,9 @@ def main():
         launches_per_query = st["kernel_launches"] / max(1, st["queries"]) if st else 0
         nl, nnz_l = eng.n_local, eng.nnz_local
         path_used = st["last_path"] if st else 0
-        if path_used == wmd.WMD_PATH_PER_ITER:
+        if not (st and st["timing_valid"]):
+            roofline = {"kernel": None, "note": "per-phase timing is off in --graph mode (one graph per query)"}
+        elif path_used == wmd.WMD_PATH_PER_ITER:
             n_iter_launch = st["iter_launches"]
             t_launch = st["iter_ms"] / 1e3 / max(1, n_iter_launch)
             B_it = 8 * nnz_l + 4 * (nl + 1) + 8 * v_r * nl      # streamed (HBM) bytes per launch
@@ -418,12 +424,13 @@ def main():
             "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded Zipf bag-of-words, N(0,1) embeddings; BASELINE.json config)",
-            "config": config_dict(cfg, wl, args, path=args.path),
+            "config": config_dict(cfg, wl, args, path=args.path, graph=bool(args.graph)),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(v_r * 8),
                     "d2h_bytes_per_step": int(wl.N * 4)},
             "gpu_launches": int(st["kernel_launches"]) if st else 0,
             "roofline": roofline,
-            "phases_ms_per_step": {k: st[k] / args.steps for k in ("build_ms", "iter_ms", "final_ms", "fallback_ms", "query_ms")},
+            "phases_ms_per_step": ({k: st[k] / args.steps for k in ("build_ms", "iter_ms", "final_ms", "fallback_ms", "query_ms")}
+                                   if st and st["timing_valid"] else None),
             "fallback_docs": int(st_sync["fallback_docs"]) if st_sync else 0,
             "launches_per_query": launches_per_query,
             "clocks": clk.summary(),

@@ -75,7 +75,11 @@ typedef enum {
   WMD_OPT_PATH = 1,        /* wmd_path; default WMD_PATH_AUTO */
   WMD_OPT_TIMING = 2,      /* 1: record CUDA events per phase (read with wmd_get_stats); default 0 */
   WMD_OPT_FALLBACK = 3,    /* 1: FP64 re-run of flagged documents (default); 0: leave them flagged */
-  WMD_OPT_GRAPH = 4,       /* 1: replay the query as a CUDA graph when the shape repeats; default 0 */
+  WMD_OPT_GRAPH = 4,       /* 1: capture a query's launches (build, Sinkhorn, final, fallback) once
+                              and replay them as a CUDA graph while the query width, lambda, iters,
+                              tolerance, path, output pointer and buffers repeat (the query rows are
+                              re-uploaded every call); per-phase timing is off in this mode.
+                              Default 0 */
   WMD_OPT_BUILD = 5        /* distance build (a2): 0 = tensor cores, 3xTF32 GEMM form (default);
                               1 = SIMT direct difference (PAPER.md:259-268 compares the two forms) */
 } wmd_option;

@@ -70,6 +70,27 @@ struct PhaseEvents {
   cudaEvent_t ev[5];  // start, after build, after iterations, after final, after fallback
 };
 
+// What a captured query graph depends on (WMD_OPT_GRAPH).
+struct GraphKey {
+  const void* sel;
+  const void* r;
+  const void* dist;
+  int32_t v_r, ld;
+  float lambda;
+  int32_t iters;
+  double tol;
+  bool fused;
+  int64_t fallback, build, targets_gen;
+  const void* bufs[5];  // Mx, Kt, ua, ub, umask: a reallocation invalidates the graph
+  bool operator==(const GraphKey& o) const {
+    for (int i = 0; i < 5; ++i)
+      if (bufs[i] != o.bufs[i]) return false;
+    return sel == o.sel && r == o.r && dist == o.dist && v_r == o.v_r && ld == o.ld && lambda == o.lambda &&
+           iters == o.iters && tol == o.tol && fused == o.fused && fallback == o.fallback &&
+           build == o.build && targets_gen == o.targets_gen;
+  }
+};
+
 }  // namespace
 
 struct wmd_handle {
@@ -123,6 +144,11 @@ struct wmd_handle {
   const float* u_last = nullptr;
   std::vector<int32_t> h_sel;
   std::vector<float> h_r;
+  // captured query graph (WMD_OPT_GRAPH)
+  cudaGraphExec_t graph_exec = nullptr;
+  GraphKey graph_key{};
+  int64_t graph_launches = 0;
+  int64_t targets_gen = 0;   // bumped by every wmd_set_targets (buffers may move)
   // options
   int64_t opt_path = WMD_PATH_AUTO, opt_timing = 0, opt_fallback = 1, opt_graph = 0, opt_build = 0;
   // stats
@@ -388,6 +414,7 @@ void wmd_destroy(wmd_handle* h) {
   DeviceGuard g(h->device);
   if (h->own_stream) cudaStreamSynchronize(h->own_stream);
   if (h->stream && h->stream != h->own_stream) cudaStreamSynchronize(h->stream);
+  if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
   for (auto& pe : h->events)
     for (auto& e : pe.ev) cudaEventDestroy(e);
   if (h->batch_stage) cudaFreeHost(h->batch_stage);
@@ -502,6 +529,7 @@ wmd_status wmd_set_targets(wmd_handle* h, const int64_t* col_ptr, const int32_t*
   h->max_doc_nnz = mx;
   h->len_prefix.swap(len_prefix);
   h->has_targets = true;
+  ++h->targets_gen;
   return WMD_OK;
 }
 
@@ -509,11 +537,8 @@ wmd_status wmd_set_targets(wmd_handle* h, const int64_t* col_ptr, const int32_t*
 
 namespace {
 
-// Enqueue one validated query whose sorted rows sel (device, v_r ids) and r (device, zero padded
-// to WMD_MAX_VR) are already on the device: a2 build, a4/a5 (fused or per iteration), a6.
-// dist: device, N floats. Asynchronous on the handle's stream.
-wmd_status enqueue_query(wmd_handle* h, const int32_t* d_sel, const float* d_r, int32_t v_r,
-                         float lambda, int32_t iters, float* dist) {
+// Path decision and buffer allocation for one query (never inside a graph capture).
+wmd_status prepare_query(wmd_handle* h, int32_t v_r, bool* fused_out, int32_t* ld_out) {
   const int64_t N = h->N;
   // fused path: ld = v_r rounded up to a power of two (the 2-D lane tiling); per-iteration
   // path: v_r rounded up to 8
@@ -531,42 +556,40 @@ wmd_status enqueue_query(wmd_handle* h, const int32_t* d_sel, const float* d_r, 
     CK(h, h->ub.ensure((size_t)N * ld));
     CK(h, h->umask.ensure((size_t)N * ((ld + 31) / 32)));
   }
+  *fused_out = fused;
+  *ld_out = ld;
+  return WMD_OK;
+}
+
+// The stream work of one prepared query (capturable into a CUDA graph): a2 build, a4/a5
+// (fused or per iteration), a6. Returns the number of kernel launches in *launches.
+wmd_status record_query(wmd_handle* h, const int32_t* d_sel, const float* d_r, int32_t v_r,
+                        float lambda, int32_t iters, float* dist, bool fused, int32_t ld,
+                        PhaseEvents* pe, int64_t* launches_out) {
+  const int64_t N = h->N;
   cudaStream_t st = h->stream;
   CK(h, cudaMemsetAsync(h->flags.p, 0, N, st));
   CK(h, cudaMemsetAsync(h->counters.p, 0, sizeof(int32_t), st));  // flagged-list length
-
-  PhaseEvents* pe = nullptr;
-  if (h->opt_timing) {
-    PhaseEvents e{};
-    for (auto& x : e.ev) CK(h, cudaEventCreate(&x));
-    h->events.push_back(e);
-    pe = &h->events.back();
-    CK(h, cudaEventRecord(pe->ev[0], st));
-  }
+  if (pe) CK(h, cudaEventRecord(pe->ev[0], st));
   int64_t launches = 0;
   // a2: M (+ m), and K~ for the per-iteration path
   wmd::launch_build_ktilde(h->E.p, h->V, h->dp, d_sel, v_r, ld, lambda, fused ? nullptr : h->Kt.p,
                            h->Mx.p, h->colmin.p, h->opt_build == 0, st);
-  h->kt_valid = !fused;
   ++launches;
   if (pe) CK(h, cudaEventRecord(pe->ev[1], st));
-
   const float tol = h->tol >= 0.0 ? (float)h->tol : -1.f;
   if (fused) {
     wmd::launch_sinkhorn_fused(h->sdoc.p, h->ent.p, N, h->len_prefix.data(),
                                h->max_doc_nnz, h->Mx.p, ld, v_r, d_r, lambda, iters, tol, h->iters_doc.p,
                                dist, h->flags.p, h->flagged.p, h->counters.p, st);
-    const int64_t nl = wmd::fused_launch_count(h->len_prefix.data(), h->max_doc_nnz, N);
-    launches += nl;
-    h->st.iter_launches += nl;
+    launches += wmd::fused_launch_count(h->len_prefix.data(), h->max_doc_nnz, N);
     if (pe) { CK(h, cudaEventRecord(pe->ev[2], st)); CK(h, cudaEventRecord(pe->ev[3], st)); }
-    h->u_valid = false;
-    h->path_used = WMD_PATH_FUSED;
   } else {
     // a4: iters fused SDDMM_SpMM launches, u ping-pong
     const float* u_in = nullptr;
     float* bufs[2] = {h->ua.p, h->ub.p};
     wmd::launch_fill_i32(h->iters_doc.p, N, iters, st);
+    ++launches;
     if (tol >= 0.f) CK(h, cudaMemsetAsync(h->conv.p, 0, N, st));
     for (int32_t t = 0; t < iters; ++t) {
       float* u_out = bufs[t & 1];
@@ -576,16 +599,12 @@ wmd_status enqueue_query(wmd_handle* h, const int32_t* d_sel, const float* d_r, 
       u_in = u_out;
     }
     launches += iters;
-    h->st.iter_launches += iters;
     if (pe) CK(h, cudaEventRecord(pe->ev[2], st));
     // a5
     wmd::launch_final_wmd(h->order.p, h->doc_ptr.p, h->ent.p, N, h->Kt.p, h->Mx.p, ld, v_r, d_r, u_in,
                           h->umask.p, dist, h->flags.p, h->flagged.p, h->counters.p, st);
     ++launches;
     if (pe) CK(h, cudaEventRecord(pe->ev[3], st));
-    h->u_valid = u_in != nullptr;
-    h->u_last = u_in;
-    h->path_used = WMD_PATH_PER_ITER;
   }
   // a6: FP64 re-run of flagged documents (device-side list; zero-cost when empty)
   if (h->opt_fallback) {
@@ -597,6 +616,65 @@ wmd_status enqueue_query(wmd_handle* h, const int32_t* d_sel, const float* d_r, 
   }
   if (pe) CK(h, cudaEventRecord(pe->ev[4], st));
   CK(h, cudaGetLastError());
+  *launches_out = launches;
+  return WMD_OK;
+}
+
+// Enqueue one validated query whose sorted rows sel (device, v_r ids) and r (device, zero padded
+// to WMD_MAX_VR) are already on the device. dist: device, N floats. Asynchronous on the handle's
+// stream. With WMD_OPT_GRAPH (and no timing) the stream work is captured once per distinct
+// (rows, output, lambda, iters, tolerance, path, options) and replayed as a CUDA graph.
+wmd_status enqueue_query(wmd_handle* h, const int32_t* d_sel, const float* d_r, int32_t v_r,
+                         float lambda, int32_t iters, float* dist) {
+  bool fused = false;
+  int32_t ld = 0;
+  wmd_status s = prepare_query(h, v_r, &fused, &ld);
+  if (s != WMD_OK) return s;
+  int64_t launches = 0;
+  if (h->opt_graph && !h->opt_timing) {
+    const GraphKey key{d_sel, d_r, dist, v_r, ld, lambda, iters, h->tol, fused, h->opt_fallback, h->opt_build,
+                       h->targets_gen, {h->Mx.p, h->Kt.p, h->ua.p, h->ub.p, h->umask.p}};
+    if (!(h->graph_exec && h->graph_key == key)) {
+      if (h->graph_exec) {  // re-capture: the old executable may still be in flight
+        CK(h, cudaStreamSynchronize(h->stream));
+        cudaGraphExecDestroy(h->graph_exec);
+      }
+      h->graph_exec = nullptr;
+      // capture on the handle's own stream (the caller's may be the uncapturable legacy
+      // default stream); the graph is then launched on the caller's stream
+      cudaStream_t user = h->stream;
+      h->stream = h->own_stream;
+      CK(h, cudaStreamBeginCapture(h->own_stream, cudaStreamCaptureModeRelaxed));
+      s = record_query(h, d_sel, d_r, v_r, lambda, iters, dist, fused, ld, nullptr, &launches);
+      cudaGraph_t g = nullptr;
+      const cudaError_t e = cudaStreamEndCapture(h->own_stream, &g);
+      h->stream = user;
+      if (s != WMD_OK) { if (g) cudaGraphDestroy(g); return s; }
+      if (e != cudaSuccess) return cuda_fail(h, e, "cudaStreamEndCapture");
+      const cudaError_t e2 = cudaGraphInstantiate(&h->graph_exec, g, 0);
+      cudaGraphDestroy(g);
+      if (e2 != cudaSuccess) { h->graph_exec = nullptr; return cuda_fail(h, e2, "cudaGraphInstantiate"); }
+      h->graph_key = key;
+      h->graph_launches = launches;
+    }
+    CK(h, cudaGraphLaunch(h->graph_exec, h->stream));
+    launches = h->graph_launches;
+  } else {
+    PhaseEvents* pe = nullptr;
+    if (h->opt_timing) {
+      PhaseEvents e{};
+      for (auto& x : e.ev) CK(h, cudaEventCreate(&x));
+      h->events.push_back(e);
+      pe = &h->events.back();
+    }
+    s = record_query(h, d_sel, d_r, v_r, lambda, iters, dist, fused, ld, pe, &launches);
+    if (s != WMD_OK) return s;
+  }
+  h->kt_valid = !fused;
+  h->u_valid = !fused && iters > 0;
+  h->u_last = (!fused && iters > 0) ? ((iters - 1) & 1 ? h->ub.p : h->ua.p) : nullptr;
+  h->path_used = fused ? WMD_PATH_FUSED : WMD_PATH_PER_ITER;
+  h->st.iter_launches += fused ? wmd::fused_launch_count(h->len_prefix.data(), h->max_doc_nnz, h->N) : iters;
   h->v_r = v_r;
   h->ld = ld;
   h->last_sel = d_sel;

@@ -630,3 +630,32 @@ def test_while_x_changes_per_document(W, path):
     assert_parity(d, o, f"while-x-changes path {path}")
     assert np.abs(its - o_its).max() <= 1
     assert np.mean(its == o_its) >= 0.9
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_graph_replay_equals_direct_launches(W, path):
+    """WMD_OPT_GRAPH: the captured query graph replays bit-identically, re-reads the uploaded
+    rows on every replay (different queries of the same width reuse it), and is re-captured
+    when lambda or the iteration count changes."""
+    wl = synth.make_workload("tiny", n_queries=3)
+    qs = [(q, w) for q, w in wl.queries]
+    qs.append((qs[0][0][::-1].copy(), qs[0][1][::-1].copy()))  # same words, other order
+    runs = {}
+    for graph in (0, 1):
+        h = W.wmd_create(wl.E)
+        try:
+            W.wmd_set_option(h, W.WMD_OPT_PATH, path)
+            W.wmd_set_option(h, W.WMD_OPT_GRAPH, graph)
+            W.wmd_set_targets(h, wl.col_ptr, wl.row_idx, wl.val)
+            out = []
+            for lam, iters in ((10.0, 15), (10.0, 15), (5.0, 15), (5.0, 3)):
+                for q, w in qs:
+                    d = np.empty(wl.N, np.float32)
+                    W.wmd_query(h, q, w, lam, iters, d)
+                    out.append(d)
+            W.wmd_sync(h)
+            runs[graph] = np.stack(out)
+        finally:
+            W.wmd_destroy(h)
+    assert np.array_equal(runs[0], runs[1])
+    assert not np.array_equal(runs[1][0], runs[1][1])
