@@ -276,6 +276,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--graph", action="store_true", help="replay each query as a CUDA graph (WMD_OPT_GRAPH)")
+    ap.add_argument("--no-shard-build", action="store_true",
+                    help="N > 1: every rank builds the whole distance table (default: vocabulary rows "
+                         "split over the ranks + NCCL all-gather of the table)")
     args = ap.parse_args()
 
     wl = synth.make_workload(args.config)
@@ -307,7 +310,7 @@ def main():
     path = {"auto": wmd.WMD_PATH_AUTO, "iter": wmd.WMD_PATH_PER_ITER, "fused": wmd.WMD_PATH_FUSED}[args.path]
     E = torch.from_numpy(wl.E).cuda()
     eng = ShardedEngine(E, wl.col_ptr, wl.row_idx, wl.val, rank, world, local_rank, path=path,
-                        timing=not args.graph)
+                        timing=not args.graph, shard_build=not args.no_shard_build)
     h = eng.engine.h
     if args.graph:
         wmd.wmd_set_option(h, wmd.WMD_OPT_GRAPH, 1)
@@ -424,7 +427,9 @@ def main():
             "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded Zipf bag-of-words, N(0,1) embeddings; BASELINE.json config)",
-            "config": config_dict(cfg, wl, args, path=args.path, graph=bool(args.graph)),
+            "config": config_dict(cfg, wl, args, path=args.path, graph=bool(args.graph),
+                                  build=("tensor-core 3xTF32, vocabulary rows sharded + NCCL table all-gather"
+                                         if world > 1 and not args.no_shard_build else "tensor-core 3xTF32")),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(v_r * 8),
                     "d2h_bytes_per_step": int(wl.N * 4)},
             "gpu_launches": int(st["kernel_launches"]) if st else 0,

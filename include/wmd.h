@@ -160,6 +160,27 @@ WMD_API wmd_status wmd_query_batch(wmd_handle* h, const int32_t* query_ids, cons
                            const int64_t* q_ptr, int32_t nq, float lambda, int32_t iters,
                            float* out_dist);
 
+/* Two-phase query, for a build sharded across ranks (SURVEY.md §8f NEXT-4, §8e Amdahl term B):
+ * wmd_query_begin validates and uploads the query like wmd_query and builds rows
+ * [row_begin, row_end) of the vocabulary tables only (each rank its share, PAPER.md:259-268's
+ * distance kernel split over vocabulary rows); the tables are allocated with
+ * max(V, table_rows) rows so equal row slices can be all-gathered in place.
+ * wmd_query_tables returns the device tables (valid until the next query on the handle):
+ * Mx (rows of mx_row_floats floats: M, then m_k at column mx_row_floats - 4) and, on the
+ * per-iteration path only, K~ (rows of kt_row_floats floats; NULL / 0 on the fused path).
+ * The caller completes every row [0, V) of both (e.g. torch.distributed.all_gather_into_tensor
+ * over NCCL: the library itself never communicates), on the handle's stream order, then
+ * wmd_query_finish runs the Sinkhorn iterations, final step and FP64 fallback into out_dist
+ * (as in wmd_query). wmd_query(...) == begin(rows [0, V)) + finish.
+ * Errors: as wmd_query; INVALID_ARGUMENT for a bad row range; STATE for finish/tables without
+ * a begun query. */
+WMD_API wmd_status wmd_query_begin(wmd_handle* h, const int32_t* query_ids, const float* query_weights,
+                           int32_t n, float lambda, int32_t iters, int64_t row_begin, int64_t row_end,
+                           int64_t table_rows);
+WMD_API wmd_status wmd_query_tables(wmd_handle* h, float** mx, int32_t* mx_row_floats, float** kt,
+                            int32_t* kt_row_floats);
+WMD_API wmd_status wmd_query_finish(wmd_handle* h, float* out_dist);
+
 /* Wait for the handle's stream; return a latched deferred status (then clear it). */
 WMD_API wmd_status wmd_sync(wmd_handle* h);
 

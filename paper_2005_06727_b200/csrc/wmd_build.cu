@@ -41,14 +41,13 @@ __device__ __forceinline__ void cp16(float* dst, const float* src, bool valid) {
 }
 
 __global__ void __launch_bounds__(kThreads, 2) build_mx_kernel(
-    const float* __restrict__ E, int64_t V, int dp, const int32_t* __restrict__ sel, int v_r,
-    int ld, float lambda, float* __restrict__ Kt, float* __restrict__ Mx,
-    float* __restrict__ colmin) {
+    const float* __restrict__ E, int64_t row0, int64_t V, int dp, const int32_t* __restrict__ sel,
+    int v_r, int ld, float lambda, float* __restrict__ Kt, float* __restrict__ Mx) {
   extern __shared__ __align__(16) float smem[];
   float* stage[2] = {smem, smem + kStageFloats};
   __shared__ float cmin[BW];
   const int tid = threadIdx.x, tw = tid & 31, ti = tid >> 5;
-  const int64_t k0 = (int64_t)blockIdx.x * BW;
+  const int64_t k0 = row0 + (int64_t)blockIdx.x * BW;  // rows [row0, V) of this launch
   const int nchunk = dp / BD;
   const int ldx = ld + 4;
   for (int w = tid; w < BW; w += kThreads) cmin[w] = FLT_MAX;
@@ -134,7 +133,6 @@ __global__ void __launch_bounds__(kThreads, 2) build_mx_kernel(
       }
       // row complete: zero padding, m_k, and K~ (reading back earlier passes' M from Mx)
       for (int x = v_r + lane; x < ldx; x += 32) Mx[k * ldx + x] = x == ld ? mn : 0.f;
-      if (lane == 0) colmin[k] = mn;
       if (Kt) {
         for (int x = lane; x < ld; x += 32) {
           float kt = 0.f;
@@ -218,9 +216,8 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 
 template <int NP>
 __global__ void __launch_bounds__(128, NP <= 32 ? 2 : 1) build_mx_tc_kernel(
-    const float* __restrict__ E, int64_t V, int dp, const int32_t* __restrict__ sel, int v_r,
-    int ld, float lambda, float* __restrict__ Kt, float* __restrict__ Mx,
-    float* __restrict__ colmin) {
+    const float* __restrict__ E, int64_t row0, int64_t V, int dp, const int32_t* __restrict__ sel,
+    int v_r, int ld, float lambda, float* __restrict__ Kt, float* __restrict__ Mx) {
   constexpr int A_BYTES = TC_M * TC_K * 4, B_BYTES = NP * TC_K * 4;
   constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;          // raw (= hi) and lo, A and B
   constexpr uint32_t TMEM_COLS = NP <= 32 ? 32 : (NP <= 64 ? 64 : 128);
@@ -233,7 +230,7 @@ __global__ void __launch_bounds__(128, NP <= 32 ? 2 : 1) build_mx_tc_kernel(
   __shared__ float qn[NP];
   __shared__ int32_t qsel[NP];
   const int tid = threadIdx.x, warp = tid >> 5;
-  const int64_t k0 = (int64_t)blockIdx.x * TC_M;
+  const int64_t k0 = row0 + (int64_t)blockIdx.x * TC_M;  // rows [row0, V) of this launch
   const int nchunk = dp / TC_K;
   const int ldx = ld + 4;
   if (tid < NP) qsel[tid] = tid < v_r ? sel[tid] : -1;
@@ -383,7 +380,6 @@ __global__ void __launch_bounds__(128, NP <= 32 ? 2 : 1) build_mx_tc_kernel(
     for (int i = 0; i < NP; ++i)
       if (i < ldx) row[i] = i < v_r ? Mrow[i] : (i == ld ? mn : 0.f);
     for (int x = NP; x < ldx; ++x) row[x] = x == ld ? mn : 0.f;
-    colmin[k] = mn;
   }
   __syncthreads();
   // the block's rows are contiguous in Mx (and K~): coalesced copies out of shared memory
@@ -408,27 +404,28 @@ __global__ void __launch_bounds__(128, NP <= 32 ? 2 : 1) build_mx_tc_kernel(
 
 }  // namespace
 
-void launch_build_ktilde(const float* E, int64_t V, int dp, const int32_t* sel, int v_r, int ld,
-                         float lambda, float* Kt, float* Mx, float* colmin, bool use_tc, cudaStream_t st) {
-  constexpr size_t smem = sizeof(float) * 2 * kStageFloats;
-  static_assert(BW * kMsPitch <= 2 * kStageFloats, "M tile must fit in the staging buffers");
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(build_mx_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+void launch_build_ktilde(const float* E, int64_t row0, int64_t row1, int dp, const int32_t* sel, int v_r,
+                         int ld, float lambda, float* Kt, float* Mx, bool use_tc, cudaStream_t st) {
+  if (row1 <= row0) return;
   if (!use_tc) {
-    const int64_t grid = (V + BW - 1) / BW;
-    build_mx_kernel<<<(unsigned)grid, kThreads, smem, st>>>(E, V, dp, sel, v_r, ld, lambda, Kt, Mx, colmin);
+    constexpr size_t smem = sizeof(float) * 2 * kStageFloats;
+    static_assert(BW * kMsPitch <= 2 * kStageFloats, "M tile must fit in the staging buffers");
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(build_mx_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    const int64_t grid = (row1 - row0 + BW - 1) / BW;
+    build_mx_kernel<<<(unsigned)grid, kThreads, smem, st>>>(E, row0, row1, dp, sel, v_r, ld, lambda, Kt, Mx);
     return;
   }
-  const unsigned grid = (unsigned)((V + TC_M - 1) / TC_M);
+  const unsigned grid = (unsigned)((row1 - row0 + TC_M - 1) / TC_M);
 #define TC_(NP)                                                                                       \
   {                                                                                                   \
-    constexpr size_t sm = TC_NS * (2 * TC_M * TC_K * 4 + 2 * NP * TC_K * 4);                              \
+    constexpr size_t sm = TC_NS * (2 * TC_M * TC_K * 4 + 2 * NP * TC_K * 4);                         \
     static bool a = false;                                                                            \
     if (!a) { cudaFuncSetAttribute(build_mx_tc_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); a = true; } \
-    build_mx_tc_kernel<NP><<<grid, 128, sm, st>>>(E, V, dp, sel, v_r, ld, lambda, Kt, Mx, colmin);   \
+    build_mx_tc_kernel<NP><<<grid, 128, sm, st>>>(E, row0, row1, dp, sel, v_r, ld, lambda, Kt, Mx);  \
   }
   if (v_r <= 32) TC_(32)
   else if (v_r <= 64) TC_(64)

@@ -115,7 +115,6 @@ struct wmd_handle {
   DevBuf<float> Kt;          // V * ld: K~ (FP32, vocab-major; per-iteration path only)
   DevBuf<float> Mx;          // V * (ld + 4): M rows + m_k (FP32, vocab-major)
   bool kt_valid = false;     // Kt holds the last query's K~
-  DevBuf<float> colmin;      // V
   DevBuf<float> ua, ub;      // N * ld
   DevBuf<uint32_t> umask;    // N * ceil(ld/32): rows with an underflowed K~ entry, per doc
   DevBuf<float> dist_tmp;    // N (host-output queries)
@@ -144,6 +143,13 @@ struct wmd_handle {
   const float* u_last = nullptr;
   std::vector<int32_t> h_sel;
   std::vector<float> h_r;
+  // two-phase query (wmd_query_begin / wmd_query_finish)
+  struct {
+    bool active = false, fused = false;
+    int32_t v_r = 0, ld = 0, iters = 0;
+    float lambda = 0.f;
+    PhaseEvents* pe = nullptr;
+  } pq;
   // captured query graph (WMD_OPT_GRAPH)
   cudaGraphExec_t graph_exec = nullptr;
   GraphKey graph_key{};
@@ -397,7 +403,7 @@ wmd_status wmd_create(const float* vocab_emb, int64_t V, int32_t d, int32_t devi
       return bail(WMD_ERR_CUDA);
   }
   if (h->sel.ensure(WMD_MAX_VR) != cudaSuccess || h->rpad.ensure(WMD_MAX_VR) != cudaSuccess ||
-      h->colmin.ensure((size_t)V) != cudaSuccess || h->counters.ensure(4) != cudaSuccess)
+      h->counters.ensure(4) != cudaSuccess)
     return bail(WMD_ERR_OUT_OF_MEMORY);
   if (cudaEventCreateWithFlags(&h->batch_ev, cudaEventDisableTiming) != cudaSuccess) return bail(WMD_ERR_CUDA);
   for (int s = 0; s < 2; ++s) {
@@ -425,7 +431,7 @@ void wmd_destroy(wmd_handle* h) {
     if (h->stage_ev[s]) cudaEventDestroy(h->stage_ev[s]);
   }
   h->E.release(); h->doc_ptr.release(); h->order.release(); h->sdoc.release(); h->ent.release(); h->sel.release(); h->rpad.release();
-  h->Kt.release(); h->Mx.release(); h->colmin.release(); h->ua.release(); h->ub.release(); h->umask.release();
+  h->Kt.release(); h->Mx.release(); h->ua.release(); h->ub.release(); h->umask.release();
   h->dist_tmp.release(); h->flags.release(); h->flagged.release(); h->counters.release();
   h->iters_doc.release(); h->conv.release();
   h->fb_scratch.release();
@@ -537,8 +543,9 @@ wmd_status wmd_set_targets(wmd_handle* h, const int64_t* col_ptr, const int32_t*
 
 namespace {
 
-// Path decision and buffer allocation for one query (never inside a graph capture).
-wmd_status prepare_query(wmd_handle* h, int32_t v_r, bool* fused_out, int32_t* ld_out) {
+// Path decision and buffer allocation for one query (never inside a graph capture). The tables
+// get max(V, table_rows) rows (a sharded build all-gathers equal row slices, which may pad).
+wmd_status prepare_query(wmd_handle* h, int32_t v_r, int64_t table_rows, bool* fused_out, int32_t* ld_out) {
   const int64_t N = h->N;
   // fused path: ld = v_r rounded up to a power of two (the 2-D lane tiling); per-iteration
   // path: v_r rounded up to 8
@@ -548,9 +555,10 @@ wmd_status prepare_query(wmd_handle* h, int32_t v_r, bool* fused_out, int32_t* l
     return fail(h, WMD_ERR_INVALID_ARGUMENT, "fused path does not support v_r=%d, max doc nnz=%lld", v_r,
                 (long long)h->max_doc_nnz);
   const int32_t ld = fused ? wmd::fused_ld(v_r) : round_up8(v_r);
+  const int64_t rows = std::max(h->V, table_rows);
   // +128 floats: the pass kernels gather unpredicated float4s up to 4*32 floats past a row
-  if (!fused) CK(h, h->Kt.ensure((size_t)h->V * ld + 128));
-  CK(h, h->Mx.ensure((size_t)h->V * (ld + 4) + 128));
+  if (!fused) CK(h, h->Kt.ensure((size_t)rows * ld + 128));
+  CK(h, h->Mx.ensure((size_t)rows * (ld + 4) + 128));
   if (!fused) {
     CK(h, h->ua.ensure((size_t)N * ld));
     CK(h, h->ub.ensure((size_t)N * ld));
@@ -561,22 +569,27 @@ wmd_status prepare_query(wmd_handle* h, int32_t v_r, bool* fused_out, int32_t* l
   return WMD_OK;
 }
 
-// The stream work of one prepared query (capturable into a CUDA graph): a2 build, a4/a5
-// (fused or per iteration), a6. Returns the number of kernel launches in *launches.
-wmd_status record_query(wmd_handle* h, const int32_t* d_sel, const float* d_r, int32_t v_r,
-                        float lambda, int32_t iters, float* dist, bool fused, int32_t ld,
-                        PhaseEvents* pe, int64_t* launches_out) {
+// a2 for vocabulary rows [row0, row1) (capturable stream work).
+wmd_status record_build(wmd_handle* h, const int32_t* d_sel, int32_t v_r, float lambda, int64_t row0,
+                        int64_t row1, bool fused, int32_t ld, PhaseEvents* pe) {
+  cudaStream_t st = h->stream;
+  if (pe) CK(h, cudaEventRecord(pe->ev[0], st));
+  // M (+ m), and K~ for the per-iteration path
+  wmd::launch_build_ktilde(h->E.p, row0, row1, h->dp, d_sel, v_r, ld, lambda, fused ? nullptr : h->Kt.p,
+                           h->Mx.p, h->opt_build == 0, st);
+  if (pe) CK(h, cudaEventRecord(pe->ev[1], st));
+  CK(h, cudaGetLastError());
+  return WMD_OK;
+}
+
+// a3-a6 on complete tables (capturable stream work). *launches_out: kernel launches.
+wmd_status record_solve(wmd_handle* h, const float* d_r, int32_t v_r, float lambda, int32_t iters,
+                        float* dist, bool fused, int32_t ld, PhaseEvents* pe, int64_t* launches_out) {
   const int64_t N = h->N;
   cudaStream_t st = h->stream;
   CK(h, cudaMemsetAsync(h->flags.p, 0, N, st));
   CK(h, cudaMemsetAsync(h->counters.p, 0, sizeof(int32_t), st));  // flagged-list length
-  if (pe) CK(h, cudaEventRecord(pe->ev[0], st));
   int64_t launches = 0;
-  // a2: M (+ m), and K~ for the per-iteration path
-  wmd::launch_build_ktilde(h->E.p, h->V, h->dp, d_sel, v_r, ld, lambda, fused ? nullptr : h->Kt.p,
-                           h->Mx.p, h->colmin.p, h->opt_build == 0, st);
-  ++launches;
-  if (pe) CK(h, cudaEventRecord(pe->ev[1], st));
   const float tol = h->tol >= 0.0 ? (float)h->tol : -1.f;
   if (fused) {
     wmd::launch_sinkhorn_fused(h->sdoc.p, h->ent.p, N, h->len_prefix.data(),
@@ -608,8 +621,7 @@ wmd_status record_query(wmd_handle* h, const int32_t* d_sel, const float* d_r, i
   }
   // a6: FP64 re-run of flagged documents (device-side list; zero-cost when empty)
   if (h->opt_fallback) {
-    wmd::launch_fallback_fp64(h->Mx.p, h->colmin.p, ld, d_r, v_r, (double)lambda, iters, tol, h->iters_doc.p,
-                              h->doc_ptr.p,
+    wmd::launch_fallback_fp64(h->Mx.p, ld, d_r, v_r, (double)lambda, iters, tol, h->iters_doc.p, h->doc_ptr.p,
                               h->ent.p, h->flagged.p, h->counters.p, h->fb_scratch.p, h->max_doc_nnz, dist,
                               h->flags.p, h->counters.p + 1, h->counters.p + 2, st);
     ++launches;
@@ -620,6 +632,34 @@ wmd_status record_query(wmd_handle* h, const int32_t* d_sel, const float* d_r, i
   return WMD_OK;
 }
 
+PhaseEvents* new_phase_events(wmd_handle* h) {
+  if (!h->opt_timing) return nullptr;
+  PhaseEvents e{};
+  for (auto& x : e.ev)
+    if (cudaEventCreate(&x) != cudaSuccess) return nullptr;
+  h->events.push_back(e);
+  return &h->events.back();
+}
+
+// Host bookkeeping after a query's solve was enqueued.
+void note_query(wmd_handle* h, const int32_t* d_sel, const float* d_r, int32_t v_r, int32_t iters, bool fused,
+                int32_t ld, int64_t launches) {
+  h->kt_valid = !fused;
+  h->u_valid = !fused && iters > 0;
+  h->u_last = (!fused && iters > 0) ? ((iters - 1) & 1 ? h->ub.p : h->ua.p) : nullptr;
+  h->path_used = fused ? WMD_PATH_FUSED : WMD_PATH_PER_ITER;
+  h->st.iter_launches += fused ? wmd::fused_launch_count(h->len_prefix.data(), h->max_doc_nnz, h->N) : iters;
+  h->v_r = v_r;
+  h->ld = ld;
+  h->last_sel = d_sel;
+  h->last_r = d_r;
+  h->st.queries += 1;
+  h->st.kernel_launches += launches;
+  h->st.last_v_r = v_r;
+  h->st.last_ld = ld;
+  h->st.last_path = h->path_used;
+}
+
 // Enqueue one validated query whose sorted rows sel (device, v_r ids) and r (device, zero padded
 // to WMD_MAX_VR) are already on the device. dist: device, N floats. Asynchronous on the handle's
 // stream. With WMD_OPT_GRAPH (and no timing) the stream work is captured once per distinct
@@ -628,7 +668,7 @@ wmd_status enqueue_query(wmd_handle* h, const int32_t* d_sel, const float* d_r, 
                          float lambda, int32_t iters, float* dist) {
   bool fused = false;
   int32_t ld = 0;
-  wmd_status s = prepare_query(h, v_r, &fused, &ld);
+  wmd_status s = prepare_query(h, v_r, h->V, &fused, &ld);
   if (s != WMD_OK) return s;
   int64_t launches = 0;
   if (h->opt_graph && !h->opt_timing) {
@@ -645,7 +685,8 @@ wmd_status enqueue_query(wmd_handle* h, const int32_t* d_sel, const float* d_r, 
       cudaStream_t user = h->stream;
       h->stream = h->own_stream;
       CK(h, cudaStreamBeginCapture(h->own_stream, cudaStreamCaptureModeRelaxed));
-      s = record_query(h, d_sel, d_r, v_r, lambda, iters, dist, fused, ld, nullptr, &launches);
+      s = record_build(h, d_sel, v_r, lambda, 0, h->V, fused, ld, nullptr);
+      if (s == WMD_OK) s = record_solve(h, d_r, v_r, lambda, iters, dist, fused, ld, nullptr, &launches);
       cudaGraph_t g = nullptr;
       const cudaError_t e = cudaStreamEndCapture(h->own_stream, &g);
       h->stream = user;
@@ -655,35 +696,19 @@ wmd_status enqueue_query(wmd_handle* h, const int32_t* d_sel, const float* d_r, 
       cudaGraphDestroy(g);
       if (e2 != cudaSuccess) { h->graph_exec = nullptr; return cuda_fail(h, e2, "cudaGraphInstantiate"); }
       h->graph_key = key;
-      h->graph_launches = launches;
+      h->graph_launches = launches + 1;
     }
     CK(h, cudaGraphLaunch(h->graph_exec, h->stream));
     launches = h->graph_launches;
   } else {
-    PhaseEvents* pe = nullptr;
-    if (h->opt_timing) {
-      PhaseEvents e{};
-      for (auto& x : e.ev) CK(h, cudaEventCreate(&x));
-      h->events.push_back(e);
-      pe = &h->events.back();
-    }
-    s = record_query(h, d_sel, d_r, v_r, lambda, iters, dist, fused, ld, pe, &launches);
+    PhaseEvents* pe = new_phase_events(h);
+    s = record_build(h, d_sel, v_r, lambda, 0, h->V, fused, ld, pe);
     if (s != WMD_OK) return s;
+    s = record_solve(h, d_r, v_r, lambda, iters, dist, fused, ld, pe, &launches);
+    if (s != WMD_OK) return s;
+    ++launches;  // the build
   }
-  h->kt_valid = !fused;
-  h->u_valid = !fused && iters > 0;
-  h->u_last = (!fused && iters > 0) ? ((iters - 1) & 1 ? h->ub.p : h->ua.p) : nullptr;
-  h->path_used = fused ? WMD_PATH_FUSED : WMD_PATH_PER_ITER;
-  h->st.iter_launches += fused ? wmd::fused_launch_count(h->len_prefix.data(), h->max_doc_nnz, h->N) : iters;
-  h->v_r = v_r;
-  h->ld = ld;
-  h->last_sel = d_sel;
-  h->last_r = d_r;
-  h->st.queries += 1;
-  h->st.kernel_launches += launches;
-  h->st.last_v_r = v_r;
-  h->st.last_ld = ld;
-  h->st.last_path = h->path_used;
+  note_query(h, d_sel, d_r, v_r, iters, fused, ld, launches);
   return WMD_OK;
 }
 
@@ -796,6 +821,82 @@ wmd_status wmd_query_batch(wmd_handle* h, const int32_t* query_ids, const float*
   return WMD_OK;
 }
 
+wmd_status wmd_query_begin(wmd_handle* h, const int32_t* query_ids, const float* query_weights, int32_t n,
+                           float lambda, int32_t iters, int64_t row_begin, int64_t row_end, int64_t table_rows) {
+  if (!h) return WMD_ERR_INVALID_ARGUMENT;
+  h->err.clear();
+  h->pq.active = false;
+  wmd_status s = check_query_args(h, (const void*)1, lambda, iters);
+  if (s != WMD_OK) return s;
+  if (row_begin < 0 || row_end < row_begin || row_end > h->V || table_rows < 0)
+    return fail(h, WMD_ERR_INVALID_ARGUMENT, "row range [%lld, %lld) outside [0, V)", (long long)row_begin,
+                (long long)row_end);
+  int64_t bad = -1;
+  std::string msg;
+  s = validate_query(query_ids, query_weights, n, h->V, &bad, &msg, &h->h_sel, &h->h_r);
+  if (s != WMD_OK) return fail(h, s, "%s", msg.c_str());
+  DeviceGuard g(h->device);
+  if (!g.ok) return fail(h, WMD_ERR_CUDA, "cudaSetDevice failed");
+  cudaStream_t st = h->stream;
+  const int slot = h->stage_slot;
+  h->stage_slot ^= 1;
+  CK(h, cudaEventSynchronize(h->stage_ev[slot]));
+  int32_t* ssel = (int32_t*)h->stage[slot];
+  float* sr = (float*)((char*)h->stage[slot] + WMD_MAX_VR * 4);
+  std::memset(h->stage[slot], 0, WMD_MAX_VR * 8);
+  for (int32_t i = 0; i < n; ++i) { ssel[i] = h->h_sel[i]; sr[i] = h->h_r[i]; }
+  CK(h, cudaMemcpyAsync(h->sel.p, ssel, WMD_MAX_VR * 4, cudaMemcpyHostToDevice, st));
+  CK(h, cudaMemcpyAsync(h->rpad.p, sr, WMD_MAX_VR * 4, cudaMemcpyHostToDevice, st));
+  CK(h, cudaEventRecord(h->stage_ev[slot], st));
+  bool fused = false;
+  int32_t ld = 0;
+  s = prepare_query(h, n, table_rows, &fused, &ld);
+  if (s != WMD_OK) return s;
+  PhaseEvents* pe = new_phase_events(h);
+  s = record_build(h, h->sel.p, n, lambda, row_begin, row_end, fused, ld, pe);
+  if (s != WMD_OK) return s;
+  h->pq.active = true;
+  h->pq.fused = fused;
+  h->pq.v_r = n;
+  h->pq.ld = ld;
+  h->pq.iters = iters;
+  h->pq.lambda = lambda;
+  h->pq.pe = pe;
+  return WMD_OK;
+}
+
+wmd_status wmd_query_tables(wmd_handle* h, float** mx, int32_t* mx_row_floats, float** kt,
+                            int32_t* kt_row_floats) {
+  if (!h || !mx || !mx_row_floats) return WMD_ERR_INVALID_ARGUMENT;
+  if (!h->pq.active) return fail(h, WMD_ERR_STATE, "no query begun");
+  *mx = h->Mx.p;
+  *mx_row_floats = h->pq.ld + 4;
+  if (kt) *kt = h->pq.fused ? nullptr : h->Kt.p;
+  if (kt_row_floats) *kt_row_floats = h->pq.fused ? 0 : h->pq.ld;
+  return WMD_OK;
+}
+
+wmd_status wmd_query_finish(wmd_handle* h, float* out_dist) {
+  if (!h) return WMD_ERR_INVALID_ARGUMENT;
+  if (!h->pq.active) return fail(h, WMD_ERR_STATE, "wmd_query_finish without wmd_query_begin");
+  if (!out_dist) return fail(h, WMD_ERR_INVALID_ARGUMENT, "out_dist NULL");
+  DeviceGuard g(h->device);
+  if (!g.ok) return fail(h, WMD_ERR_CUDA, "cudaSetDevice failed");
+  h->pq.active = false;
+  const bool dev_out = is_device_ptr(out_dist);
+  float* dist = dev_out ? out_dist : h->dist_tmp.p;
+  int64_t launches = 0;
+  wmd_status s = record_solve(h, h->rpad.p, h->pq.v_r, h->pq.lambda, h->pq.iters, dist, h->pq.fused,
+                              h->pq.ld, h->pq.pe, &launches);
+  if (s != WMD_OK) return s;
+  note_query(h, h->sel.p, h->rpad.p, h->pq.v_r, h->pq.iters, h->pq.fused, h->pq.ld, launches + 1);
+  if (!dev_out) {
+    CK(h, cudaMemcpyAsync(out_dist, dist, h->N * sizeof(float), cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+  }
+  return WMD_OK;
+}
+
 wmd_status wmd_sync(wmd_handle* h) {
   if (!h) return WMD_ERR_INVALID_ARGUMENT;
   DeviceGuard g(h->device);
@@ -866,7 +967,8 @@ wmd_status wmd_read_kernel(wmd_handle* h, int64_t k0, int64_t count, float* ktil
   if (ktilde) CK(h, cudaMemcpy(ktilde, h->Kt.p + k0 * row, count * row * 4, cudaMemcpyDeviceToHost));
   if (m && count > 0)
     CK(h, cudaMemcpy2D(m, row * 4, h->Mx.p + k0 * rowx, rowx * 4, row * 4, count, cudaMemcpyDeviceToHost));
-  if (colmin) CK(h, cudaMemcpy(colmin, h->colmin.p + k0, count * 4, cudaMemcpyDeviceToHost));
+  if (colmin && count > 0)  // m_k is column ld of the Mx rows
+    CK(h, cudaMemcpy2D(colmin, 4, h->Mx.p + k0 * rowx + row, rowx * 4, 4, count, cudaMemcpyDeviceToHost));
   return WMD_OK;
 }
 

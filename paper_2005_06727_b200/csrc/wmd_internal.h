@@ -32,9 +32,10 @@ struct QueryDev {
 // --- a2: distance + column-rescaled kernel build -------
 // Mx: V rows of ld + 4 floats [M_k0 .. M_k,ld-1 (zero beyond v_r), m_k = min_i M_ik, 0, 0, 0].
 // Kt (V x ld, K~ = exp(-lambda (M - m))) is written only when non-null (per-iteration path).
-// E: V rows of dp floats (d padded with zeros to a multiple of 32).
-void launch_build_ktilde(const float* E, int64_t V, int dp, const int32_t* sel, int v_r, int ld,
-                         float lambda, float* Kt, float* Mx, float* colmin, bool use_tc, cudaStream_t st);
+// Rows [row0, row1) only (a rank's share of a sharded build); E: rows of dp floats (d padded
+// with zeros to a multiple of 32). use_tc: tensor-core 3xTF32 GEMM form, else SIMT.
+void launch_build_ktilde(const float* E, int64_t row0, int64_t row1, int dp, const int32_t* sel, int v_r,
+                         int ld, float lambda, float* Kt, float* Mx, bool use_tc, cudaStream_t st);
 
 // "While x changes" (NEXT-3): tol < 0 runs the fixed iteration count. Otherwise a
 // document stops after the first x-update with max_i |x_new/x - 1| <= tol (R31);
@@ -77,7 +78,7 @@ int fused_launch_count(const int64_t* len_prefix, int64_t max_len, int64_t N);
 // --- a6: FP64 re-run of flagged documents (no CPU fallback) --------------------------------
 constexpr int kFallbackBlocks = 148;  // 1 per SM (200 KB of shared memory each)
 size_t fallback_scratch_bytes(int64_t max_doc_nnz);
-void launch_fallback_fp64(const float* Mx, const float* colmin, int ld, const float* rpad, int v_r,
+void launch_fallback_fp64(const float* Mx, int ld, const float* rpad, int v_r,
                           double lambda, int iters, float tol, int32_t* iters_doc,
                           const int32_t* doc_ptr, const Entry* ent,
                           const int32_t* flagged_list, const int32_t* flagged_count,

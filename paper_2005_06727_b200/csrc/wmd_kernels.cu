@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(256, FINAL ? 2 : PASS_BLOCKS_PER_SM) sinkhorn_
 constexpr int kFallbackSmem = 200 * 1024;
 
 __global__ void __launch_bounds__(256) fallback_fp64_kernel(
-    const float* __restrict__ Mt, const float* __restrict__ colmin, int ld,
+    const float* __restrict__ Mt, int ld,
     const float* __restrict__ rpad, int v_r, double lambda, int iters, float tol,
     int32_t* __restrict__ iters_doc, const int32_t* __restrict__ doc_ptr, const Entry* __restrict__ ent,
     const int32_t* __restrict__ flagged_list, const int32_t* __restrict__ flagged_count,
@@ -377,7 +377,8 @@ __global__ void __launch_bounds__(256) fallback_fp64_kernel(
     for (int p = tid; p < L * v_r; p += blockDim.x) {  // K = exp(-lambda (M - m)), FP64
       const int e_ = p / v_r, i = p % v_r;
       const int k = ent[b + e_].k;
-      K[(int64_t)e_ * pitch + i] = exp(-lambda * ((double)Mt[(int64_t)k * ldx + i] - (double)colmin[k]));
+      // column minimum m_k sits at Mx row position ld
+      K[(int64_t)e_ * pitch + i] = exp(-lambda * ((double)Mt[(int64_t)k * ldx + i] - (double)Mt[(int64_t)k * ldx + ld]));
     }
     for (int i = tid; i < v_r; i += blockDim.x) u[i] = (double)v_r;  // x0 = 1/v_r
     __syncthreads();
@@ -542,7 +543,7 @@ size_t fallback_scratch_bytes(int64_t max_doc_nnz) {
   return sizeof(double) * (size_t)kFallbackBlocks * (size_t)fallback_block_doubles(max_doc_nnz);
 }
 
-void launch_fallback_fp64(const float* Mt, const float* colmin, int ld, const float* rpad, int v_r,
+void launch_fallback_fp64(const float* Mt, int ld, const float* rpad, int v_r,
                           double lambda, int iters, float tol, int32_t* iters_doc,
                           const int32_t* doc_ptr, const Entry* ent,
                           const int32_t* flagged_list, const int32_t* flagged_count,
@@ -553,7 +554,7 @@ void launch_fallback_fp64(const float* Mt, const float* colmin, int ld, const fl
     cudaFuncSetAttribute(fallback_fp64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFallbackSmem);
     attr = true;
   }
-  fallback_fp64_kernel<<<kFallbackBlocks, 256, kFallbackSmem, st>>>(Mt, colmin, ld, rpad, v_r, lambda, iters, tol,
+  fallback_fp64_kernel<<<kFallbackBlocks, 256, kFallbackSmem, st>>>(Mt, ld, rpad, v_r, lambda, iters, tol,
                                                         iters_doc, doc_ptr,
                                                         ent, flagged_list, flagged_count, scratch,
                                                         max_doc_nnz, dist, flags, breakdown,

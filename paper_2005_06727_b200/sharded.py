@@ -74,12 +74,33 @@ def _compaction_index(bounds, n_max, device):
     return _IDX_CACHE[key]
 
 
+def build_rows(V: int, world: int, rank: int) -> Tuple[int, int, int]:
+    """Sharded distance build: rank g builds vocabulary rows [g R, min(V, (g+1) R)), R = ceil(V/P);
+    returns (row_begin, row_end, R)."""
+    R = -(-V // world)
+    b = min(V, rank * R)
+    return b, min(V, b + R), R
+
+
+def gather_table(table, R: int, width: int, world: int, rank: int, group=None):
+    """In-place all-gather of equal R-row slices of a flat (P R width) table view (NCCL)."""
+    import torch.distributed as dist
+    full = table[: world * R * width]
+    dist.all_gather_into_tensor(full, full[rank * R * width:(rank + 1) * R * width], group=group)
+
+
 class ShardedEngine:
-    """One rank's view: owns a wmd handle over its document shard."""
+    """One rank's view: owns a wmd handle over its document shard. With shard_build the per-query
+    distance build is split over the ranks by vocabulary rows and the tables are all-gathered
+    (NEXT-4; removes the replicated build from the per-rank critical path)."""
 
     def __init__(self, vocab_emb, col_ptr, row_idx, val, rank: int, world: int, device: int,
-                 group=None, path: int = wmd.WMD_PATH_AUTO, timing: bool = False):
+                 group=None, path: int = wmd.WMD_PATH_AUTO, timing: bool = False,
+                 shard_build: bool = False):
         self.rank, self.world, self.group = rank, world, group
+        self.device = device
+        self.shard_build = shard_build and world > 1
+        self.V = int(vocab_emb.shape[0])
         self.bounds = shard_bounds(col_ptr, world)
         self.N = int(np.shape(col_ptr)[0]) - 1
         cp, ri, va = local_shard(col_ptr, row_idx, val, self.bounds, rank)
@@ -89,13 +110,27 @@ class ShardedEngine:
         self.engine = wmd.Engine(vocab_emb, device=device, path=path, timing=timing)
         if self.n_local > 0:
             self.engine.set_targets(cp, ri, va)
+        elif self.shard_build:  # no documents, but this rank still builds and gathers its rows
+            self.engine.set_targets(np.array([0, 1], np.int64), np.array([0], np.int32),
+                                    np.array([1.0], np.float32))
         import torch
         self._local = torch.zeros(max(self.n_local, 1), dtype=torch.float32, device=f"cuda:{device}")
         self._out = torch.empty(self.N, dtype=torch.float32, device=f"cuda:{device}")
 
     def query(self, ids, weights, lam: float, iters: int):
         """Distances of all N documents (global order) on every rank."""
-        if self.n_local > 0:
+        if self.shard_build:
+            # every rank builds its vocabulary rows, the tables are all-gathered, then each rank
+            # solves its documents (ranks without documents still build and gather)
+            h = self.engine.h
+            b, e, R = build_rows(self.V, self.world, self.rank)
+            wmd.wmd_query_begin(h, ids, weights, lam, iters, b, e, table_rows=self.world * R)
+            mx, wm, kt, wk = wmd.wmd_query_tables(h, self.world * R, self.device)
+            gather_table(mx, R, wm, self.world, self.rank, self.group)
+            if kt is not None:
+                gather_table(kt, R, wk, self.world, self.rank, self.group)
+            wmd.wmd_query_finish(h, self._local[: max(self.n_local, 1)])
+        elif self.n_local > 0:
             self.engine.query(ids, weights, lam, iters, out=self._local[: self.n_local])
         if self.world == 1:
             return self._local[: self.n_local]

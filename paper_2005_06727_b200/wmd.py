@@ -39,7 +39,7 @@ WMD_OPT_PATH, WMD_OPT_TIMING, WMD_OPT_FALLBACK, WMD_OPT_GRAPH, WMD_OPT_BUILD = 1
 
 EXPORTED = (
     "wmd_create", "wmd_set_stream", "wmd_set_option", "wmd_set_targets", "wmd_query",
-    "wmd_query_batch", "wmd_sync",
+    "wmd_query_batch", "wmd_query_begin", "wmd_query_tables", "wmd_query_finish", "wmd_sync",
     "wmd_partition", "wmd_validate_csc", "wmd_validate_query", "wmd_get_stats", "wmd_reset_stats",
     "wmd_get_query_rows", "wmd_read_kernel", "wmd_read_scaling", "wmd_read_flags",
     "wmd_set_tolerance", "wmd_read_iterations",
@@ -74,6 +74,9 @@ def _load():
         "wmd_set_targets": [P, P, P, P, I64, I64],
         "wmd_query": [P, P, P, I32, ctypes.c_float, I32, P],
         "wmd_query_batch": [P, P, P, P, I32, ctypes.c_float, I32, P],
+        "wmd_query_begin": [P, P, P, I32, ctypes.c_float, I32, I64, I64, I64],
+        "wmd_query_tables": [P, ctypes.POINTER(P), ctypes.POINTER(I32), ctypes.POINTER(P), ctypes.POINTER(I32)],
+        "wmd_query_finish": [P, P],
         "wmd_sync": [P],
         "wmd_partition": [P, I64, I32, P],
         "wmd_validate_csc": [P, P, P, I64, I64, I64, P],
@@ -204,6 +207,41 @@ def wmd_query_batch(h, queries, lam: float, iters: int, out_dist) -> None:
     pq, k3 = _ptr(qp, np.int64)
     po, k4 = _ptr(out_dist, np.float32)
     _check(lib.wmd_query_batch(h, pi, pw, pq, len(queries), float(lam), int(iters), po), h)
+
+
+def wmd_query_begin(h, query_ids, query_weights, lam: float, iters: int, row_begin: int, row_end: int,
+                    table_rows: int = 0) -> None:
+    """Phase 1 of a two-phase query: upload + build vocabulary rows [row_begin, row_end)."""
+    pi, k1 = _ptr(np.asarray(query_ids), np.int32)
+    pw, k2 = _ptr(np.asarray(query_weights), np.float32)
+    n = int(np.asarray(query_ids).shape[0])
+    _check(lib.wmd_query_begin(h, pi, pw, n, float(lam), int(iters), int(row_begin), int(row_end),
+                               int(table_rows)), h)
+
+
+class _DevArray:
+    """Zero-copy view of library-owned device memory for torch.as_tensor."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False), "version": 3}
+
+
+def wmd_query_tables(h, rows: int, device: int = 0):
+    """Device tables of the begun query as flat torch float32 views of `rows` rows each:
+    (mx, mx_row_floats, kt or None, kt_row_floats)."""
+    import torch
+    mx, kt = ctypes.c_void_p(), ctypes.c_void_p()
+    wm, wk = ctypes.c_int32(), ctypes.c_int32()
+    _check(lib.wmd_query_tables(h, ctypes.byref(mx), ctypes.byref(wm), ctypes.byref(kt), ctypes.byref(wk)), h)
+    with torch.cuda.device(device):
+        tm = torch.as_tensor(_DevArray(mx.value, rows * wm.value), device=f"cuda:{device}")
+        tk = torch.as_tensor(_DevArray(kt.value, rows * wk.value), device=f"cuda:{device}") if kt.value else None
+    return tm, wm.value, tk, wk.value
+
+
+def wmd_query_finish(h, out_dist) -> None:
+    po, k = _ptr(out_dist, np.float32)
+    _check(lib.wmd_query_finish(h, po), h)
 
 
 def wmd_sync(h) -> None:

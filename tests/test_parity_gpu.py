@@ -659,3 +659,70 @@ def test_graph_replay_equals_direct_launches(W, path):
             W.wmd_destroy(h)
     assert np.array_equal(runs[0], runs[1])
     assert not np.array_equal(runs[1][0], runs[1][1])
+
+
+# ------------------------------------------------------------------ NEXT-4: sharded build
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("P", [2, 3])
+def test_sharded_build_two_phase_equals_one_shot(W, path, P):
+    """wmd_query_begin/tables/finish with the vocabulary rows split over P ranks (emulated by P
+    handles on one GPU; the table all-gather done here by copying the ranks' row slices) gives
+    the one-shot wmd_query's distances bit for bit, for every rank's document shard."""
+    import torch
+    from paper_2005_06727_b200 import sharded
+    wl = synth.make_workload("tweet", n_queries=1, N=600)
+    q, w = wl.queries[0]
+    ref = run_gpu(W, wl.E, wl.col_ptr, wl.row_idx, wl.val, q, w, 10.0, 15, path=path)
+    bounds = sharded.shard_bounds(wl.col_ptr, P)
+    V = wl.cfg.V
+    hs = []
+    try:
+        for g in range(P):
+            h = W.wmd_create(wl.E)
+            W.wmd_set_option(h, W.WMD_OPT_PATH, path)
+            cp, ri, va = sharded.local_shard(wl.col_ptr, wl.row_idx, wl.val, bounds, g)
+            W.wmd_set_targets(h, cp, ri, va)
+            hs.append(h)
+        tabs = []
+        for g, h in enumerate(hs):
+            b, e, R = sharded.build_rows(V, P, g)
+            W.wmd_query_begin(h, q, w, 10.0, 15, b, e, table_rows=P * R)
+            tabs.append(W.wmd_query_tables(h, P * R))
+        torch.cuda.synchronize()
+        for g in range(P):  # emulated all-gather of the row slices
+            b, e, R = sharded.build_rows(V, P, g)
+            for t in (0, 2):
+                if tabs[g][t] is None:
+                    continue
+                wdt = tabs[g][t + 1]
+                for dst in range(P):
+                    if dst != g:
+                        tabs[dst][t][b * wdt:e * wdt].copy_(tabs[g][t][b * wdt:e * wdt])
+        torch.cuda.synchronize()
+        got = []
+        for g, h in enumerate(hs):
+            d = np.empty(int(bounds[g + 1] - bounds[g]), np.float32)
+            W.wmd_query_finish(h, d)
+            W.wmd_sync(h)
+            got.append(d)
+    finally:
+        for h in hs:
+            W.wmd_destroy(h)
+    assert np.array_equal(np.concatenate(got), ref)
+
+
+def test_two_phase_errors(W):
+    wl = synth.make_workload("tiny")
+    q, w = wl.queries[0]
+    h = W.wmd_create(wl.E)
+    try:
+        W.wmd_set_targets(h, wl.col_ptr, wl.row_idx, wl.val)
+        with pytest.raises(W.WmdError) as e:
+            W.wmd_query_finish(h, np.empty(wl.N, np.float32))
+        assert e.value.status == W.WMD_ERR_STATE
+        with pytest.raises(W.WmdError) as e:
+            W.wmd_query_begin(h, q, w, 10.0, 15, 5, wl.cfg.V + 1)
+        assert e.value.status == W.WMD_ERR_INVALID_ARGUMENT
+    finally:
+        W.wmd_destroy(h)

@@ -137,3 +137,35 @@ def test_query_assignment_partitions_queries():
         for P in (1, 2, 3, 8):
             parts = [sharded.query_assignment(nq, P, g) for g in range(P)]
             assert np.array_equal(np.sort(np.concatenate(parts)), np.arange(nq))
+
+
+def _table_worker(rank, world, port, result_path, V, width):
+    """Sharded build bookkeeping: each rank fills its build_rows slice, gather_table (in-place
+    all_gather_into_tensor of equal R-row slices) must give every rank the full table."""
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2005_06727_b200 import sharded
+    b, e, R = sharded.build_rows(V, world, rank)
+    table = torch.full((world * R * width,), -1.0)
+    rows = torch.arange(b, e, dtype=torch.float32).repeat_interleave(width)
+    table[b * width:e * width] = rows
+    sharded.gather_table(table, R, width, world, rank)
+    if rank == 0:
+        np.save(result_path, table.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,V", [(2, 11), (3, 10), (3, 2)])
+def test_sharded_build_table_gather(tmp_path, world, V):
+    width = 5
+    res = str(tmp_path / "table.npy")
+    mp.start_processes(_table_worker, args=(world, _free_port(), res, V, width), nprocs=world, join=True,
+                       start_method="spawn")
+    got = np.load(res)
+    assert np.array_equal(got[: V * width], np.arange(V, dtype=np.float32).repeat(width))
