@@ -76,7 +76,7 @@ void launch_sinkhorn_fused(const int4* sdoc, const Entry* ent, int64_t N,
 int fused_launch_count(const int64_t* len_prefix, int64_t max_len, int64_t N);
 
 // --- a6: FP64 re-run of flagged documents (no CPU fallback) --------------------------------
-constexpr int kFallbackBlocks = 148;  // 1 per SM (200 KB of shared memory each)
+constexpr int kFallbackBlocks = 296;  // 2 per SM (1 per SM for documents whose K needs > 100 KB)
 size_t fallback_scratch_bytes(int64_t max_doc_nnz);
 void launch_fallback_fp64(const float* Mx, int ld, const float* rpad, int v_r,
                           double lambda, int iters, float tol, int32_t* iters_doc,

@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(256, FINAL ? 2 : PASS_BLOCKS_PER_SM) sinkhorn_
 // threads over rows, the SpMM with threads over columns) when the document fits
 // (kFallbackSmem), else in a per-block global scratch with the same layout. The SpMM splits
 // the rows over two thread halves; gauge and change test are block reductions.
-constexpr int kFallbackSmem = 200 * 1024;
+constexpr int kFallbackSmem = 200 * 1024;  // per block at most; 100 KB lets two blocks share an SM
 
 __global__ void __launch_bounds__(256) fallback_fp64_kernel(
     const float* __restrict__ Mt, int ld,
@@ -360,7 +360,8 @@ __global__ void __launch_bounds__(256) fallback_fp64_kernel(
     int32_t* __restrict__ iters_doc, const int32_t* __restrict__ doc_ptr, const Entry* __restrict__ ent,
     const int32_t* __restrict__ flagged_list, const int32_t* __restrict__ flagged_count,
     double* __restrict__ scratch, int64_t max_doc_nnz, float* __restrict__ dist,
-    uint8_t* __restrict__ flags, int32_t* __restrict__ breakdown, int32_t* __restrict__ fb_count) {
+    uint8_t* __restrict__ flags, int32_t* __restrict__ breakdown, int32_t* __restrict__ fb_count,
+    int smem_bytes) {
   extern __shared__ double ksm[];
   __shared__ double u[WMD_MAX_VR_DEV], part[2][WMD_MAX_VR_DEV], red[3][8];
   const int n = *flagged_count;
@@ -373,7 +374,7 @@ __global__ void __launch_bounds__(256) fallback_fp64_kernel(
   for (int idx = blockIdx.x; idx < n; idx += gridDim.x) {
     const int j = flagged_list[idx];
     const int b = doc_ptr[j], L = doc_ptr[j + 1] - b;
-    double* K = (int64_t)L * pitch * 8 <= kFallbackSmem ? ksm : gK;
+    double* K = (int64_t)L * pitch * 8 <= smem_bytes ? ksm : gK;
     for (int p = tid; p < L * v_r; p += blockDim.x) {  // K = exp(-lambda (M - m)), FP64
       const int e_ = p / v_r, i = p % v_r;
       const int k = ent[b + e_].k;
@@ -549,16 +550,18 @@ void launch_fallback_fp64(const float* Mt, int ld, const float* rpad, int v_r,
                           const int32_t* flagged_list, const int32_t* flagged_count,
                           double* scratch, int64_t max_doc_nnz, float* dist, uint8_t* flags,
                           int32_t* breakdown, int32_t* fallback_count, cudaStream_t st) {
+  // shared memory for the largest document's K (two blocks per SM when it fits in 100 KB)
+  const int64_t need = max_doc_nnz * (v_r + 1) * 8;
+  const int smem = (int)std::min<int64_t>(need, kFallbackSmem);
+  const int blocks = smem <= kFallbackSmem / 2 ? kFallbackBlocks : kFallbackBlocks / 2;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(fallback_fp64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFallbackSmem);
     attr = true;
   }
-  fallback_fp64_kernel<<<kFallbackBlocks, 256, kFallbackSmem, st>>>(Mt, ld, rpad, v_r, lambda, iters, tol,
-                                                        iters_doc, doc_ptr,
-                                                        ent, flagged_list, flagged_count, scratch,
-                                                        max_doc_nnz, dist, flags, breakdown,
-                                                        fallback_count);
+  fallback_fp64_kernel<<<blocks, 256, smem, st>>>(Mt, ld, rpad, v_r, lambda, iters, tol, iters_doc, doc_ptr, ent,
+                                                  flagged_list, flagged_count, scratch, max_doc_nnz, dist, flags,
+                                                  breakdown, fallback_count, smem);
 }
 
 __global__ void fill_i32_kernel(int32_t* p, int64_t n, int32_t v) {
