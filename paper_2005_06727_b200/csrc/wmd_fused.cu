@@ -39,12 +39,13 @@
 #include <cfloat>
 #include <cstdint>
 
-#include "wmd_device.cuh"
+#include "wmd_tile.cuh"
 
 namespace wmd {
 namespace {
 
 using namespace dev;
+using namespace tile;
 
 constexpr int kWarps = 4;                  // warps per block
 constexpr int kThreads = 32 * kWarps;
@@ -64,128 +65,6 @@ struct Shape {
   static constexpr int TSH = TW == 4 ? 1 : 2;   // tail row slot t of lane b: TW a + (t ^ (b >> TSH))
   static constexpr int REGS = RW * CW;
 };
-
-__device__ __forceinline__ float lg2_approx(float x) {
-  float y;
-  asm("lg2.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-__device__ __forceinline__ float ex2_ftz(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint64_t pol) {
-  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "l"(pol)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ float shx(float v, int m) { return __shfl_xor_sync(kFull, v, m); }
-
-// Row index (within the document) of row slot s of lane (a, b).
-template <int NT, int TW>
-__device__ __forceinline__ int row_of(int s, int a, int b) {
-  constexpr int TSH = TW == 4 ? 1 : 2;
-  if (s < 8 * NT) return 32 * (s >> 3) + 8 * a + ((s & 7) ^ b);
-  return 32 * NT + TW * a + ((s - 8 * NT) ^ (b >> TSH));
-}
-
-// Column (query row) of column slot c of lane (a, b).
-template <int CW>
-__device__ __forceinline__ int col_of(int c, int a, int b) {
-  if constexpr (CW == 8) return 8 * b + 4 * (c >> 2) + ((c & 3) ^ a);
-  else if constexpr (CW == 4) return 4 * b + (c ^ a);
-  else if constexpr (CW == 2) return 2 * b + (c ^ (a >> 1));
-  else return b;
-}
-
-// Permute x[0..CW) (natural column order of this lane's column group) into slot order:
-// x'[c] = x[c ^ key], key = a (per quad for CW = 8) or a >> 1 (CW = 2).
-template <int CW>
-__device__ __forceinline__ void to_slots(float (&x)[CW], int a) {
-  if constexpr (CW >= 4) {
-#pragma unroll
-    for (int q = 0; q < CW / 4; ++q) {
-      float* y = x + 4 * q;
-      const bool s1 = a & 1, s2 = a & 2;
-      float t0 = s1 ? y[1] : y[0], t1 = s1 ? y[0] : y[1];
-      float t2 = s1 ? y[3] : y[2], t3 = s1 ? y[2] : y[3];
-      y[0] = s2 ? t2 : t0; y[2] = s2 ? t0 : t2;
-      y[1] = s2 ? t3 : t1; y[3] = s2 ? t1 : t3;
-    }
-  } else if constexpr (CW == 2) {
-    const bool s2 = a & 2;
-    const float t0 = s2 ? x[1] : x[0], t1 = s2 ? x[0] : x[1];
-    x[0] = t0; x[1] = t1;
-  }
-}
-
-// Loads this lane's CW natural-order columns of one staged row.
-template <int CW>
-__device__ __forceinline__ void load_cols(const float* row, int b, float (&x)[CW]) {
-  if constexpr (CW >= 4) {
-#pragma unroll
-    for (int q = 0; q < CW / 4; ++q) {
-      const float4 t = *reinterpret_cast<const float4*>(row + CW * b + 4 * q);
-      x[4 * q] = t.x; x[4 * q + 1] = t.y; x[4 * q + 2] = t.z; x[4 * q + 3] = t.w;
-    }
-  } else if constexpr (CW == 2) {
-    const float2 t = *reinterpret_cast<const float2*>(row + 2 * b);
-    x[0] = t.x; x[1] = t.y;
-  } else {
-    x[0] = row[b];
-  }
-}
-
-// Transpose-reduce of the row partials p[0..RW) over the 8 b-lanes: afterwards p[8T] holds the
-// full sum of row 32T + 8a + b (full tiles) and p[8NT] that of tail row 32NT + TW a + (b >> TSH).
-template <int NT, int TW>
-__device__ __forceinline__ void reduce_rows(float* p) {
-#pragma unroll
-  for (int T = 0; T < NT; ++T) {
-    float* q = p + 8 * T;
-#pragma unroll
-    for (int t = 0; t < 4; ++t) q[t] += shx(q[t + 4], 4);
-#pragma unroll
-    for (int t = 0; t < 2; ++t) q[t] += shx(q[t + 2], 2);
-    q[0] += shx(q[1], 1);
-  }
-  if constexpr (TW == 4) {
-    float* q = p + 8 * NT;
-    q[0] += shx(q[2], 4); q[1] += shx(q[3], 4);
-    q[0] += shx(q[1], 2);
-    q[0] += shx(q[0], 1);
-  } else if constexpr (TW == 2) {
-    float* q = p + 8 * NT;
-    q[0] += shx(q[1], 4);
-    q[0] += shx(q[0], 2);
-    q[0] += shx(q[0], 1);
-  }
-}
-
-// Transpose-reduce of the column partials q[0..CW) over the 4 a-lanes (lane xor 16, 8):
-// afterwards q[0] (and q[4] for CW = 8) holds the full sum of the lane's own column(s).
-template <int CW>
-__device__ __forceinline__ void reduce_cols(float* q) {
-  if constexpr (CW >= 4) {
-#pragma unroll
-    for (int g = 0; g < CW / 4; ++g) {
-      float* y = q + 4 * g;
-      y[0] += shx(y[2], 16); y[1] += shx(y[3], 16);
-      y[0] += shx(y[1], 8);
-    }
-  } else if constexpr (CW == 2) {
-    q[0] += shx(q[1], 16);
-    q[0] += shx(q[0], 8);
-  } else {
-    q[0] += shx(q[0], 16);
-    q[0] += shx(q[0], 8);
-  }
-}
 
 #ifndef WMD_FUSED_DOCS_PER_WARP
 #define WMD_FUSED_DOCS_PER_WARP 1
@@ -354,7 +233,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW, D>()) sinkhor
         for (int c = 0; c < CW; ++c) {
           const float dd = K[d][s][c];
           const float kx = ex2_ftz(fmaf(-alpha, dd, amu[c]));   // rows past n: 2^-huge = 0
-          flushed |= kx < FLT_MIN && dd != FLT_MAX;
+          flushed |= nreal[c] && kx < FLT_MIN && dd != FLT_MAX;
           K[d][s][c] = nreal[c] ? kx : (dd != FLT_MAX ? 1.f : 0.f);  // padded columns: 1 on real rows
         }
         to_slots<CW>(K[d][s], a);
@@ -492,7 +371,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW, D>()) sinkhor
     //   M_ie = D_ei + m_e = mu_i + m_e - log2(Kh_ei) / alpha,
     // so q_e = sum_i Kh_ei uh_i (mu_i - log2(Kh_ei)/alpha) + m_e s_e with s_e = Kh uh from the
     // last SDDMM. Entries flushed to 0 contribute 0 (Kh log2 Kh -> 0).
-    const float ia = -1.f / alpha;
+    const float ia = -rcp_fast(alpha);  // (approximate: no IEEE-division slow-path call)
 #pragma unroll
     for (int d = 0; d < D; ++d) {
       float p[RW];
@@ -601,17 +480,22 @@ void dispatch_bucket(int bi, const int4* sdoc, const Entry* ent, int64_t p0,
 
 }  // namespace
 
-int fused_ld(int v_r) {
-  int ld = 8;
-  while (ld < v_r) ld *= 2;
-  return ld;
+// Longest document the one-warp kernel takes at row width ld (0: none).
+int warp_max_rows(int ld) {
+  int best = 0;
+  for (int b = 0; b < kNumBuckets; ++b)
+    if (fits(ld / 8, kBuckets[b].ne)) best = kBuckets[b].ne;
+  return ld <= 64 ? best : 0;
 }
 
-bool fused_supported(int ld, int64_t max_doc_nnz) {
-  if (ld > 64 || (ld & (ld - 1)) || ld < 8 || max_doc_nnz > 64) return false;
-  for (int b = 0; b < kNumBuckets; ++b)
-    if (kBuckets[b].ne >= max_doc_nnz) return fits(ld / 8, kBuckets[b].ne);
-  return false;
+int fused_ld(int v_r, int64_t max_doc_nnz, bool conv) {
+  int ld = 8;
+  while (ld < v_r) ld *= 2;
+  if (ld > 128) return 0;
+  if (max_doc_nnz <= warp_max_rows(ld)) return ld;
+  // longer documents: one CTA per document (wmd_fused_cta.cu; fixed iteration count, ld >= 32)
+  if (conv || max_doc_nnz > cta_max_rows()) return 0;
+  return std::max(ld, 32);
 }
 
 void launch_sinkhorn_fused(const int4* sdoc, const Entry* ent, int64_t N,
@@ -620,9 +504,11 @@ void launch_sinkhorn_fused(const int4* sdoc, const Entry* ent, int64_t N,
                            int32_t* iters_doc, float* dist, uint8_t* flags, int32_t* flagged_list,
                            int32_t* flagged_count, cudaStream_t st) {
   // len_prefix[L] = number of documents with fewer than L nonzeros: the length-sorted order
-  // splits into buckets of at most 8 / 16 / 32 / 40 / 48 / 64 nonzeros, one launch each.
+  // splits into buckets of at most 8 / 16 / 32 / 40 / 48 / 64 nonzeros (one-warp kernel, one
+  // launch each) and, past warp_max_rows(ld), 64 / 128 / ... / 320 (one-CTA kernel).
+  const int wmax = warp_max_rows(ld);
   int64_t p0 = 0;
-  for (int bi = 0; bi < kNumBuckets && p0 < N; ++bi) {
+  for (int bi = 0; bi < kNumBuckets && p0 < N && kBuckets[bi].ne <= wmax; ++bi) {
     const int NE = kBuckets[bi].ne;
     const int64_t p1 = NE >= max_len ? N : len_prefix[NE + 1];
     if (p1 > p0) {
@@ -634,19 +520,23 @@ void launch_sinkhorn_fused(const int4* sdoc, const Entry* ent, int64_t N,
         default: break;
       }
     }
-    p0 = p1;
+    p0 = std::max(p0, p1);
   }
+  if (p0 < N)
+    launch_sinkhorn_cta(sdoc, ent, p0, N, len_prefix, max_len, Mx, ld, v_r, rpad, lambda, iters, iters_doc,
+                        dist, flags, flagged_list, flagged_count, st);
 }
 
-int fused_launch_count(const int64_t* len_prefix, int64_t max_len, int64_t N) {
+int fused_launch_count(const int64_t* len_prefix, int64_t max_len, int64_t N, int ld) {
+  const int wmax = warp_max_rows(ld);
   int64_t p0 = 0;
   int cnt = 0;
-  for (int bi = 0; bi < kNumBuckets && p0 < N; ++bi) {
+  for (int bi = 0; bi < kNumBuckets && p0 < N && kBuckets[bi].ne <= wmax; ++bi) {
     const int64_t p1 = kBuckets[bi].ne >= max_len ? N : len_prefix[kBuckets[bi].ne + 1];
     cnt += p1 > p0;
-    p0 = p1;
+    p0 = std::max(p0, p1);
   }
-  return cnt;
+  return cnt + (p0 < N ? cta_launch_count(p0, N, len_prefix, max_len) : 0);
 }
 
 }  // namespace wmd

@@ -1,0 +1,558 @@
+// wmd_fused_cta.cu — NEXT-1 for long documents: all Sinkhorn iterations and the final step of a
+// document of up to 32 W words in ONE CTA of W warps, the document's Kh block in registers.
+//
+// Same method as the one-warp-per-document kernel (wmd_fused.cu: doc-local two-sided rescale
+// Kh = 2^(-alpha D + beta_i + gamma_e), power-of-two gauge, FP32 range certificate, final step
+// with D recovered from Kh), for the shapes that do not fit one warp's registers (the Long
+// config: 50-300-word documents against 100 query words). Warp w holds rows [32w, 32w + 32) of
+// the block as the 2-D lane tile of wmd_tile.cuh (8 rows x CW columns per lane, LD = 8 CW):
+//   SDDMM  s = Kh uh    : warp-local (row partials, transpose-reduce over the b-lanes)
+//   SpMM   acc = Kh^T vh: per-warp column partials (transpose-reduce over the a-lanes) to shared
+//                         memory; ONE barrier; then every warp sums the W partials of all LD
+//                         columns itself (LD / 32 per lane, vector reads), so uh = r / acc, its
+//                         gauge and the range checks are computed redundantly and bit-identically
+//                         by every warp (no second barrier), and each lane gets its CW columns by
+//                         three xor-shuffles per column quad.
+// The column partials are double-buffered by pass parity, so one barrier per iteration orders
+// everything. No global memory traffic inside the loop.
+//
+// Re-anchoring (R33) instead of flagging: when a range check fails (a uh spread too
+// wide for the FP32 exponent; PAPER.md:62-66 iterates K = exp(-lambda M) in FP64), the CTA
+// recomputes the block from D in the log domain with the pass's input uh absorbed into the
+// column shifts, beta_i += log2 uh_i, and row shifts gamma_e = -max_i(-alpha D_ei + beta_i) (each
+// row's largest entry becomes 1), sets uh = 1 and redoes the pass. Kh -> diag(a) Kh diag(b) is a
+// diagonal rescaling under which Algorithm 1's iterates are equivariant (u -> u / b, v -> v / a,
+// transport plan and distance unchanged), so only rounding changes; entries are recomputed from
+// D, never from flushed products, so the certificate's invariant (a zero entry stands for a true
+// value < 2^-126 in the current scale) holds after the rescale. Only a document that still fails
+// after kMaxAnchors re-anchors is flagged for the FP64 re-run. Bound: FP32 issue.
+#include <algorithm>
+#include <cfloat>
+#include <cstdint>
+
+#include "wmd_tile.cuh"
+
+namespace wmd {
+namespace {
+
+using namespace dev;
+using namespace tile;
+
+constexpr float kUnderC = 0x1p-110f;        // 2^-126 / 2^-16
+constexpr float kLog2eC = 1.4426950408889634f;
+#ifndef WMD_CTA_MAX_ANCHORS
+#define WMD_CTA_MAX_ANCHORS 4
+#endif
+constexpr int kMaxAnchors = WMD_CTA_MAX_ANCHORS;
+
+template <int CW, int W, int TW>
+struct CtaShape {
+  static constexpr int LD = 8 * CW;
+  static constexpr int NQ = CW / 4;            // columns per lane in the column step (LD / 32)
+  static constexpr int RPW = 32 + 4 * TW;      // rows per warp: a 32-row tile + 4 TW tail rows
+  static constexpr int RW = 8 + TW;            // row slots per lane
+  static constexpr int NOWN = TW ? 2 : 1;      // own rows per lane after the row reduce
+  static constexpr int TSH = TW == 4 ? 1 : 2;  // tail row slot t of lane b: 32 + TW a + (t ^ (b >> TSH))
+  static constexpr int ROWS = W * RPW;
+  static constexpr int P = LD + 4;             // row pitch of Mx
+  static constexpr int CP = LD + 4;            // pitch of one warp's column partials (+ its vmax)
+  static constexpr int SMEM_FLOATS = 2 * W * CP + LD + 2 * ROWS + W + 4;
+};
+
+// Resident warps per SM the register budget is written for: 12 (168 registers per thread) for
+// CW <= 8; 8 (255 registers) for CW = 16, whose Kh block alone takes 128-160 registers per
+// thread (at 168 it spills, and the spilling build faulted on some shapes: DESIGN.md §5).
+#ifndef WMD_CTA_WARPS_PER_SM
+#define WMD_CTA_WARPS_PER_SM 12
+#endif
+#ifndef WMD_CTA_WARPS_PER_SM_16
+#define WMD_CTA_WARPS_PER_SM_16 8
+#endif
+template <int CW, int W>
+constexpr int cta_min_blocks() {
+  constexpr int wps = CW >= 16 ? WMD_CTA_WARPS_PER_SM_16 : WMD_CTA_WARPS_PER_SM;
+  return W < wps ? wps / W : 1;
+}
+
+template <int CW, int W, int TW>
+__global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W>()) sinkhorn_cta_kernel(
+    const int4* __restrict__ sdoc, const Entry* __restrict__ ent, int64_t pos0, int64_t pos1,
+    const float* __restrict__ Mx, int v_r, const float* __restrict__ rpad, float lambda, int iters,
+    int32_t* __restrict__ iters_doc, float* __restrict__ dist, uint8_t* __restrict__ flags,
+    int32_t* __restrict__ flagged_list, int32_t* __restrict__ flagged_count) {
+  using S = CtaShape<CW, W, TW>;
+  constexpr int LD = S::LD, NQ = S::NQ, P = S::P, CP = S::CP, RW = S::RW, RPW = S::RPW;
+  constexpr int NOWN = S::NOWN, TSH = S::TSH, ROWS = S::ROWS, NT = 32 * W;
+  constexpr int EPT = (ROWS + NT - 1) / NT;    // entries each thread prefetches
+  static_assert(CW % 4 == 0, "column quads");
+  static_assert(TW == 0 || TW == 2 || TW == 4, "tail width");
+  extern __shared__ __align__(16) float csm[];
+  float* colpart = csm;                                    // [2][W][CP]; [.][w][LD] = warp's vmax
+  float* betal = colpart + 2 * W * CP;                     // [LD] column shifts beta (log2 units)
+  int* ents = reinterpret_cast<int*>(betal + LD);          // [ROWS] vocabulary row of each word
+  float* cents = reinterpret_cast<float*>(ents + ROWS);    // [ROWS] its c
+  float* wred = cents + ROWS;                              // [W] per-warp distance partials
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int a = lane >> 3, b = lane & 7;
+  const int row0 = RPW * warp;                             // first row of this warp's block
+  const int2* ent2 = reinterpret_cast<const int2*>(ent);
+  const float alpha = lambda * kLog2eC;
+  const float ia = -rcp_fast(alpha);  // (approximate: no IEEE-division slow-path call)
+  const float kv_s = (float)v_r * kUnderC;
+  // column step: this lane owns columns CW*b + 4g + a (g < NQ), the ones reduce_cols leaves it
+  float r_own[NQ];
+#pragma unroll
+  for (int g = 0; g < NQ; ++g) r_own[g] = __ldg(rpad + CW * b + 4 * g + a);  // zero beyond v_r
+  // own rows after the row reduce: row0 + lane, and the tail row row0 + 32 + TW a + (b >> TSH)
+  int orow[NOWN];
+  orow[0] = row0 + lane;
+  if constexpr (TW > 0) orow[NOWN - 1] = row0 + 32 + TW * a + (b >> TSH);
+
+  // ---- prefetch: header and this thread's entries (rows tid, tid + 32 W, ...) of the next document
+  int64_t pos = pos0 + blockIdx.x;
+  int pj = -1, pb = 0, pn = 0;
+  int2 pe[EPT];
+  auto stage1 = [&](int64_t p) {
+    pj = -1; pn = 0; pb = 0;
+    if (p < pos1) {
+      const int4 x = __ldg(sdoc + p);
+      pj = x.x; pb = x.y; pn = x.z;
+    }
+  };
+  auto stage2 = [&]() {
+#pragma unroll
+    for (int x = 0; x < EPT; ++x) {
+      const int e = tid + NT * x;
+      pe[x] = e < pn ? __ldg(ent2 + pb + e) : make_int2(0, 0);
+    }
+  };
+  stage1(pos);
+  stage2();
+
+  float K[RW][CW];
+  // a per-own-row value broadcast to the row slots (slot s < 8: row 8a + (s ^ b), lane ^ s;
+  // tail slot 8 + t: row 32 + TW a + (t ^ (b >> TSH)), lane ^ (t << TSH))
+  auto rows_to_slots = [&](const float (&o)[NOWN], float (&x)[RW]) {
+    x[0] = o[0];
+#pragma unroll
+    for (int t = 1; t < 8; ++t) x[t] = shx(o[0], t);
+    if constexpr (TW > 0) {
+      x[8] = o[NOWN - 1];
+#pragma unroll
+      for (int t = 1; t < TW; ++t) x[8 + t] = shx(o[NOWN - 1], t << TSH);
+    }
+  };
+  // D = M - m of this lane's row slots, natural column order; FLT_MAX on rows past n
+  auto load_D = [&](int n) {
+#pragma unroll
+    for (int s = 0; s < RW; ++s) {
+      const int e = row0 + row_of<1, TW>(s, a, b);
+      const bool ok = e < n;
+      const float* row = Mx + (size_t)(ok ? ents[e] : 0) * P;
+      float x[CW];
+#pragma unroll
+      for (int q = 0; q < CW / 4; ++q) {
+        const float4 t = __ldg(reinterpret_cast<const float4*>(row + CW * b) + q);
+        x[4 * q] = t.x; x[4 * q + 1] = t.y; x[4 * q + 2] = t.z; x[4 * q + 3] = t.w;
+      }
+      const float me = __ldg(row + LD);
+#pragma unroll
+      for (int c = 0; c < CW; ++c) K[s][c] = ok ? x[c] - me : FLT_MAX;
+    }
+  };
+
+  for (; pos < pos1; pos += gridDim.x) {
+    const int j = pj, n = pn;
+#pragma unroll
+    for (int x = 0; x < EPT; ++x) {
+      const int e = tid + NT * x;
+      if (e < ROWS) {
+        ents[e] = pe[x].x;
+        cents[e] = __int_as_float(pe[x].y);
+      }
+    }
+    stage1(pos + gridDim.x);
+    __syncthreads();  // entries published; the previous document is done with shared memory
+
+    bool v_ok[NOWN];
+    float c_own[NOWN], m_own[NOWN];
+#pragma unroll
+    for (int o = 0; o < NOWN; ++o) {
+      v_ok[o] = orow[o] < n;
+      c_own[o] = v_ok[o] ? cents[orow[o]] : 0.f;
+      m_own[o] = v_ok[o] ? __ldg(Mx + (size_t)ents[orow[o]] * P + LD) : 0.f;
+    }
+    // ---- block tile: D, column minima mu (per warp, then over the CTA), beta = alpha mu
+    load_D(n);
+    float uo[NQ];  // uh of the owned columns CW b + 4g + a; the slots are rebuilt by shuffles
+    bool und;
+    {
+      float mu[CW];
+#pragma unroll
+      for (int c = 0; c < CW; ++c) {
+        mu[c] = K[0][c];
+#pragma unroll
+        for (int s = 1; s < RW; ++s) mu[c] = fminf(mu[c], K[s][c]);
+        mu[c] = fminf(mu[c], shx(mu[c], 8));
+        mu[c] = fminf(mu[c], shx(mu[c], 16));
+      }
+      if (a == 0) {
+#pragma unroll
+        for (int q = 0; q < CW / 4; ++q)
+          *reinterpret_cast<float4*>(colpart + warp * CP + CW * b + 4 * q) =
+              make_float4(mu[4 * q], mu[4 * q + 1], mu[4 * q + 2], mu[4 * q + 3]);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+#pragma unroll
+        for (int q = 0; q < CW / 4; ++q) {
+          const float4 t = *reinterpret_cast<const float4*>(colpart + w * CP + CW * b + 4 * q);
+          mu[4 * q] = fminf(mu[4 * q], t.x); mu[4 * q + 1] = fminf(mu[4 * q + 1], t.y);
+          mu[4 * q + 2] = fminf(mu[4 * q + 2], t.z); mu[4 * q + 3] = fminf(mu[4 * q + 3], t.w);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < CW; ++c) mu[c] = alpha * mu[c];  // beta (gamma = 0)
+      if (warp == 0 && a == 0) {
+#pragma unroll
+        for (int c = 0; c < CW; ++c) betal[CW * b + c] = mu[c];
+      }
+      bool flushed = false;
+#pragma unroll
+      for (int s = 0; s < RW; ++s) {
+#pragma unroll
+        for (int c = 0; c < CW; ++c) {
+          const bool real = CW * b + c < v_r;
+          const float dd = K[s][c];
+          const float kx = ex2_ftz(fmaf(-alpha, dd, mu[c]));
+          flushed |= real && kx < FLT_MIN && dd != FLT_MAX;
+          K[s][c] = real ? kx : (dd != FLT_MAX ? 1.f : 0.f);  // padded columns: 1 on real rows
+        }
+        to_slots<CW>(K[s], a);
+      }
+      und = __syncthreads_or(flushed);  // also: the minima are read, betal is published
+    }
+    // uh0 = v_r 2^-beta (x0 = 1 / v_r, in the rescaled variables) of the owned columns
+#pragma unroll
+    for (int g = 0; g < NQ; ++g) {
+      const int col = CW * b + 4 * g + a;
+      uo[g] = col < v_r ? (float)v_r * ex2_ftz(-betal[col]) : 0.f;
+    }
+    stage2();  // the next document's entries
+
+    float umax_k = (float)v_r * kv_s;  // v_r max(uh) 2^-110 (max uh0 <= v_r)
+    float gamma_own[NOWN];             // row shifts of this lane's own rows
+#pragma unroll
+    for (int o = 0; o < NOWN; ++o) gamma_own[o] = 0.f;
+    bool bad = false;
+    int anchors = 0;
+    float v_own[NOWN], s_own[NOWN];
+    int it = 0;
+    for (int pass = 0;; ++pass) {
+      // SDDMM (warp-local)
+      // (one column quad of uh live at a time: its 4 slots come from lanes ^ 0, 8, 16, 24)
+      float p[RW];
+#pragma unroll
+      for (int g = 0; g < NQ; ++g) {
+        float u4[4];
+        u4[0] = uo[g];
+#pragma unroll
+        for (int t = 1; t < 4; ++t) u4[t] = shx(uo[g], 8 * t);
+#pragma unroll
+        for (int s = 0; s < RW; ++s) {
+          float acc = g == 0 ? K[s][0] * u4[0] : fmaf(K[s][4 * g], u4[0], p[s]);
+#pragma unroll
+          for (int t = 1; t < 4; ++t) acc = fmaf(K[s][4 * g + t], u4[t], acc);
+          p[s] = acc;
+        }
+      }
+      reduce_rows<1, TW>(p);
+      bool sfail = false;
+      uint32_t vmax_l = 0u;
+#pragma unroll
+      for (int o = 0; o < NOWN; ++o) {
+        s_own[o] = p[8 * o];
+        v_own[o] = v_ok[o] ? c_own[o] * rcp_fast(s_own[o]) : 0.f;
+        sfail |= v_ok[o] && und && umax_k > s_own[o];
+        vmax_l = max(vmax_l, __float_as_uint(v_own[o]));
+      }
+      const bool last = it == iters;
+      float* cp = colpart + (pass & 1) * W * CP;
+      if (!last) {
+        const uint32_t vmax_w = __reduce_max_sync(kFull, vmax_l);
+        // SpMM: this warp's column partials
+        float vs[RW];
+        rows_to_slots(v_own, vs);
+        // (one column quad at a time: partials, then its transpose-reduce over the a-lanes)
+        float qo[NQ];
+#pragma unroll
+        for (int g = 0; g < NQ; ++g) {
+          float q[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            float q0 = K[0][4 * g + t] * vs[0];
+#pragma unroll
+            for (int s = 1; s < RW; ++s) q0 = fmaf(K[s][4 * g + t], vs[s], q0);
+            q[t] = q0;
+          }
+          reduce_cols<4>(q);
+          qo[g] = q[0];
+        }
+        // lane-major layout: this lane's NQ columns are contiguous (read back by the same lane)
+        if constexpr (NQ == 4) {
+          *reinterpret_cast<float4*>(cp + warp * CP + 4 * lane) = make_float4(qo[0], qo[1], qo[2], qo[3]);
+        } else if constexpr (NQ == 2) {
+          *reinterpret_cast<float2*>(cp + warp * CP + 2 * lane) = make_float2(qo[0], qo[1]);
+        } else {
+          cp[warp * CP + lane] = qo[0];
+        }
+        if (lane == 0) cp[warp * CP + LD] = __uint_as_float(vmax_w);
+      }
+      bool fail = __syncthreads_or(sfail);
+      float un[NQ];
+#pragma unroll
+      for (int g = 0; g < NQ; ++g) un[g] = 0.f;
+      if (!fail && !last) {
+        // column step, redundantly in every warp: acc = sum of the W warps' partials
+        float acc[NQ];
+#pragma unroll
+        for (int g = 0; g < NQ; ++g) acc[g] = 0.f;
+#pragma unroll 2
+        for (int w = 0; w < W; ++w) {  // (not fully unrolled: bounds the loads in flight)
+          if constexpr (NQ == 4) {
+            const float4 t = *reinterpret_cast<const float4*>(cp + w * CP + 4 * lane);
+            acc[0] += t.x; acc[1] += t.y; acc[2] += t.z; acc[3] += t.w;
+          } else if constexpr (NQ == 2) {
+            const float2 t = *reinterpret_cast<const float2*>(cp + w * CP + 2 * lane);
+            acc[0] += t.x; acc[1] += t.y;
+          } else {
+            acc[0] += cp[w * CP + lane];
+          }
+        }
+        bool cfail = false;
+        if (und) {  // acc-side certificate: flushed entries move acc_i by < n vmax 2^-126
+          float vmax = 0.f;
+#pragma unroll
+          for (int w = 0; w < W; ++w) vmax = fmaxf(vmax, cp[w * CP + LD]);
+          const float vcap = (float)n * vmax * kUnderC;
+#pragma unroll
+          for (int g = 0; g < NQ; ++g) cfail |= vcap > acc[g];
+        }
+        uint32_t um = 0u;
+#pragma unroll
+        for (int g = 0; g < NQ; ++g) {
+          un[g] = r_own[g] * rcp_fast(acc[g]);
+          um = max(um, __float_as_uint(un[g]));
+        }
+        // gauge: max uh -> [1, 2) by an exact power of two (identical in every warp)
+        const uint32_t umax_b = __reduce_max_sync(kFull, um);
+        const float sc = __uint_as_float((254u - min(umax_b >> 23, 253u)) << 23);
+        cfail |= umax_b > 0x7f7fffffu;
+#pragma unroll
+        for (int g = 0; g < NQ; ++g) {
+          un[g] *= sc;
+          cfail |= CW * b + 4 * g + a < v_r && !(un[g] >= FLT_MIN);
+        }
+        fail = __any_sync(kFull, cfail);  // warp-uniform, and the same in every warp
+      }
+      if (fail && anchors == kMaxAnchors) {
+        bad = true;  // give up: the FP64 re-run recomputes this document
+        fail = false;
+      }
+      if (fail) {
+        // ---- re-anchor (CTA-uniform branch): beta += log2 uh, Kh recomputed from D
+        ++anchors;
+        float bown[NQ];  // new beta of the owned columns (the same in every warp)
+#pragma unroll
+        for (int g = 0; g < NQ; ++g) {
+          const float bo = betal[CW * b + 4 * g + a];
+          bown[g] = uo[g] > 0.f ? bo + lg2_approx(uo[g]) : bo;
+        }
+        __syncthreads();  // every warp has read betal
+        if (warp == 0) {
+#pragma unroll
+          for (int g = 0; g < NQ; ++g) betal[CW * b + 4 * g + a] = bown[g];
+        }
+        load_D(n);
+#pragma unroll
+        for (int s = 0; s < RW; ++s) to_slots<CW>(K[s], a);
+        __syncthreads();  // the new betal is published
+        // L = -alpha D + beta; gamma_e = -(max of L over the real columns of row e)
+        float rmax[RW];
+#pragma unroll
+        for (int s = 0; s < RW; ++s) rmax[s] = -FLT_MAX;
+#pragma unroll
+        for (int c = 0; c < CW; ++c) {
+          const int col = col_of<CW>(c, a, b);
+          const float bc = betal[col];
+#pragma unroll
+          for (int s = 0; s < RW; ++s) {
+            const float dd = K[s][c];
+            const float L = fmaf(-alpha, dd, bc);
+            K[s][c] = L;
+            rmax[s] = (col < v_r && dd != FLT_MAX) ? fmaxf(rmax[s], L) : rmax[s];
+          }
+        }
+        reduce_rows_max<1, TW>(rmax);
+#pragma unroll
+        for (int o = 0; o < NOWN; ++o) gamma_own[o] = v_ok[o] ? -rmax[8 * o] : 0.f;
+        float gs[RW];
+        rows_to_slots(gamma_own, gs);
+        bool flushed = false;
+#pragma unroll
+        for (int s = 0; s < RW; ++s) {
+          const bool rowok = row0 + row_of<1, TW>(s, a, b) < n;
+#pragma unroll
+          for (int c = 0; c < CW; ++c) {
+            const bool real = col_of<CW>(c, a, b) < v_r;
+            const float kx = ex2_ftz(K[s][c] + gs[s]);
+            flushed |= real && rowok && kx < FLT_MIN;
+            K[s][c] = rowok ? (real ? kx : 1.f) : 0.f;
+          }
+        }
+#pragma unroll
+        for (int g = 0; g < NQ; ++g) uo[g] = CW * b + 4 * g + a < v_r ? 1.f : 0.f;
+        umax_k = kv_s;
+        und = __syncthreads_or(flushed);  // also: betal published
+        continue;                         // redo this pass in the new scale
+      }
+      if (last) break;
+      ++it;
+      umax_k = 2.f * kv_s;
+#pragma unroll
+      for (int g = 0; g < NQ; ++g) uo[g] = un[g];
+    }
+    // ---- final step: D = (beta + gamma - log2 Kh) / alpha (PAPER.md:64-66 with M = m + D)
+    {
+      float p[RW];
+#pragma unroll
+      for (int s = 0; s < RW; ++s) p[s] = 0.f;
+#pragma unroll
+      for (int g = 0; g < NQ; ++g) {
+        float u4[4], ub4[4];
+        u4[0] = uo[g];
+#pragma unroll
+        for (int t = 1; t < 4; ++t) u4[t] = shx(uo[g], 8 * t);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) ub4[t] = u4[t] * (-ia * betal[col_of<CW>(4 * g + t, a, b)]);  // uh beta / alpha
+#pragma unroll
+        for (int s = 0; s < RW; ++s) {
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const float k = K[s][4 * g + t];
+            const float kl = k > 0.f ? k * lg2_approx(k) : 0.f;
+            p[s] = fmaf(k, ub4[t], fmaf(kl * ia, u4[t], p[s]));
+          }
+        }
+      }
+      reduce_rows<1, TW>(p);
+      float wsum = 0.f;
+#pragma unroll
+      for (int o = 0; o < NOWN; ++o) {
+        const float m = fmaf(-ia, gamma_own[o], m_own[o]);
+        // each tail row is held by 2^TSH lanes: count it once
+        const bool once = o == 0 || (b & ((1 << TSH) - 1)) == 0;
+        if (v_ok[o] && once) wsum = fmaf(v_own[o], fmaf(m, s_own[o], p[8 * o]), wsum);
+      }
+#pragma unroll
+      for (int off = 16; off; off >>= 1) wsum += shx(wsum, off);
+      if (lane == 0) wred[warp] = wsum;
+    }
+    const bool anybad = __syncthreads_or(bad);
+    if (tid == 0) {
+      float total = 0.f;
+#pragma unroll
+      for (int w = 0; w < W; ++w) total += wred[w];
+      dist[j] = total;
+      if (iters_doc) iters_doc[j] = it;
+      if (anybad || !(fabsf(total) <= FLT_MAX)) {
+        flags[j] |= kFlagFp32Range;
+        flagged_list[atomicAdd(flagged_count, 1)] = j;
+      }
+    }
+  }
+}
+
+int num_sms_cta() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+template <int CW, int W, int TW>
+void launch_cta_range(const int4* sdoc, const Entry* ent, int64_t p0, int64_t p1, const float* Mx, int v_r,
+                      const float* rpad, float lambda, int iters, int32_t* itd, float* dist, uint8_t* flags,
+                      int32_t* fl, int32_t* fc, cudaStream_t st) {
+  if (p1 <= p0) return;
+  constexpr size_t smem = sizeof(float) * CtaShape<CW, W, TW>::SMEM_FLOATS;
+  static int resident = 0;
+  if (!resident) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sinkhorn_cta_kernel<CW, W, TW>, 32 * W, smem);
+    resident = std::max(1, per_sm) * num_sms_cta();
+  }
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(p1 - p0, resident));
+  sinkhorn_cta_kernel<CW, W, TW><<<grid, 32 * W, smem, st>>>(sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters,
+                                                             itd, dist, flags, fl, fc);
+}
+
+// Row buckets: W warps of 32 rows (64 ... 256), then 8 warps of 40 rows (320).
+struct CtaBucket { int rows, w, tw; };
+constexpr CtaBucket kCta[] = {{64, 2, 0}, {128, 4, 0}, {192, 6, 0}, {256, 8, 0}, {320, 8, 2}};
+constexpr int kNumCta = 5;
+
+template <int CW>
+void dispatch_cta(int wi, const int4* sdoc, const Entry* ent, int64_t p0, int64_t p1, const float* Mx, int v_r,
+                  const float* rpad, float lambda, int iters, int32_t* itd, float* dist, uint8_t* flags,
+                  int32_t* fl, int32_t* fc, cudaStream_t st) {
+  switch (wi) {
+#define C_(I, W, TW) case I: launch_cta_range<CW, W, TW>(sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, itd, dist, flags, fl, fc, st); break;
+    C_(0, 2, 0) C_(1, 4, 0) C_(2, 6, 0) C_(3, 8, 0) C_(4, 8, 2)
+#undef C_
+    default: break;
+  }
+}
+
+}  // namespace
+
+int cta_max_rows() { return kCta[kNumCta - 1].rows; }
+
+// Documents of the length-sorted range [p0, N) by row buckets (kCta); len_prefix[L] = number of
+// documents with fewer than L nonzeros.
+void launch_sinkhorn_cta(const int4* sdoc, const Entry* ent, int64_t p0, int64_t N, const int64_t* len_prefix,
+                         int64_t max_len, const float* Mx, int ld, int v_r, const float* rpad, float lambda,
+                         int iters, int32_t* iters_doc, float* dist, uint8_t* flags, int32_t* flagged_list,
+                         int32_t* flagged_count, cudaStream_t st) {
+  for (int wi = 0; wi < kNumCta && p0 < N; ++wi) {
+    const int rows = kCta[wi].rows;
+    const int64_t p1 = rows >= max_len ? N : len_prefix[rows + 1];
+    if (p1 > p0) {
+      switch (ld) {
+        case 32: dispatch_cta<4>(wi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, iters_doc, dist, flags, flagged_list, flagged_count, st); break;
+        case 64: dispatch_cta<8>(wi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, iters_doc, dist, flags, flagged_list, flagged_count, st); break;
+        case 128: dispatch_cta<16>(wi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, iters_doc, dist, flags, flagged_list, flagged_count, st); break;
+        default: break;
+      }
+    }
+    p0 = std::max(p0, p1);
+  }
+}
+
+int cta_launch_count(int64_t p0, int64_t N, const int64_t* len_prefix, int64_t max_len) {
+  int cnt = 0;
+  for (int wi = 0; wi < kNumCta && p0 < N; ++wi) {
+    const int rows = kCta[wi].rows;
+    const int64_t p1 = rows >= max_len ? N : len_prefix[rows + 1];
+    cnt += p1 > p0;
+    p0 = std::max(p0, p1);
+  }
+  return cnt;
+}
+
+}  // namespace wmd

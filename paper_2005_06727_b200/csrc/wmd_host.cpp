@@ -549,12 +549,12 @@ wmd_status prepare_query(wmd_handle* h, int32_t v_r, int64_t table_rows, bool* f
   const int64_t N = h->N;
   // fused path: ld = v_r rounded up to a power of two (the 2-D lane tiling); per-iteration
   // path: v_r rounded up to 8
-  const bool fused = (h->opt_path == WMD_PATH_FUSED || h->opt_path == WMD_PATH_AUTO) &&
-                     wmd::fused_supported(wmd::fused_ld(v_r), h->max_doc_nnz);
+  const int32_t fld = wmd::fused_ld(v_r, h->max_doc_nnz, h->tol >= 0.0);
+  const bool fused = (h->opt_path == WMD_PATH_FUSED || h->opt_path == WMD_PATH_AUTO) && fld > 0;
   if (h->opt_path == WMD_PATH_FUSED && !fused)
     return fail(h, WMD_ERR_INVALID_ARGUMENT, "fused path does not support v_r=%d, max doc nnz=%lld", v_r,
                 (long long)h->max_doc_nnz);
-  const int32_t ld = fused ? wmd::fused_ld(v_r) : round_up8(v_r);
+  const int32_t ld = fused ? fld : round_up8(v_r);
   const int64_t rows = std::max(h->V, table_rows);
   // +128 floats: the pass kernels gather unpredicated float4s up to 4*32 floats past a row
   if (!fused) CK(h, h->Kt.ensure((size_t)rows * ld + 128));
@@ -595,7 +595,7 @@ wmd_status record_solve(wmd_handle* h, const float* d_r, int32_t v_r, float lamb
     wmd::launch_sinkhorn_fused(h->sdoc.p, h->ent.p, N, h->len_prefix.data(),
                                h->max_doc_nnz, h->Mx.p, ld, v_r, d_r, lambda, iters, tol, h->iters_doc.p,
                                dist, h->flags.p, h->flagged.p, h->counters.p, st);
-    launches += wmd::fused_launch_count(h->len_prefix.data(), h->max_doc_nnz, N);
+    launches += wmd::fused_launch_count(h->len_prefix.data(), h->max_doc_nnz, N, ld);
     if (pe) { CK(h, cudaEventRecord(pe->ev[2], st)); CK(h, cudaEventRecord(pe->ev[3], st)); }
   } else {
     // a4: iters fused SDDMM_SpMM launches, u ping-pong
@@ -648,7 +648,7 @@ void note_query(wmd_handle* h, const int32_t* d_sel, const float* d_r, int32_t v
   h->u_valid = !fused && iters > 0;
   h->u_last = (!fused && iters > 0) ? ((iters - 1) & 1 ? h->ub.p : h->ua.p) : nullptr;
   h->path_used = fused ? WMD_PATH_FUSED : WMD_PATH_PER_ITER;
-  h->st.iter_launches += fused ? wmd::fused_launch_count(h->len_prefix.data(), h->max_doc_nnz, h->N) : iters;
+  h->st.iter_launches += fused ? wmd::fused_launch_count(h->len_prefix.data(), h->max_doc_nnz, h->N, ld) : iters;
   h->v_r = v_r;
   h->ld = ld;
   h->last_sel = d_sel;

@@ -1,0 +1,163 @@
+// wmd_tile.cuh — register-tile helpers shared by the fused Sinkhorn kernels (wmd_fused.cu: one
+// warp per document; wmd_fused_cta.cu: one CTA per long document). A warp holds a document-row
+// x query-row tile of Kh with lane = 8a + b: a in [0,4) selects 8-row groups of a 32-row tile,
+// b in [0,8) selects CW-column groups; register slots are XOR-permuted by the lane bits so the
+// transpose-reduces below send the upper half of the slots and keep the lower half (no selects).
+#pragma once
+#include <cstdint>
+
+#include "wmd_device.cuh"
+
+namespace wmd {
+namespace tile {
+
+using dev::kFull;
+
+__device__ __forceinline__ float lg2_approx(float x) {
+  float y;
+  asm("lg2.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint64_t pol) {
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ float shx(float v, int m) { return __shfl_xor_sync(kFull, v, m); }
+
+// Row index (within the document) of row slot s of lane (a, b).
+template <int NT, int TW>
+__device__ __forceinline__ int row_of(int s, int a, int b) {
+  constexpr int TSH = TW == 4 ? 1 : 2;
+  if (s < 8 * NT) return 32 * (s >> 3) + 8 * a + ((s & 7) ^ b);
+  return 32 * NT + TW * a + ((s - 8 * NT) ^ (b >> TSH));
+}
+
+// Column (query row) of column slot c of lane (a, b).
+template <int CW>
+__device__ __forceinline__ int col_of(int c, int a, int b) {
+  if constexpr (CW >= 4) return CW * b + 4 * (c >> 2) + ((c & 3) ^ a);
+  else if constexpr (CW == 2) return 2 * b + (c ^ (a >> 1));
+  else return b;
+}
+
+// Permute x[0..CW) (natural column order of this lane's column group) into slot order:
+// x'[c] = x[c ^ key], key = a (per quad for CW = 8) or a >> 1 (CW = 2).
+template <int CW>
+__device__ __forceinline__ void to_slots(float (&x)[CW], int a) {
+  if constexpr (CW >= 4) {
+#pragma unroll
+    for (int q = 0; q < CW / 4; ++q) {
+      float* y = x + 4 * q;
+      const bool s1 = a & 1, s2 = a & 2;
+      float t0 = s1 ? y[1] : y[0], t1 = s1 ? y[0] : y[1];
+      float t2 = s1 ? y[3] : y[2], t3 = s1 ? y[2] : y[3];
+      y[0] = s2 ? t2 : t0; y[2] = s2 ? t0 : t2;
+      y[1] = s2 ? t3 : t1; y[3] = s2 ? t1 : t3;
+    }
+  } else if constexpr (CW == 2) {
+    const bool s2 = a & 2;
+    const float t0 = s2 ? x[1] : x[0], t1 = s2 ? x[0] : x[1];
+    x[0] = t0; x[1] = t1;
+  }
+}
+
+// Loads this lane's CW natural-order columns of one staged row.
+template <int CW>
+__device__ __forceinline__ void load_cols(const float* row, int b, float (&x)[CW]) {
+  if constexpr (CW >= 4) {
+#pragma unroll
+    for (int q = 0; q < CW / 4; ++q) {
+      const float4 t = *reinterpret_cast<const float4*>(row + CW * b + 4 * q);
+      x[4 * q] = t.x; x[4 * q + 1] = t.y; x[4 * q + 2] = t.z; x[4 * q + 3] = t.w;
+    }
+  } else if constexpr (CW == 2) {
+    const float2 t = *reinterpret_cast<const float2*>(row + 2 * b);
+    x[0] = t.x; x[1] = t.y;
+  } else {
+    x[0] = row[b];
+  }
+}
+
+// Transpose-reduce of the row partials p[0..RW) over the 8 b-lanes: afterwards p[8T] holds the
+// full sum of row 32T + 8a + b (full tiles) and p[8NT] that of tail row 32NT + TW a + (b >> TSH).
+template <int NT, int TW>
+__device__ __forceinline__ void reduce_rows(float* p) {
+#pragma unroll
+  for (int T = 0; T < NT; ++T) {
+    float* q = p + 8 * T;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) q[t] += shx(q[t + 4], 4);
+#pragma unroll
+    for (int t = 0; t < 2; ++t) q[t] += shx(q[t + 2], 2);
+    q[0] += shx(q[1], 1);
+  }
+  if constexpr (TW == 4) {
+    float* q = p + 8 * NT;
+    q[0] += shx(q[2], 4); q[1] += shx(q[3], 4);
+    q[0] += shx(q[1], 2);
+    q[0] += shx(q[0], 1);
+  } else if constexpr (TW == 2) {
+    float* q = p + 8 * NT;
+    q[0] += shx(q[1], 4);
+    q[0] += shx(q[0], 2);
+    q[0] += shx(q[0], 1);
+  }
+}
+
+// As reduce_rows with max instead of sum.
+template <int NT, int TW>
+__device__ __forceinline__ void reduce_rows_max(float* p) {
+#pragma unroll
+  for (int T = 0; T < NT; ++T) {
+    float* q = p + 8 * T;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) q[t] = fmaxf(q[t], shx(q[t + 4], 4));
+#pragma unroll
+    for (int t = 0; t < 2; ++t) q[t] = fmaxf(q[t], shx(q[t + 2], 2));
+    q[0] = fmaxf(q[0], shx(q[1], 1));
+  }
+  if constexpr (TW == 4) {
+    float* q = p + 8 * NT;
+    q[0] = fmaxf(q[0], shx(q[2], 4)); q[1] = fmaxf(q[1], shx(q[3], 4));
+    q[0] = fmaxf(q[0], shx(q[1], 2));
+    q[0] = fmaxf(q[0], shx(q[0], 1));
+  } else if constexpr (TW == 2) {
+    float* q = p + 8 * NT;
+    q[0] = fmaxf(q[0], shx(q[1], 4));
+    q[0] = fmaxf(q[0], shx(q[0], 2));
+    q[0] = fmaxf(q[0], shx(q[0], 1));
+  }
+}
+
+// Transpose-reduce of the column partials q[0..CW) over the 4 a-lanes (lane xor 16, 8):
+// afterwards q[0] (and q[4] for CW = 8) holds the full sum of the lane's own column(s).
+template <int CW>
+__device__ __forceinline__ void reduce_cols(float* q) {
+  if constexpr (CW >= 4) {
+#pragma unroll
+    for (int g = 0; g < CW / 4; ++g) {
+      float* y = q + 4 * g;
+      y[0] += shx(y[2], 16); y[1] += shx(y[3], 16);
+      y[0] += shx(y[1], 8);
+    }
+  } else if constexpr (CW == 2) {
+    q[0] += shx(q[1], 16);
+    q[0] += shx(q[0], 8);
+  } else {
+    q[0] += shx(q[0], 16);
+    q[0] += shx(q[0], 8);
+  }
+}
+
+}  // namespace tile
+}  // namespace wmd

@@ -497,16 +497,22 @@ def test_auto_path_selection_and_cross_path_agreement(W):
     assert np.array_equal(res[W.WMD_PATH_AUTO][0], res[W.WMD_PATH_FUSED][0])
     a, b = res[W.WMD_PATH_PER_ITER][0].astype(np.float64), res[W.WMD_PATH_FUSED][0].astype(np.float64)
     assert np.all(np.abs(a - b) <= 2e-4 * np.abs(a) + 2e-5)
-    # long documents exceed the fused kernel's register budget: AUTO falls back per iteration
-    cp, ri, va = synth.csc_from_lists([{int(k): 1.0 / 100 for k in range(100)}], wl.cfg.V)
-    h = W.wmd_create(wl.E)
-    try:
-        W.wmd_set_targets(h, cp, ri, va)
-        d = np.empty(1, np.float32)
-        W.wmd_query(h, q, w, wl.cfg.lam, wl.cfg.iters, d)
-        assert W.wmd_get_stats(h)["last_path"] == W.WMD_PATH_PER_ITER
-    finally:
-        W.wmd_destroy(h)
+    # documents of up to 320 words run fused (one CTA per document); longer ones, and long
+    # ones under a stopping tolerance, fall back to the per-iteration path
+    for n_words, tol, want in ((100, -1.0, W.WMD_PATH_FUSED), (320, -1.0, W.WMD_PATH_FUSED),
+                               (321, -1.0, W.WMD_PATH_PER_ITER), (100, 1e-5, W.WMD_PATH_PER_ITER),
+                               (64, 1e-5, W.WMD_PATH_FUSED)):
+        cp, ri, va = synth.csc_from_lists([{int(k): 1.0 / n_words for k in range(n_words)}], wl.cfg.V)
+        h = W.wmd_create(wl.E)
+        try:
+            W.wmd_set_targets(h, cp, ri, va)
+            if tol >= 0:
+                W.wmd_set_tolerance(h, tol)
+            d = np.empty(1, np.float32)
+            W.wmd_query(h, q[:8], w[:8] / w[:8].sum(), wl.cfg.lam, wl.cfg.iters, d)
+            assert W.wmd_get_stats(h)["last_path"] == want, (n_words, tol)
+        finally:
+            W.wmd_destroy(h)
 
 
 # ------------------------------------------------------------------ fused-kernel shape grid
@@ -533,7 +539,7 @@ def test_fused_bucket_and_width_grid(W, v_r):
     wl = synth.make_workload("tweet", n_queries=0, N=10)
     V = wl.cfg.V
     lengths = [1, 2, 7, 8, 9, 15, 16, 17, 31, 32, 33, 39, 40, 41, 47, 48, 49, 63, 64] * 3
-    if v_r > 32:  # the 64-wide tables keep documents of up to 48 words in registers
+    if v_r > 32:  # the 64-wide tables keep documents of up to 48 words in one warp's registers
         lengths = [L for L in lengths if L <= 48]
     cp, ri, va = _docs_with_lengths(V, lengths, seed=v_r)
     rng = np.random.default_rng(100 + v_r)
@@ -551,6 +557,38 @@ def test_fused_bucket_and_width_grid(W, v_r):
         W.wmd_destroy(h)
     o = oracle.sinkhorn_wmd(wl.E, cp, ri, va, q, w, 10.0, 15)
     assert_parity(d, o, f"fused grid v_r={v_r}")
+
+
+@pytest.mark.parametrize("v_r", [3, 20, 33, 64, 65, 100, 128])
+def test_fused_cta_long_documents(W, v_r):
+    """One-CTA-per-document kernel (documents past the one-warp kernel's register budget): every
+    row bucket {64, 128, 192, 256: 32-row warps; 320: 40-row warps} x ld {32, 64, 128}, documents
+    at and next to each boundary up to the 320-word maximum plus a sweep of every third length,
+    mixed with short documents that stay on the one-warp kernel; AUTO must pick the fused path,
+    and the distances must match the FP64 oracle."""
+    wl = synth.make_workload("tweet", n_queries=0, N=10)
+    V = wl.cfg.V
+    lengths = [1, 5, 8, 16, 33, 48, 49, 63, 64, 65, 70, 96, 127, 128, 129, 160, 191, 192, 193, 224,
+               255, 256, 257, 290, 300, 319, 320] * 2 + list(range(50, 321, 3))
+    cp, ri, va = _docs_with_lengths(V, lengths, seed=500 + v_r)
+    rng = np.random.default_rng(600 + v_r)
+    q = np.sort(rng.choice(3000, v_r, replace=False)).astype(np.int32)
+    cnt = rng.geometric(0.6, v_r).astype(np.float64)
+    w = (cnt / cnt.sum()).astype(np.float32)
+    for lam, iters in ((10.0, 15), (1.0, 40)):
+        h = W.wmd_create(wl.E)
+        try:
+            W.wmd_set_targets(h, cp, ri, va)
+            d = np.empty(cp.shape[0] - 1, np.float32)
+            W.wmd_query(h, q, w, lam, iters, d)
+            W.wmd_sync(h)
+            st = W.wmd_get_stats(h)
+            assert st["last_path"] == W.WMD_PATH_FUSED
+            assert st["last_ld"] == max(32, 1 << (v_r - 1).bit_length())
+        finally:
+            W.wmd_destroy(h)
+        o = oracle.sinkhorn_wmd(wl.E, cp, ri, va, q, w, lam, iters)
+        assert_parity(d, o, f"fused CTA v_r={v_r} lam={lam}")
 
 
 # ------------------------------------------------------------------ NEXT-2: query batches
