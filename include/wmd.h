@@ -66,9 +66,14 @@ typedef enum {
 
 /* Execution path of the Sinkhorn loop (wmd_set_option(WMD_OPT_PATH, ...)). */
 typedef enum {
-  WMD_PATH_AUTO = 0,       /* library choice (currently WMD_PATH_FUSED when it supports the shape) */
+  WMD_PATH_AUTO = 0,       /* library choice: WMD_PATH_FUSED when it supports the shape (v_r <= 128 and
+                              every document <= 320 words; <= 64 words while a stopping tolerance is
+                              set), else WMD_PATH_PER_ITER */
   WMD_PATH_PER_ITER = 1,   /* one fused SDDMM_SpMM launch per iteration + final kernel */
-  WMD_PATH_FUSED = 2       /* all iterations + final in one launch, per-document state on chip */
+  WMD_PATH_FUSED = 2       /* all iterations + final in one launch per length bucket, per-document
+                              state on chip (one warp per document up to 64 words, one CTA per
+                              document up to 320); WMD_ERR_INVALID_ARGUMENT if the shape is outside
+                              the limits above */
 } wmd_path;
 
 typedef enum {
@@ -91,7 +96,7 @@ typedef struct {
   int64_t fallback_docs;     /* documents recomputed in FP64, summed over queries (updated by wmd_sync) */
   int64_t flagged_docs;      /* documents of the last query flagged in FP32 (updated by wmd_sync) */
   int32_t last_v_r;
-  int32_t last_ld;           /* row width (floats) of the K~ / M tables: v_r rounded up to 8 (per-iteration path) or to 8/16/32/64 (fused path) */
+  int32_t last_ld;           /* row width (floats) of the K~ / M tables: v_r rounded up to 8 (per-iteration path) or to 8/16/32/64/128 (fused path; at least 32 when a document needs the one-CTA kernel) */
   int32_t last_path;         /* wmd_path actually used by the last query */
   int32_t timing_valid;      /* 1 if the *_ms fields below are populated (WMD_OPT_TIMING) */
   double build_ms;           /* distance + kernel build (step a2), summed over queries */

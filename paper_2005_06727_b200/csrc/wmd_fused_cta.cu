@@ -182,56 +182,47 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W>()) sinkhorn_cta_
       c_own[o] = v_ok[o] ? cents[orow[o]] : 0.f;
       m_own[o] = v_ok[o] ? __ldg(Mx + (size_t)ents[orow[o]] * P + LD) : 0.f;
     }
-    // ---- block tile: D, column minima mu (per warp, then over the CTA), beta = alpha mu
+    // ---- block tile: D, column minima mu (per warp, then over the CTA), beta = alpha mu, Kh
     load_D(n);
     float uo[NQ];  // uh of the owned columns CW b + 4g + a; the slots are rebuilt by shuffles
     bool und;
     {
-      float mu[CW];
+      // per-warp column minima (one column at a time: the block alone fills the registers)
 #pragma unroll
       for (int c = 0; c < CW; ++c) {
-        mu[c] = K[0][c];
+        float m = K[0][c];
 #pragma unroll
-        for (int s = 1; s < RW; ++s) mu[c] = fminf(mu[c], K[s][c]);
-        mu[c] = fminf(mu[c], shx(mu[c], 8));
-        mu[c] = fminf(mu[c], shx(mu[c], 16));
-      }
-      if (a == 0) {
-#pragma unroll
-        for (int q = 0; q < CW / 4; ++q)
-          *reinterpret_cast<float4*>(colpart + warp * CP + CW * b + 4 * q) =
-              make_float4(mu[4 * q], mu[4 * q + 1], mu[4 * q + 2], mu[4 * q + 3]);
+        for (int s = 1; s < RW; ++s) m = fminf(m, K[s][c]);
+        m = fminf(m, shx(m, 8));
+        m = fminf(m, shx(m, 16));
+        if (a == 0) colpart[warp * CP + CW * b + c] = m;
       }
       __syncthreads();
+      if (warp == 0) {  // CTA minima: beta = alpha mu (gamma = 0)
+        for (int col = lane; col < LD; col += 32) {
+          float m = colpart[col];
 #pragma unroll
-      for (int w = 0; w < W; ++w) {
-#pragma unroll
-        for (int q = 0; q < CW / 4; ++q) {
-          const float4 t = *reinterpret_cast<const float4*>(colpart + w * CP + CW * b + 4 * q);
-          mu[4 * q] = fminf(mu[4 * q], t.x); mu[4 * q + 1] = fminf(mu[4 * q + 1], t.y);
-          mu[4 * q + 2] = fminf(mu[4 * q + 2], t.z); mu[4 * q + 3] = fminf(mu[4 * q + 3], t.w);
+          for (int w = 1; w < W; ++w) m = fminf(m, colpart[w * CP + col]);
+          betal[col] = alpha * m;
         }
       }
-#pragma unroll
-      for (int c = 0; c < CW; ++c) mu[c] = alpha * mu[c];  // beta (gamma = 0)
-      if (warp == 0 && a == 0) {
-#pragma unroll
-        for (int c = 0; c < CW; ++c) betal[CW * b + c] = mu[c];
-      }
+      __syncthreads();
       bool flushed = false;
 #pragma unroll
-      for (int s = 0; s < RW; ++s) {
+      for (int c = 0; c < CW; ++c) {
+        const bool real = CW * b + c < v_r;
+        const float bc = betal[CW * b + c];
 #pragma unroll
-        for (int c = 0; c < CW; ++c) {
-          const bool real = CW * b + c < v_r;
+        for (int s = 0; s < RW; ++s) {
           const float dd = K[s][c];
-          const float kx = ex2_ftz(fmaf(-alpha, dd, mu[c]));
+          const float kx = ex2_ftz(fmaf(-alpha, dd, bc));
           flushed |= real && kx < FLT_MIN && dd != FLT_MAX;
           K[s][c] = real ? kx : (dd != FLT_MAX ? 1.f : 0.f);  // padded columns: 1 on real rows
         }
-        to_slots<CW>(K[s], a);
       }
-      und = __syncthreads_or(flushed);  // also: the minima are read, betal is published
+#pragma unroll
+      for (int s = 0; s < RW; ++s) to_slots<CW>(K[s], a);
+      und = __syncthreads_or(flushed);  // also: the minima are read
     }
     // uh0 = v_r 2^-beta (x0 = 1 / v_r, in the rescaled variables) of the owned columns
 #pragma unroll
@@ -502,9 +493,15 @@ void launch_cta_range(const int4* sdoc, const Entry* ent, int64_t p0, int64_t p1
                                                              itd, dist, flags, fl, fc);
 }
 
-// Row buckets: W warps of 32 rows (64 ... 256), then 8 warps of 40 rows (320).
+// Row buckets (rows = W x (32 + 4 TW)): 2 / 4 warps of 32 rows (64, 128), 4 warps of 48 rows
+// (192: two CTAs per SM, where 6 warps of 32 rows would leave one 6-warp CTA per SM), 8 warps
+// of 32 rows (256) and of 40 rows (320).
 struct CtaBucket { int rows, w, tw; };
+#ifdef WMD_CTA_192_W6
 constexpr CtaBucket kCta[] = {{64, 2, 0}, {128, 4, 0}, {192, 6, 0}, {256, 8, 0}, {320, 8, 2}};
+#else
+constexpr CtaBucket kCta[] = {{64, 2, 0}, {128, 4, 0}, {192, 4, 4}, {256, 8, 0}, {320, 8, 2}};
+#endif
 constexpr int kNumCta = 5;
 
 template <int CW>
@@ -513,7 +510,12 @@ void dispatch_cta(int wi, const int4* sdoc, const Entry* ent, int64_t p0, int64_
                   int32_t* fl, int32_t* fc, cudaStream_t st) {
   switch (wi) {
 #define C_(I, W, TW) case I: launch_cta_range<CW, W, TW>(sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, itd, dist, flags, fl, fc, st); break;
-    C_(0, 2, 0) C_(1, 4, 0) C_(2, 6, 0) C_(3, 8, 0) C_(4, 8, 2)
+    C_(0, 2, 0) C_(1, 4, 0) C_(3, 8, 0) C_(4, 8, 2)
+#ifdef WMD_CTA_192_W6
+    C_(2, 6, 0)
+#else
+    C_(2, 4, 4)
+#endif
 #undef C_
     default: break;
   }

@@ -123,3 +123,28 @@ def test_create_rejects_bad_arguments_before_touching_cuda(W):
     with pytest.raises(W.WmdError) as e:
         W.wmd_create(E, 4, 0, 0)
     assert e.value.status == W.WMD_ERR_INVALID_ARGUMENT
+
+
+def test_fused_kernels_keep_the_block_in_registers(W):
+    """Resource check of the built fused kernels (ptxas -v of the in-tree build): every
+    instance keeps its Kh block in registers (at most 128 B of spill, all in the once-per-document
+    setup; a heavily spilling build faulted), and no kernel calls the IEEE-division
+    slow path on the device."""
+    import subprocess
+    from paper_2005_06727_b200 import build
+    logs = {s: os.path.join(build.PKG, "build", s + ".ptxas.txt") for s in ("wmd_fused.cu", "wmd_fused_cta.cu")}
+    if not all(os.path.exists(p) for p in logs.values()):
+        build.build(force=True)
+    checked = 0
+    for src, path in logs.items():
+        txt = open(path).read()
+        for m in re.finditer(r"Compiling entry function '(\w+)'.*?(\d+) bytes spill stores", txt, re.S):
+            name, spill = m.group(1), int(m.group(2))
+            if "sinkhorn" in name:
+                checked += 1
+                assert spill <= 128, (src, name, spill)
+    assert checked >= 20
+    obj = os.path.join(build.PKG, "build", "wmd_fused_cta.cu.o")
+    sass = subprocess.run(["cuobjdump", "-sass", obj], capture_output=True, text=True).stdout
+    if sass:
+        assert "slowpath" not in sass and " CALL" not in sass
