@@ -66,6 +66,9 @@ struct Shape {
   static constexpr int REGS = RW * CW;
 };
 
+#ifndef WMD_FUSED_DOCS_PER_WARP_SMALL  // documents per warp in the <= 16-row buckets
+#define WMD_FUSED_DOCS_PER_WARP_SMALL 1
+#endif
 #ifndef WMD_FUSED_DOCS_PER_WARP
 #define WMD_FUSED_DOCS_PER_WARP 1
 #endif
@@ -450,7 +453,8 @@ void launch_fused_range(const int4* sdoc, const Entry* ent, int64_t p0, int64_t 
   if (tol >= 0.f)
     launch_fused_range_t<CW, NT, TW, true, 1>(sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, tol, itd, dist, flags, fl, fc, st);
   else
-    launch_fused_range_t<CW, NT, TW, false, WMD_FUSED_DOCS_PER_WARP>(sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, tol, itd, dist, flags, fl, fc, st);
+    launch_fused_range_t<CW, NT, TW, false, (NT == 0 ? WMD_FUSED_DOCS_PER_WARP_SMALL : WMD_FUSED_DOCS_PER_WARP)>(
+        sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, tol, itd, dist, flags, fl, fc, st);
 }
 
 // Length buckets (rows covered: 8, 16, 32, 40, 48, 64) over the length-sorted order.
@@ -493,9 +497,9 @@ int fused_ld(int v_r, int64_t max_doc_nnz, bool conv) {
   while (ld < v_r) ld *= 2;
   if (ld > 128) return 0;
   if (max_doc_nnz <= warp_max_rows(ld)) return ld;
-  // longer documents: one CTA per document (wmd_fused_cta.cu; fixed iteration count, ld >= 32)
+  // longer documents: one CTA per document (wmd_fused_cta.cu; fixed iteration count)
   if (conv || max_doc_nnz > cta_max_rows()) return 0;
-  return std::max(ld, 32);
+  return cta_ld(v_r);
 }
 
 void launch_sinkhorn_fused(const int4* sdoc, const Entry* ent, int64_t N,

@@ -1,18 +1,21 @@
 // wmd_fused_cta.cu — NEXT-1 for long documents: all Sinkhorn iterations and the final step of a
-// document of up to 32 W words in ONE CTA of W warps, the document's Kh block in registers.
+// document of up to 320 words in ONE CTA of W warps, the document's Kh block in registers.
 //
 // Same method as the one-warp-per-document kernel (wmd_fused.cu: doc-local two-sided rescale
 // Kh = 2^(-alpha D + beta_i + gamma_e), power-of-two gauge, FP32 range certificate, final step
 // with D recovered from Kh), for the shapes that do not fit one warp's registers (the Long
-// config: 50-300-word documents against 100 query words). Warp w holds rows [32w, 32w + 32) of
-// the block as the 2-D lane tile of wmd_tile.cuh (8 rows x CW columns per lane, LD = 8 CW):
+// config: 50-300-word documents against 100 query words). Warp w holds rows [RPW w, RPW (w+1))
+// of the block (RPW = 32, or 32 + 4 TW with a tail) as a 2-D lane tile, lane = 8a + b: row slots
+// as in wmd_tile.cuh, and CW = 4Q + R columns per lane, LD = 8 CW: Q XOR-permuted quads (quad g
+// of lane b: columns 32g + 4b + j, slot 4g + t holding j = t ^ a) and R plain columns
+// (32Q + Rb + r), so LD need not be a power of two (v_r = 100: LD = 104, not 128).
 //   SDDMM  s = Kh uh    : warp-local (row partials, transpose-reduce over the b-lanes)
 //   SpMM   acc = Kh^T vh: per-warp column partials (transpose-reduce over the a-lanes) to shared
 //                         memory; ONE barrier; then every warp sums the W partials of all LD
-//                         columns itself (LD / 32 per lane, vector reads), so uh = r / acc, its
-//                         gauge and the range checks are computed redundantly and bit-identically
-//                         by every warp (no second barrier), and each lane gets its CW columns by
-//                         three xor-shuffles per column quad.
+//                         columns itself (Q + R per lane), so uh = r / acc, its gauge and the
+//                         range checks are computed redundantly and bit-identically by every
+//                         warp (no second barrier); each lane gets its quad slots by three
+//                         xor-shuffles per quad.
 // The column partials are double-buffered by pass parity, so one barrier per iteration orders
 // everything. No global memory traffic inside the loop.
 //
@@ -47,47 +50,70 @@ constexpr int kMaxAnchors = WMD_CTA_MAX_ANCHORS;
 
 template <int CW, int W, int TW>
 struct CtaShape {
-  static constexpr int LD = 8 * CW;
-  static constexpr int NQ = CW / 4;            // columns per lane in the column step (LD / 32)
+  static constexpr int Q = CW / 4;             // XOR-permuted column quads per lane
+  static constexpr int R = CW % 4;             // plain columns per lane
+  static constexpr int LD = 8 * CW;            // = 32 Q + 8 R
   static constexpr int RPW = 32 + 4 * TW;      // rows per warp: a 32-row tile + 4 TW tail rows
   static constexpr int RW = 8 + TW;            // row slots per lane
   static constexpr int NOWN = TW ? 2 : 1;      // own rows per lane after the row reduce
   static constexpr int TSH = TW == 4 ? 1 : 2;  // tail row slot t of lane b: 32 + TW a + (t ^ (b >> TSH))
   static constexpr int ROWS = W * RPW;
   static constexpr int P = LD + 4;             // row pitch of Mx
-  static constexpr int CP = LD + 4;            // pitch of one warp's column partials (+ its vmax)
+  // one warp's column partials: quads lane-major (4 floats per lane), then the 8R plain
+  // columns, then the warp's vmax
+  static constexpr int CREM = 128, CVMAX = 128 + 8 * R, CP = CVMAX + 4;
   static constexpr int SMEM_FLOATS = 2 * W * CP + LD + 2 * ROWS + W + 4;
 };
 
-// Resident warps per SM the register budget is written for: 12 (168 registers per thread) for
-// CW <= 8; 8 (255 registers) for CW = 16, whose Kh block alone takes 128-160 registers per
-// thread (at 168 it spills, and the spilling build faulted on some shapes: DESIGN.md §5).
-#ifndef WMD_CTA_WARPS_PER_SM
-#define WMD_CTA_WARPS_PER_SM 12
-#endif
-#ifndef WMD_CTA_WARPS_PER_SM_16
-#define WMD_CTA_WARPS_PER_SM_16 8
-#endif
-template <int CW, int W>
+// Natural column of natural slot c (Mx order: query row i at column i); slot column of register
+// slot c (quads permuted by a).
+template <int CW>
+__device__ __forceinline__ int nat_col(int c, int b) {
+  constexpr int Q = CW / 4, R = CW % 4;
+  return c < 4 * Q ? 32 * (c >> 2) + 4 * b + (c & 3) : 32 * Q + R * b + (c - 4 * Q);
+}
+template <int CW>
+__device__ __forceinline__ int slot_col(int c, int a, int b) {
+  constexpr int Q = CW / 4, R = CW % 4;
+  return c < 4 * Q ? 32 * (c >> 2) + 4 * b + ((c & 3) ^ a) : 32 * Q + R * b + (c - 4 * Q);
+}
+// natural -> slot order (the quads; the plain columns stay)
+template <int CW>
+__device__ __forceinline__ void quads_to_slots(float (&x)[CW], int a) {
+  const bool s1 = a & 1, s2 = a & 2;
+#pragma unroll
+  for (int q = 0; q < CW / 4; ++q) {
+    float* y = x + 4 * q;
+    float t0 = s1 ? y[1] : y[0], t1 = s1 ? y[0] : y[1];
+    float t2 = s1 ? y[3] : y[2], t3 = s1 ? y[2] : y[3];
+    y[0] = s2 ? t2 : t0; y[2] = s2 ? t0 : t2;
+    y[1] = s2 ? t3 : t1; y[3] = s2 ? t1 : t3;
+  }
+}
+
+// Resident warps per SM the register budget is written for: 12 (168 registers per thread) when
+// the block takes at most 96 registers per thread, else 8 (255): at 168 such instances spill,
+// and a spilling build faulted on some shapes.
+template <int CW, int W, int TW>
 constexpr int cta_min_blocks() {
-  constexpr int wps = CW >= 16 ? WMD_CTA_WARPS_PER_SM_16 : WMD_CTA_WARPS_PER_SM;
+  constexpr int wps = (8 + TW) * CW > 96 ? 8 : 12;
   return W < wps ? wps / W : 1;
 }
 
 template <int CW, int W, int TW>
-__global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W>()) sinkhorn_cta_kernel(
+__global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W, TW>()) sinkhorn_cta_kernel(
     const int4* __restrict__ sdoc, const Entry* __restrict__ ent, int64_t pos0, int64_t pos1,
     const float* __restrict__ Mx, int v_r, const float* __restrict__ rpad, float lambda, int iters,
     int32_t* __restrict__ iters_doc, float* __restrict__ dist, uint8_t* __restrict__ flags,
     int32_t* __restrict__ flagged_list, int32_t* __restrict__ flagged_count) {
   using S = CtaShape<CW, W, TW>;
-  constexpr int LD = S::LD, NQ = S::NQ, P = S::P, CP = S::CP, RW = S::RW, RPW = S::RPW;
+  constexpr int LD = S::LD, Q = S::Q, R = S::R, P = S::P, CP = S::CP, RW = S::RW, RPW = S::RPW;
   constexpr int NOWN = S::NOWN, TSH = S::TSH, ROWS = S::ROWS, NT = 32 * W;
   constexpr int EPT = (ROWS + NT - 1) / NT;    // entries each thread prefetches
-  static_assert(CW % 4 == 0, "column quads");
+  static_assert(Q >= 1 && Q <= 4, "1 to 4 column quads per lane (LD <= 128)");
   static_assert(TW == 0 || TW == 2 || TW == 4, "tail width");
   extern __shared__ __align__(16) float csm[];
-  float* colpart = csm;                                    // [2][W][CP]; [.][w][LD] = warp's vmax
+  float* colpart = csm;                                    // [2][W][CP]
   float* betal = colpart + 2 * W * CP;                     // [LD] column shifts beta (log2 units)
   int* ents = reinterpret_cast<int*>(betal + LD);          // [ROWS] vocabulary row of each word
   float* cents = reinterpret_cast<float*>(ents + ROWS);    // [ROWS] its c
@@ -99,10 +125,13 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W>()) sinkhorn_cta_
   const float alpha = lambda * kLog2eC;
   const float ia = -rcp_fast(alpha);  // (approximate: no IEEE-division slow-path call)
   const float kv_s = (float)v_r * kUnderC;
-  // column step: this lane owns columns CW*b + 4g + a (g < NQ), the ones reduce_cols leaves it
-  float r_own[NQ];
+  // column step: this lane owns quad columns 32g + 4b + a (the ones reduce_cols leaves it) and,
+  // with its three a-partners, the plain columns 32Q + Rb + r
+  float r_own[Q], r_rem[R > 0 ? R : 1];
 #pragma unroll
-  for (int g = 0; g < NQ; ++g) r_own[g] = __ldg(rpad + CW * b + 4 * g + a);  // zero beyond v_r
+  for (int g = 0; g < Q; ++g) r_own[g] = __ldg(rpad + 32 * g + 4 * b + a);  // zero beyond v_r
+#pragma unroll
+  for (int r = 0; r < R; ++r) r_rem[r] = __ldg(rpad + 32 * Q + R * b + r);
   // own rows after the row reduce: row0 + lane, and the tail row row0 + 32 + TW a + (b >> TSH)
   int orow[NOWN];
   orow[0] = row0 + lane;
@@ -151,10 +180,12 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W>()) sinkhorn_cta_
       const float* row = Mx + (size_t)(ok ? ents[e] : 0) * P;
       float x[CW];
 #pragma unroll
-      for (int q = 0; q < CW / 4; ++q) {
-        const float4 t = __ldg(reinterpret_cast<const float4*>(row + CW * b) + q);
+      for (int q = 0; q < Q; ++q) {
+        const float4 t = __ldg(reinterpret_cast<const float4*>(row + 32 * q + 4 * b));
         x[4 * q] = t.x; x[4 * q + 1] = t.y; x[4 * q + 2] = t.z; x[4 * q + 3] = t.w;
       }
+#pragma unroll
+      for (int r = 0; r < R; ++r) x[4 * Q + r] = __ldg(row + 32 * Q + R * b + r);
       const float me = __ldg(row + LD);
 #pragma unroll
       for (int c = 0; c < CW; ++c) K[s][c] = ok ? x[c] - me : FLT_MAX;
@@ -184,7 +215,7 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W>()) sinkhorn_cta_
     }
     // ---- block tile: D, column minima mu (per warp, then over the CTA), beta = alpha mu, Kh
     load_D(n);
-    float uo[NQ];  // uh of the owned columns CW b + 4g + a; the slots are rebuilt by shuffles
+    float uo[Q], ur[R > 0 ? R : 1];  // uh of the owned quad columns and of the plain columns
     bool und;
     {
       // per-warp column minima (one column at a time: the block alone fills the registers)
@@ -195,7 +226,7 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W>()) sinkhorn_cta_
         for (int s = 1; s < RW; ++s) m = fminf(m, K[s][c]);
         m = fminf(m, shx(m, 8));
         m = fminf(m, shx(m, 16));
-        if (a == 0) colpart[warp * CP + CW * b + c] = m;
+        if (a == 0) colpart[warp * CP + nat_col<CW>(c, b)] = m;
       }
       __syncthreads();
       if (warp == 0) {  // CTA minima: beta = alpha mu (gamma = 0)
@@ -210,8 +241,9 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W>()) sinkhorn_cta_
       bool flushed = false;
 #pragma unroll
       for (int c = 0; c < CW; ++c) {
-        const bool real = CW * b + c < v_r;
-        const float bc = betal[CW * b + c];
+        const int col = nat_col<CW>(c, b);
+        const bool real = col < v_r;
+        const float bc = betal[col];
 #pragma unroll
         for (int s = 0; s < RW; ++s) {
           const float dd = K[s][c];
@@ -221,14 +253,19 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W>()) sinkhorn_cta_
         }
       }
 #pragma unroll
-      for (int s = 0; s < RW; ++s) to_slots<CW>(K[s], a);
+      for (int s = 0; s < RW; ++s) quads_to_slots<CW>(K[s], a);
       und = __syncthreads_or(flushed);  // also: the minima are read
     }
-    // uh0 = v_r 2^-beta (x0 = 1 / v_r, in the rescaled variables) of the owned columns
+    // uh0 = v_r 2^-beta (x0 = 1 / v_r, in the rescaled variables)
 #pragma unroll
-    for (int g = 0; g < NQ; ++g) {
-      const int col = CW * b + 4 * g + a;
+    for (int g = 0; g < Q; ++g) {
+      const int col = 32 * g + 4 * b + a;
       uo[g] = col < v_r ? (float)v_r * ex2_ftz(-betal[col]) : 0.f;
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int col = 32 * Q + R * b + r;
+      ur[r] = col < v_r ? (float)v_r * ex2_ftz(-betal[col]) : 0.f;
     }
     stage2();  // the next document's entries
 
@@ -241,11 +278,10 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W>()) sinkhorn_cta_
     float v_own[NOWN], s_own[NOWN];
     int it = 0;
     for (int pass = 0;; ++pass) {
-      // SDDMM (warp-local)
-      // (one column quad of uh live at a time: its 4 slots come from lanes ^ 0, 8, 16, 24)
+      // SDDMM (warp-local; one quad of uh live at a time: its slots come from lanes ^ 0, 8, 16, 24)
       float p[RW];
 #pragma unroll
-      for (int g = 0; g < NQ; ++g) {
+      for (int g = 0; g < Q; ++g) {
         float u4[4];
         u4[0] = uo[g];
 #pragma unroll
@@ -257,6 +293,11 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W>()) sinkhorn_cta_
           for (int t = 1; t < 4; ++t) acc = fmaf(K[s][4 * g + t], u4[t], acc);
           p[s] = acc;
         }
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+#pragma unroll
+        for (int s = 0; s < RW; ++s) p[s] = fmaf(K[s][4 * Q + r], ur[r], p[s]);
       }
       reduce_rows<1, TW>(p);
       bool sfail = false;
@@ -272,13 +313,14 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W>()) sinkhorn_cta_
       float* cp = colpart + (pass & 1) * W * CP;
       if (!last) {
         const uint32_t vmax_w = __reduce_max_sync(kFull, vmax_l);
-        // SpMM: this warp's column partials
+        // SpMM: this warp's column partials, one quad at a time, then its transpose-reduce
         float vs[RW];
         rows_to_slots(v_own, vs);
-        // (one column quad at a time: partials, then its transpose-reduce over the a-lanes)
-        float qo[NQ];
+        float qo[4];
 #pragma unroll
-        for (int g = 0; g < NQ; ++g) {
+        for (int g = 0; g < 4; ++g) qo[g] = 0.f;
+#pragma unroll
+        for (int g = 0; g < Q; ++g) {
           float q[4];
 #pragma unroll
           for (int t = 0; t < 4; ++t) {
@@ -290,60 +332,74 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W>()) sinkhorn_cta_
           reduce_cols<4>(q);
           qo[g] = q[0];
         }
-        // lane-major layout: this lane's NQ columns are contiguous (read back by the same lane)
-        if constexpr (NQ == 4) {
-          *reinterpret_cast<float4*>(cp + warp * CP + 4 * lane) = make_float4(qo[0], qo[1], qo[2], qo[3]);
-        } else if constexpr (NQ == 2) {
-          *reinterpret_cast<float2*>(cp + warp * CP + 2 * lane) = make_float2(qo[0], qo[1]);
-        } else {
-          cp[warp * CP + lane] = qo[0];
+        // lane-major quads: this lane's columns are contiguous (read back by the same lane)
+        *reinterpret_cast<float4*>(cp + warp * CP + 4 * lane) = make_float4(qo[0], qo[1], qo[2], qo[3]);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          float q0 = K[0][4 * Q + r] * vs[0];
+#pragma unroll
+          for (int s = 1; s < RW; ++s) q0 = fmaf(K[s][4 * Q + r], vs[s], q0);
+          q0 += shx(q0, 16);
+          q0 += shx(q0, 8);
+          if (a == 0) cp[warp * CP + S::CREM + R * b + r] = q0;
         }
-        if (lane == 0) cp[warp * CP + LD] = __uint_as_float(vmax_w);
+        if (lane == 0) cp[warp * CP + S::CVMAX] = __uint_as_float(vmax_w);
       }
       bool fail = __syncthreads_or(sfail);
-      float un[NQ];
+      float un[Q], unr[R > 0 ? R : 1];
 #pragma unroll
-      for (int g = 0; g < NQ; ++g) un[g] = 0.f;
+      for (int g = 0; g < Q; ++g) un[g] = 0.f;
+#pragma unroll
+      for (int r = 0; r < R; ++r) unr[r] = 0.f;
       if (!fail && !last) {
         // column step, redundantly in every warp: acc = sum of the W warps' partials
-        float acc[NQ];
+        float acc[4], accr[R > 0 ? R : 1];
 #pragma unroll
-        for (int g = 0; g < NQ; ++g) acc[g] = 0.f;
+        for (int g = 0; g < 4; ++g) acc[g] = 0.f;
+#pragma unroll
+        for (int r = 0; r < R; ++r) accr[r] = 0.f;
 #pragma unroll 2
         for (int w = 0; w < W; ++w) {  // (not fully unrolled: bounds the loads in flight)
-          if constexpr (NQ == 4) {
-            const float4 t = *reinterpret_cast<const float4*>(cp + w * CP + 4 * lane);
-            acc[0] += t.x; acc[1] += t.y; acc[2] += t.z; acc[3] += t.w;
-          } else if constexpr (NQ == 2) {
-            const float2 t = *reinterpret_cast<const float2*>(cp + w * CP + 2 * lane);
-            acc[0] += t.x; acc[1] += t.y;
-          } else {
-            acc[0] += cp[w * CP + lane];
-          }
+          const float4 t = *reinterpret_cast<const float4*>(cp + w * CP + 4 * lane);
+          acc[0] += t.x; acc[1] += t.y; acc[2] += t.z; acc[3] += t.w;
+#pragma unroll
+          for (int r = 0; r < R; ++r) accr[r] += cp[w * CP + S::CREM + R * b + r];
         }
         bool cfail = false;
         if (und) {  // acc-side certificate: flushed entries move acc_i by < n vmax 2^-126
           float vmax = 0.f;
 #pragma unroll
-          for (int w = 0; w < W; ++w) vmax = fmaxf(vmax, cp[w * CP + LD]);
+          for (int w = 0; w < W; ++w) vmax = fmaxf(vmax, cp[w * CP + S::CVMAX]);
           const float vcap = (float)n * vmax * kUnderC;
 #pragma unroll
-          for (int g = 0; g < NQ; ++g) cfail |= vcap > acc[g];
+          for (int g = 0; g < Q; ++g) cfail |= vcap > acc[g];
+#pragma unroll
+          for (int r = 0; r < R; ++r) cfail |= vcap > accr[r];
         }
         uint32_t um = 0u;
 #pragma unroll
-        for (int g = 0; g < NQ; ++g) {
+        for (int g = 0; g < Q; ++g) {
           un[g] = r_own[g] * rcp_fast(acc[g]);
           um = max(um, __float_as_uint(un[g]));
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          unr[r] = r_rem[r] * rcp_fast(accr[r]);
+          um = max(um, __float_as_uint(unr[r]));
         }
         // gauge: max uh -> [1, 2) by an exact power of two (identical in every warp)
         const uint32_t umax_b = __reduce_max_sync(kFull, um);
         const float sc = __uint_as_float((254u - min(umax_b >> 23, 253u)) << 23);
         cfail |= umax_b > 0x7f7fffffu;
 #pragma unroll
-        for (int g = 0; g < NQ; ++g) {
+        for (int g = 0; g < Q; ++g) {
           un[g] *= sc;
-          cfail |= CW * b + 4 * g + a < v_r && !(un[g] >= FLT_MIN);
+          cfail |= 32 * g + 4 * b + a < v_r && !(un[g] >= FLT_MIN);
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          unr[r] *= sc;
+          cfail |= 32 * Q + R * b + r < v_r && !(unr[r] >= FLT_MIN);
         }
         fail = __any_sync(kFull, cfail);  // warp-uniform, and the same in every warp
       }
@@ -354,20 +410,29 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W>()) sinkhorn_cta_
       if (fail) {
         // ---- re-anchor (CTA-uniform branch): beta += log2 uh, Kh recomputed from D
         ++anchors;
-        float bown[NQ];  // new beta of the owned columns (the same in every warp)
+        float bown[Q], brem[R > 0 ? R : 1];  // new beta of this lane's columns (same in every warp)
 #pragma unroll
-        for (int g = 0; g < NQ; ++g) {
-          const float bo = betal[CW * b + 4 * g + a];
+        for (int g = 0; g < Q; ++g) {
+          const float bo = betal[32 * g + 4 * b + a];
           bown[g] = uo[g] > 0.f ? bo + lg2_approx(uo[g]) : bo;
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const float bo = betal[32 * Q + R * b + r];
+          brem[r] = ur[r] > 0.f ? bo + lg2_approx(ur[r]) : bo;
         }
         __syncthreads();  // every warp has read betal
         if (warp == 0) {
 #pragma unroll
-          for (int g = 0; g < NQ; ++g) betal[CW * b + 4 * g + a] = bown[g];
+          for (int g = 0; g < Q; ++g) betal[32 * g + 4 * b + a] = bown[g];
+          if (a == 0) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) betal[32 * Q + R * b + r] = brem[r];
+          }
         }
         load_D(n);
 #pragma unroll
-        for (int s = 0; s < RW; ++s) to_slots<CW>(K[s], a);
+        for (int s = 0; s < RW; ++s) quads_to_slots<CW>(K[s], a);
         __syncthreads();  // the new betal is published
         // L = -alpha D + beta; gamma_e = -(max of L over the real columns of row e)
         float rmax[RW];
@@ -375,7 +440,7 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W>()) sinkhorn_cta_
         for (int s = 0; s < RW; ++s) rmax[s] = -FLT_MAX;
 #pragma unroll
         for (int c = 0; c < CW; ++c) {
-          const int col = col_of<CW>(c, a, b);
+          const int col = slot_col<CW>(c, a, b);
           const float bc = betal[col];
 #pragma unroll
           for (int s = 0; s < RW; ++s) {
@@ -396,14 +461,16 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W>()) sinkhorn_cta_
           const bool rowok = row0 + row_of<1, TW>(s, a, b) < n;
 #pragma unroll
           for (int c = 0; c < CW; ++c) {
-            const bool real = col_of<CW>(c, a, b) < v_r;
+            const bool real = slot_col<CW>(c, a, b) < v_r;
             const float kx = ex2_ftz(K[s][c] + gs[s]);
             flushed |= real && rowok && kx < FLT_MIN;
             K[s][c] = rowok ? (real ? kx : 1.f) : 0.f;
           }
         }
 #pragma unroll
-        for (int g = 0; g < NQ; ++g) uo[g] = CW * b + 4 * g + a < v_r ? 1.f : 0.f;
+        for (int g = 0; g < Q; ++g) uo[g] = 32 * g + 4 * b + a < v_r ? 1.f : 0.f;
+#pragma unroll
+        for (int r = 0; r < R; ++r) ur[r] = 32 * Q + R * b + r < v_r ? 1.f : 0.f;
         umax_k = kv_s;
         und = __syncthreads_or(flushed);  // also: betal published
         continue;                         // redo this pass in the new scale
@@ -412,7 +479,9 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W>()) sinkhorn_cta_
       ++it;
       umax_k = 2.f * kv_s;
 #pragma unroll
-      for (int g = 0; g < NQ; ++g) uo[g] = un[g];
+      for (int g = 0; g < Q; ++g) uo[g] = un[g];
+#pragma unroll
+      for (int r = 0; r < R; ++r) ur[r] = unr[r];
     }
     // ---- final step: D = (beta + gamma - log2 Kh) / alpha (PAPER.md:64-66 with M = m + D)
     {
@@ -420,21 +489,15 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W>()) sinkhorn_cta_
 #pragma unroll
       for (int s = 0; s < RW; ++s) p[s] = 0.f;
 #pragma unroll
-      for (int g = 0; g < NQ; ++g) {
-        float u4[4], ub4[4];
-        u4[0] = uo[g];
-#pragma unroll
-        for (int t = 1; t < 4; ++t) u4[t] = shx(uo[g], 8 * t);
-#pragma unroll
-        for (int t = 0; t < 4; ++t) ub4[t] = u4[t] * (-ia * betal[col_of<CW>(4 * g + t, a, b)]);  // uh beta / alpha
+      for (int c = 0; c < CW; ++c) {
+        // uh of slot c, and uh beta / alpha
+        const float uc = c < 4 * Q ? ((c & 3) == 0 ? uo[c >> 2] : shx(uo[c >> 2], 8 * (c & 3))) : ur[c - 4 * Q];
+        const float ub = uc * (-ia * betal[slot_col<CW>(c, a, b)]);
 #pragma unroll
         for (int s = 0; s < RW; ++s) {
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const float k = K[s][4 * g + t];
-            const float kl = k > 0.f ? k * lg2_approx(k) : 0.f;
-            p[s] = fmaf(k, ub4[t], fmaf(kl * ia, u4[t], p[s]));
-          }
+          const float k = K[s][c];
+          const float kl = k > 0.f ? k * lg2_approx(k) : 0.f;
+          p[s] = fmaf(k, ub, fmaf(kl * ia, uc, p[s]));
         }
       }
       reduce_rows<1, TW>(p);
@@ -497,11 +560,7 @@ void launch_cta_range(const int4* sdoc, const Entry* ent, int64_t p0, int64_t p1
 // (192: two CTAs per SM, where 6 warps of 32 rows would leave one 6-warp CTA per SM), 8 warps
 // of 32 rows (256) and of 40 rows (320).
 struct CtaBucket { int rows, w, tw; };
-#ifdef WMD_CTA_192_W6
-constexpr CtaBucket kCta[] = {{64, 2, 0}, {128, 4, 0}, {192, 6, 0}, {256, 8, 0}, {320, 8, 2}};
-#else
 constexpr CtaBucket kCta[] = {{64, 2, 0}, {128, 4, 0}, {192, 4, 4}, {256, 8, 0}, {320, 8, 2}};
-#endif
 constexpr int kNumCta = 5;
 
 template <int CW>
@@ -510,12 +569,7 @@ void dispatch_cta(int wi, const int4* sdoc, const Entry* ent, int64_t p0, int64_
                   int32_t* fl, int32_t* fc, cudaStream_t st) {
   switch (wi) {
 #define C_(I, W, TW) case I: launch_cta_range<CW, W, TW>(sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, itd, dist, flags, fl, fc, st); break;
-    C_(0, 2, 0) C_(1, 4, 0) C_(3, 8, 0) C_(4, 8, 2)
-#ifdef WMD_CTA_192_W6
-    C_(2, 6, 0)
-#else
-    C_(2, 4, 4)
-#endif
+    C_(0, 2, 0) C_(1, 4, 0) C_(2, 4, 4) C_(3, 8, 0) C_(4, 8, 2)
 #undef C_
     default: break;
   }
@@ -524,6 +578,17 @@ void dispatch_cta(int wi, const int4* sdoc, const Entry* ent, int64_t p0, int64_
 }  // namespace
 
 int cta_max_rows() { return kCta[kNumCta - 1].rows; }
+
+// Row width of the one-CTA kernel's tables for a query of v_r rows: 32 or 64 for v_r <= 64
+// (shared with the one-warp kernel's power-of-two widths), else 8 CW with CW in {10, 12, 13, 16}
+// (LD = 80, 96, 104, 128: at v_r = 100, 4 padded columns instead of 28).
+int cta_ld(int v_r) {
+  if (v_r <= 32) return 32;
+  if (v_r <= 64) return 64;
+  for (int cw : {10, 12, 13, 16})
+    if (8 * cw >= v_r) return 8 * cw;
+  return 0;
+}
 
 // Documents of the length-sorted range [p0, N) by row buckets (kCta); len_prefix[L] = number of
 // documents with fewer than L nonzeros.
@@ -536,9 +601,9 @@ void launch_sinkhorn_cta(const int4* sdoc, const Entry* ent, int64_t p0, int64_t
     const int64_t p1 = rows >= max_len ? N : len_prefix[rows + 1];
     if (p1 > p0) {
       switch (ld) {
-        case 32: dispatch_cta<4>(wi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, iters_doc, dist, flags, flagged_list, flagged_count, st); break;
-        case 64: dispatch_cta<8>(wi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, iters_doc, dist, flags, flagged_list, flagged_count, st); break;
-        case 128: dispatch_cta<16>(wi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, iters_doc, dist, flags, flagged_list, flagged_count, st); break;
+#define D_(LDV) case LDV: dispatch_cta<LDV / 8>(wi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, iters_doc, dist, flags, flagged_list, flagged_count, st); break;
+        D_(32) D_(64) D_(80) D_(96) D_(104) D_(128)
+#undef D_
         default: break;
       }
     }

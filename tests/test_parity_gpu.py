@@ -559,10 +559,17 @@ def test_fused_bucket_and_width_grid(W, v_r):
     assert_parity(d, o, f"fused grid v_r={v_r}")
 
 
-@pytest.mark.parametrize("v_r", [3, 20, 33, 64, 65, 100, 128])
+def _cta_ld(v_r):
+    if v_r <= 64:
+        return 32 if v_r <= 32 else 64
+    return min(x for x in (80, 96, 104, 128) if x >= v_r)
+
+
+@pytest.mark.parametrize("v_r", [3, 20, 33, 64, 65, 80, 81, 97, 100, 104, 105, 128])
 def test_fused_cta_long_documents(W, v_r):
     """One-CTA-per-document kernel (documents past the one-warp kernel's register budget): every
-    row bucket {64, 128, 192, 256: 32-row warps; 320: 40-row warps} x ld {32, 64, 128}, documents
+    row bucket {64, 128, 256: 32-row warps; 192: 48-row warps; 320: 40-row warps} x table width
+    {32, 64, 80, 96, 104, 128} (column quads plus 0-3 plain columns per lane), documents
     at and next to each boundary up to the 320-word maximum plus a sweep of every third length,
     mixed with short documents that stay on the one-warp kernel; AUTO must pick the fused path,
     and the distances must match the FP64 oracle."""
@@ -584,7 +591,7 @@ def test_fused_cta_long_documents(W, v_r):
             W.wmd_sync(h)
             st = W.wmd_get_stats(h)
             assert st["last_path"] == W.WMD_PATH_FUSED
-            assert st["last_ld"] == max(32, 1 << (v_r - 1).bit_length())
+            assert st["last_ld"] == _cta_ld(v_r)
         finally:
             W.wmd_destroy(h)
         o = oracle.sinkhorn_wmd(wl.E, cp, ri, va, q, w, lam, iters)
