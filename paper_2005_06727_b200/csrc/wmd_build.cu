@@ -164,14 +164,21 @@ __global__ void __launch_bounds__(kThreads, 2) build_mx_kernel(
 // Mx / K~ rows. Bound: reading E once from HBM (the MMAs need ~2 % of the tensor peak).
 // ============================================================================================
 constexpr int TC_M = 128;             // vocabulary rows per block (MMA M, TMEM lanes)
-#ifndef WMD_TC_CHUNK
-#define WMD_TC_CHUNK 16
+// d chunk (floats) and layout per query-tile width: swizzled 32-float chunks up to
+// WMD_TC_SWZ_MAX query rows, no-swizzle 16-float chunks beyond (shared memory per stage)
+#ifndef WMD_TC_SWZ_MAX
+#define WMD_TC_SWZ_MAX 32
 #endif
-constexpr int TC_K = WMD_TC_CHUNK;    // d chunk (floats)
+template <int NP> constexpr bool tc_swz() { return NP <= WMD_TC_SWZ_MAX; }
+template <int NP> constexpr int tc_k() { return tc_swz<NP>() ? 32 : 16; }
 #ifndef WMD_TC_STAGES
 #define WMD_TC_STAGES 3
 #endif
-constexpr int TC_NS = WMD_TC_STAGES;  // pipeline stages
+#ifndef WMD_TC_LO
+#define WMD_TC_LO 2
+#endif
+constexpr int TC_NS = WMD_TC_STAGES;  // raw-chunk ring stages
+constexpr int TC_LO = WMD_TC_LO;      // lo-part buffers = how many chunks back the MMA wait is
 constexpr float kNearFrac = 1.0f / 64.f;
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
@@ -179,12 +186,24 @@ __device__ __forceinline__ uint32_t su32(const void* p) {
 }
 // byte offset of element (r, k) (k < 32) in a K-major no-swizzle tile of R rows: core matrices
 // of 8 rows x 4 floats; SBO = 128 B between 8-row groups, LBO = R/8 * 128 B between K quads
+// Operand layouts (K-major). SWZ: SWIZZLE_128B with 32-float chunks (one 128-byte row): 8-row
+// atoms of 1024 B, the 16-byte piece j of row r stored at piece j ^ (r % 8) (the tensor core
+// undoes the XOR; conflict-free). Else the no-swizzle core-matrix layout with 16-float chunks:
+// core matrices of 8 rows x 16 B, SBO = 128 B, LBO = R / 8 * 128 B (half the shared memory per
+// stage, which keeps two 128-query-row blocks per SM).
+template <bool SWZ>
 __device__ __forceinline__ uint32_t km_off(int r, int k, int R) {
-  return (uint32_t)((k >> 2) * (R / 8 * 128) + (r >> 3) * 128 + (r & 7) * 16 + (k & 3) * 4);
+  if constexpr (SWZ) return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((((k >> 2) ^ r) & 7) << 4) + (k & 3) * 4);
+  else return (uint32_t)((k >> 2) * (R / 8 * 128) + (r >> 3) * 128 + (r & 7) * 16 + (k & 3) * 4);
 }
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
          ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);  // version 1, no swizzle
+}
+// SWIZZLE_128B K-major: SBO = 1024 B between 8-row atoms, LBO unused (1), layout type 2
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
 __device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
   asm volatile(
@@ -218,13 +237,17 @@ template <int NP>
 __global__ void __launch_bounds__(128, NP <= 32 ? 2 : 1) build_mx_tc_kernel(
     const float* __restrict__ E, int64_t row0, int64_t V, int dp, const int32_t* __restrict__ sel,
     int v_r, int ld, float lambda, float* __restrict__ Kt, float* __restrict__ Mx) {
+  constexpr bool SWZ = tc_swz<NP>();
+  constexpr int TC_K = tc_k<NP>();
   constexpr int A_BYTES = TC_M * TC_K * 4, B_BYTES = NP * TC_K * 4;
-  constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;          // raw (= hi) and lo, A and B
+  constexpr int STAGE = A_BYTES + B_BYTES;                  // one chunk: A rows, then B rows
   constexpr uint32_t TMEM_COLS = NP <= 32 ? 32 : (NP <= 64 ? 64 : 128);
   constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NP >> 3) << 17) |
                              ((uint32_t)(TC_M >> 4) << 24);   // F32 += TF32 x TF32, K-major both
   extern __shared__ __align__(1024) uint8_t tc_smem[];
-  uint8_t* smem = tc_smem;
+  // operand tiles at a 1024-byte aligned base (the swizzle atoms); 1 KB of slack is allocated
+  uint8_t* smem = tc_smem + ((1024u - (su32(tc_smem) & 1023u)) & 1023u);  // [TC_NS][STAGE]: raw (= hi)
+  uint8_t* lo_buf = smem + TC_NS * STAGE;                   // [TC_LO][STAGE]: their lo parts
   __shared__ uint32_t tmem_base;
   __shared__ __align__(8) uint64_t mbar[TC_NS];
   __shared__ float qn[NP];
@@ -254,43 +277,44 @@ __global__ void __launch_bounds__(128, NP <= 32 ? 2 : 1) build_mx_tc_kernel(
       const int r = p / (TC_K / 4), q = p % (TC_K / 4);
       const bool ok = k0 + r < V;
       const float* src = E + (ok ? k0 + r : 0) * (int64_t)dp + c * TC_K + 4 * q;
-      const uint32_t dst = su32(base + km_off(r, 4 * q, TC_M));
+      const uint32_t dst = su32(base + km_off<SWZ>(r, 4 * q, TC_M));
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0) : "memory");
     }
     for (int p = tid; p < NP * (TC_K / 4); p += 128) {
       const int r = p / (TC_K / 4), q = p % (TC_K / 4);
       const int row = qsel[r];
       const float* src = E + (row >= 0 ? row : 0) * (int64_t)dp + c * TC_K + 4 * q;
-      const uint32_t dst = su32(base + 2 * A_BYTES + km_off(r, 4 * q, NP));
+      const uint32_t dst = su32(base + A_BYTES + km_off<SWZ>(r, 4 * q, NP));
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(row >= 0 ? 16 : 0) : "memory");
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
   __syncthreads();  // qsel
   float en = 0.f, qq = 0.f;   // |E_row|^2 of this thread's vocabulary row; |q|^2 (tid < NP)
-  // copies run TC_NS - 2 chunks ahead: the stage being refilled was read by the MMAs of chunk
-  // c - 2, which have had a whole chunk step to complete
-  constexpr int AHEAD = TC_NS - 2;
+  // Raw chunks land AHEAD = TC_NS - TC_LO chunks ahead in a TC_NS-stage ring (the raw copy is
+  // also the hi operand: the tensor core reads TF32 from the FP32 bits); the lo parts go to a
+  // TC_LO-deep buffer. Ring stage (c + AHEAD) % TC_NS and lo buffer c % TC_LO are free once the
+  // MMAs of chunk c - TC_LO retired: waiting TC_LO chunks back hides the MMA completion latency.
+  constexpr int AHEAD = TC_NS - TC_LO;
+  static_assert(AHEAD >= 1, "ring deeper than the lo buffer");
   for (int c = 0; c < AHEAD; ++c) {
     if (c < nchunk) issue(c, c);
     else asm volatile("cp.async.commit_group;" ::: "memory");
   }
   for (int c = 0; c < nchunk; ++c) {
     const int st = c % TC_NS;
+    if (c >= TC_LO) mbar_wait(su32(&mbar[(c - TC_LO) % TC_NS]), ((c - TC_LO) / TC_NS) & 1);
     const int cn = c + AHEAD;
-    if (cn < nchunk) {
-      if (cn >= TC_NS) mbar_wait(su32(&mbar[cn % TC_NS]), ((cn - TC_NS) / TC_NS) & 1);
-      issue(cn, cn % TC_NS);
-    } else {
-      asm volatile("cp.async.commit_group;" ::: "memory");
-    }
+    if (cn < nchunk) issue(cn, cn % TC_NS);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
     asm volatile("cp.async.wait_group %0;" ::"n"(AHEAD) : "memory");  // chunk c has landed
     __syncthreads();
     uint8_t* base = smem + st * STAGE;
+    uint8_t* lob = lo_buf + (c % TC_LO) * STAGE;
     // lo parts and norms: thread tid owns vocabulary row tid (and query row tid < NP)
 #pragma unroll
     for (int q = 0; q < TC_K / 4; ++q) {
-      const uint32_t off = km_off(tid, 4 * q, TC_M);
+      const uint32_t off = km_off<SWZ>(tid, 4 * q, TC_M);
       const float4 x = *reinterpret_cast<const float4*>(base + off);
       en = fmaf(x.x, x.x, en); en = fmaf(x.y, x.y, en); en = fmaf(x.z, x.z, en); en = fmaf(x.w, x.w, en);
       float4 lo;
@@ -298,12 +322,12 @@ __global__ void __launch_bounds__(128, NP <= 32 ? 2 : 1) build_mx_tc_kernel(
       lo.y = x.y - __uint_as_float(__float_as_uint(x.y) & 0xffffe000u);
       lo.z = x.z - __uint_as_float(__float_as_uint(x.z) & 0xffffe000u);
       lo.w = x.w - __uint_as_float(__float_as_uint(x.w) & 0xffffe000u);
-      *reinterpret_cast<float4*>(base + A_BYTES + off) = lo;
+      *reinterpret_cast<float4*>(lob + off) = lo;
     }
     if (tid < NP) {
 #pragma unroll
       for (int q = 0; q < TC_K / 4; ++q) {
-        const uint32_t off = 2 * A_BYTES + km_off(tid, 4 * q, NP);
+        const uint32_t off = A_BYTES + km_off<SWZ>(tid, 4 * q, NP);
         const float4 x = *reinterpret_cast<const float4*>(base + off);
         qq = fmaf(x.x, x.x, qq); qq = fmaf(x.y, x.y, qq); qq = fmaf(x.z, x.z, qq); qq = fmaf(x.w, x.w, qq);
         float4 lo;
@@ -311,22 +335,28 @@ __global__ void __launch_bounds__(128, NP <= 32 ? 2 : 1) build_mx_tc_kernel(
         lo.y = x.y - __uint_as_float(__float_as_uint(x.y) & 0xffffe000u);
         lo.z = x.z - __uint_as_float(__float_as_uint(x.z) & 0xffffe000u);
         lo.w = x.w - __uint_as_float(__float_as_uint(x.w) & 0xffffe000u);
-        *reinterpret_cast<float4*>(base + 2 * A_BYTES + B_BYTES + (off - 2 * A_BYTES)) = lo;
+        *reinterpret_cast<float4*>(lob + off) = lo;
       }
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
     __syncthreads();
     if (tid == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;");
-      const uint32_t a_hi = su32(base), a_lo = a_hi + A_BYTES;
-      const uint32_t b_hi = su32(base + 2 * A_BYTES), b_lo = b_hi + B_BYTES;
+      const uint32_t a_hi = su32(base), a_lo = su32(lob);
+      const uint32_t b_hi = a_hi + A_BYTES, b_lo = a_lo + A_BYTES;
 #pragma unroll
       for (int pass = 0; pass < 3; ++pass) {          // hi.hi + hi.lo + lo.hi
         const uint32_t a = pass == 2 ? a_lo : a_hi, b = pass == 1 ? b_lo : b_hi;
 #pragma unroll
         for (int kk = 0; kk < TC_K; kk += 8) {
-          const uint64_t da = umma_desc(a + (kk >> 2) * (TC_M / 8 * 128), TC_M / 8 * 128, 128);
-          const uint64_t db = umma_desc(b + (kk >> 2) * (NP / 8 * 128), NP / 8 * 128, 128);
+          uint64_t da, db;
+          if constexpr (SWZ) {
+            da = umma_desc_sw128(a + 4 * kk);
+            db = umma_desc_sw128(b + 4 * kk);
+          } else {
+            da = umma_desc(a + (kk >> 2) * (TC_M / 8 * 128), TC_M / 8 * 128, 128);
+            db = umma_desc(b + (kk >> 2) * (NP / 8 * 128), NP / 8 * 128, 128);
+          }
           mma_tf32(tm, da, db, IDESC, (c | pass | kk) ? 1u : 0u);
         }
       }
@@ -422,7 +452,7 @@ void launch_build_ktilde(const float* E, int64_t row0, int64_t row1, int dp, con
   const unsigned grid = (unsigned)((row1 - row0 + TC_M - 1) / TC_M);
 #define TC_(NP)                                                                                       \
   {                                                                                                   \
-    constexpr size_t sm = TC_NS * (2 * TC_M * TC_K * 4 + 2 * NP * TC_K * 4);                         \
+    constexpr size_t sm = (TC_NS + TC_LO) * (TC_M + NP) * tc_k<NP>() * 4 + 1024;                    \
     static bool a = false;                                                                            \
     if (!a) { cudaFuncSetAttribute(build_mx_tc_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); a = true; } \
     build_mx_tc_kernel<NP><<<grid, 128, sm, st>>>(E, row0, row1, dp, sel, v_r, ld, lambda, Kt, Mx);  \
