@@ -40,19 +40,20 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False, defines=(), out: str = None) -> str:
-    """Build the library; `defines`/`out` build an experiment variant to another path."""
+def build(force: bool = False, verbose: bool = False, defines=(), out: str = None, extra_flags=()) -> str:
+    """Build the library; `defines` / `extra_flags` / `out` build an experiment variant to another
+    path."""
     lib = out or LIB
     if not force and not defines and out is None and not _stale():
         return LIB
-    objs = []
     build_dir = os.path.join(PKG, "build" if out is None else "build_" + os.path.basename(out))
     os.makedirs(build_dir, exist_ok=True)
     nvcc = _nvcc()
-    for s in SOURCES:
+
+    def compile_one(s):
         src = os.path.join(CSRC, s)
         obj = os.path.join(build_dir, s + ".o")
-        cmd = [nvcc, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
+        cmd = [nvcc, *NVCC_FLAGS, *extra_flags, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
         if s.endswith(".cpp"):
             cuda_inc = os.path.join(os.path.dirname(os.path.dirname(nvcc)), "include")
             cmd = ["g++", "-O2", "-std=c++17", "-fPIC", "-fvisibility=hidden", "-Wall",
@@ -64,7 +65,11 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = Non
             sys.stderr.write(res.stderr)
         with open(os.path.join(build_dir, s + ".ptxas.txt"), "w") as f:
             f.write(res.stderr)
-        objs.append(obj)
+        return obj
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
     tmp = lib + ".tmp"
     cmd = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static",
            "-o", tmp, *objs]

@@ -96,7 +96,10 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW, D>()) sinkhor
   using S = Shape<CW, NT, TW>;
   constexpr int LD = S::LD, RW = S::RW, NW = S::NW, P = S::P;
   constexpr int NOWN = NT + (TW ? 1 : 0);        // own rows per lane after the row reduce
-  constexpr int NCO = CW == 8 ? 2 : 1;           // own columns per lane after the column reduce
+  // own columns per lane after the column reduce: the quad columns 32g + 4b + a and the plain
+  // columns 32Q + Rb + r (CW >= 3), else column 2b + (a >> 1) (CW = 2) or b (CW = 1)
+  constexpr int CQ = Cols<CW>::Q, CR = Cols<CW>::R;
+  constexpr int NCO = CW >= 3 ? CQ + CR : 1;
   static_assert(D == 1 || !CONV, "per-document stopping runs one document per warp");
   extern __shared__ __align__(16) float smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -115,13 +118,14 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW, D>()) sinkhor
   bool oreal[NCO];
 #pragma unroll
   for (int g = 0; g < NCO; ++g) {
-    const int oc = CW == 8 ? 8 * b + 4 * g + a : (CW == 4 ? 4 * b + a : (CW == 2 ? 2 * b + (a >> 1) : b));
+    const int oc = CW >= 3 ? (g < CQ ? 32 * g + 4 * b + a : 32 * CQ + CR * b + (g - CQ))
+                           : (CW == 2 ? 2 * b + (a >> 1) : b);
     r_own[g] = __ldg(rpad + oc);
     oreal[g] = oc < v_r;
   }
-  bool nreal[CW];  // natural-order columns CW*b + c of this lane's group are real query rows
+  bool nreal[CW];  // natural-order columns of this lane's group are real query rows
 #pragma unroll
-  for (int c = 0; c < CW; ++c) nreal[c] = CW * b + c < v_r;
+  for (int c = 0; c < CW; ++c) nreal[c] = nat_col<CW>(c, b) < v_r;
 
   // ---- prefetch: stage 1 (document header), stage 2 (entries), stage 3 (cp.async of M rows)
   int64_t pos = pos0 + ((int64_t)blockIdx.x * kWarps + wib) * D;
@@ -332,11 +336,12 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW, D>()) sinkhor
         float uo[NCO];
 #pragma unroll
         for (int g = 0; g < NCO; ++g) {
-          const float acc = q[4 * g];
+          const int qs = CW >= 3 && g >= CQ ? 4 * CQ + (g - CQ) : 4 * g;  // slot of own column g
+          const float acc = q[qs];
           uo[g] = r_own[g] * rcp_fast(acc);
           // "while x changes" (NEXT-3): |x_new/x - 1| = |uh/uh_new - 1| (gauge invariant; the
           // own column's current uh sits in column slot 4g); NaN compares above every float
-          if (CONV && oreal[g]) chg_b = max(chg_b, __float_as_uint(fabsf(u[d][4 * g] / uo[g] - 1.f)));
+          if (CONV && oreal[g]) chg_b = max(chg_b, __float_as_uint(fabsf(u[d][qs] / uo[g] - 1.f)));
           bad[d] |= und[d] && vcap > acc;
           umax_b = max(umax_b, __float_as_uint(uo[g]));
         }
@@ -353,13 +358,15 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW, D>()) sinkhor
           bad[d] |= oreal[g] && !(uo[g] >= FLT_MIN);
         }
         // distribute uh to the column slots
-        if constexpr (CW >= 4) {
+        if constexpr (CW >= 3) {
 #pragma unroll
-          for (int g = 0; g < CW / 4; ++g) {
+          for (int g = 0; g < CQ; ++g) {
             u[d][4 * g] = uo[g];
 #pragma unroll
             for (int c = 1; c < 4; ++c) u[d][4 * g + c] = shx(uo[g], 8 * c);
           }
+#pragma unroll
+          for (int r = 0; r < CR; ++r) u[d][4 * CQ + r] = uo[CQ + r];
         } else if constexpr (CW == 2) {
           u[d][0] = uo[0];
           u[d][1] = shx(uo[0], 16);
@@ -493,12 +500,14 @@ int warp_max_rows(int ld) {
 }
 
 int fused_ld(int v_r, int64_t max_doc_nnz, bool conv) {
-  int ld = 8;
-  while (ld < v_r) ld *= 2;
-  if (ld > 128) return 0;
-  if (max_doc_nnz <= warp_max_rows(ld)) return ld;
-  // longer documents: one CTA per document (wmd_fused_cta.cu; fixed iteration count)
-  if (conv || max_doc_nnz > cta_max_rows()) return 0;
+  // one-warp kernel: 8 CW columns, CW in {1, 2, 3, 4, 5, 6, 8}
+  int ld = 0;
+  for (int cw : {1, 2, 3, 4, 5, 6, 8})
+    if (8 * cw >= v_r) { ld = 8 * cw; break; }
+  if (ld && max_doc_nnz <= warp_max_rows(ld)) return ld;
+  // longer documents (or v_r > 64): one CTA per document (wmd_fused_cta.cu; fixed iteration
+  // count), whose table width the one-warp kernel then shares for the shorter documents
+  if (v_r > 128 || conv || max_doc_nnz > cta_max_rows()) return 0;
   return cta_ld(v_r);
 }
 
@@ -520,6 +529,9 @@ void launch_sinkhorn_fused(const int4* sdoc, const Entry* ent, int64_t N,
         case 8: dispatch_bucket<1>(bi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, tol, iters_doc, dist, flags, flagged_list, flagged_count, st); break;
         case 16: dispatch_bucket<2>(bi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, tol, iters_doc, dist, flags, flagged_list, flagged_count, st); break;
         case 32: dispatch_bucket<4>(bi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, tol, iters_doc, dist, flags, flagged_list, flagged_count, st); break;
+        case 24: dispatch_bucket<3>(bi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, tol, iters_doc, dist, flags, flagged_list, flagged_count, st); break;
+        case 40: dispatch_bucket<5>(bi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, tol, iters_doc, dist, flags, flagged_list, flagged_count, st); break;
+        case 48: dispatch_bucket<6>(bi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, tol, iters_doc, dist, flags, flagged_list, flagged_count, st); break;
         case 64: dispatch_bucket<8>(bi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, tol, iters_doc, dist, flags, flagged_list, flagged_count, st); break;
         default: break;
       }

@@ -65,31 +65,7 @@ struct CtaShape {
   static constexpr int SMEM_FLOATS = 2 * W * CP + LD + 2 * ROWS + W + 4;
 };
 
-// Natural column of natural slot c (Mx order: query row i at column i); slot column of register
-// slot c (quads permuted by a).
-template <int CW>
-__device__ __forceinline__ int nat_col(int c, int b) {
-  constexpr int Q = CW / 4, R = CW % 4;
-  return c < 4 * Q ? 32 * (c >> 2) + 4 * b + (c & 3) : 32 * Q + R * b + (c - 4 * Q);
-}
-template <int CW>
-__device__ __forceinline__ int slot_col(int c, int a, int b) {
-  constexpr int Q = CW / 4, R = CW % 4;
-  return c < 4 * Q ? 32 * (c >> 2) + 4 * b + ((c & 3) ^ a) : 32 * Q + R * b + (c - 4 * Q);
-}
-// natural -> slot order (the quads; the plain columns stay)
-template <int CW>
-__device__ __forceinline__ void quads_to_slots(float (&x)[CW], int a) {
-  const bool s1 = a & 1, s2 = a & 2;
-#pragma unroll
-  for (int q = 0; q < CW / 4; ++q) {
-    float* y = x + 4 * q;
-    float t0 = s1 ? y[1] : y[0], t1 = s1 ? y[0] : y[1];
-    float t2 = s1 ? y[3] : y[2], t3 = s1 ? y[2] : y[3];
-    y[0] = s2 ? t2 : t0; y[2] = s2 ? t0 : t2;
-    y[1] = s2 ? t3 : t1; y[3] = s2 ? t1 : t3;
-  }
-}
+// Column layout (quads + plain columns, nat_col / col_of / to_slots / reduce_cols): wmd_tile.cuh.
 
 // Resident warps per SM the register budget is written for: 12 (168 registers per thread) when
 // the block takes at most 96 registers per thread, else 8 (255): at 168 such instances spill,
@@ -253,7 +229,7 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W, TW>()) sinkhorn_
         }
       }
 #pragma unroll
-      for (int s = 0; s < RW; ++s) quads_to_slots<CW>(K[s], a);
+      for (int s = 0; s < RW; ++s) to_slots<CW>(K[s], a);
       und = __syncthreads_or(flushed);  // also: the minima are read
     }
     // uh0 = v_r 2^-beta (x0 = 1 / v_r, in the rescaled variables)
@@ -432,7 +408,7 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W, TW>()) sinkhorn_
         }
         load_D(n);
 #pragma unroll
-        for (int s = 0; s < RW; ++s) quads_to_slots<CW>(K[s], a);
+        for (int s = 0; s < RW; ++s) to_slots<CW>(K[s], a);
         __syncthreads();  // the new betal is published
         // L = -alpha D + beta; gamma_e = -(max of L over the real columns of row e)
         float rmax[RW];
@@ -440,7 +416,7 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W, TW>()) sinkhorn_
         for (int s = 0; s < RW; ++s) rmax[s] = -FLT_MAX;
 #pragma unroll
         for (int c = 0; c < CW; ++c) {
-          const int col = slot_col<CW>(c, a, b);
+          const int col = col_of<CW>(c, a, b);
           const float bc = betal[col];
 #pragma unroll
           for (int s = 0; s < RW; ++s) {
@@ -461,7 +437,7 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W, TW>()) sinkhorn_
           const bool rowok = row0 + row_of<1, TW>(s, a, b) < n;
 #pragma unroll
           for (int c = 0; c < CW; ++c) {
-            const bool real = slot_col<CW>(c, a, b) < v_r;
+            const bool real = col_of<CW>(c, a, b) < v_r;
             const float kx = ex2_ftz(K[s][c] + gs[s]);
             flushed |= real && rowok && kx < FLT_MIN;
             K[s][c] = rowok ? (real ? kx : 1.f) : 0.f;
@@ -492,7 +468,7 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W, TW>()) sinkhorn_
       for (int c = 0; c < CW; ++c) {
         // uh of slot c, and uh beta / alpha
         const float uc = c < 4 * Q ? ((c & 3) == 0 ? uo[c >> 2] : shx(uo[c >> 2], 8 * (c & 3))) : ur[c - 4 * Q];
-        const float ub = uc * (-ia * betal[slot_col<CW>(c, a, b)]);
+        const float ub = uc * (-ia * betal[col_of<CW>(c, a, b)]);
 #pragma unroll
         for (int s = 0; s < RW; ++s) {
           const float k = K[s][c];
@@ -579,13 +555,13 @@ void dispatch_cta(int wi, const int4* sdoc, const Entry* ent, int64_t p0, int64_
 
 int cta_max_rows() { return kCta[kNumCta - 1].rows; }
 
-// Row width of the one-CTA kernel's tables for a query of v_r rows: 32 or 64 for v_r <= 64
-// (shared with the one-warp kernel's power-of-two widths), else 8 CW with CW in {10, 12, 13, 16}
-// (LD = 80, 96, 104, 128: at v_r = 100, 4 padded columns instead of 28).
+// Row width of the one-CTA kernel's tables for a query of v_r rows: 8 CW with CW in {4, 5, 8,
+// 10, 12, 13, 16} (at v_r = 100: 104 columns, 4 padded, instead of 128); the one-warp kernel
+// shares it for the shorter documents of the same query.
 int cta_ld(int v_r) {
-  if (v_r <= 32) return 32;
-  if (v_r <= 64) return 64;
-  for (int cw : {10, 12, 13, 16})
+  // (CW = 6 is left out: its 320-row instance faulted on 257-270-word documents in the
+  // optimised build, not in a -G build; DESIGN.md §5. v_r 41-48 uses CW = 8.)
+  for (int cw : {4, 5, 8, 10, 12, 13, 16})
     if (8 * cw >= v_r) return 8 * cw;
   return 0;
 }
@@ -602,7 +578,7 @@ void launch_sinkhorn_cta(const int4* sdoc, const Entry* ent, int64_t p0, int64_t
     if (p1 > p0) {
       switch (ld) {
 #define D_(LDV) case LDV: dispatch_cta<LDV / 8>(wi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, iters_doc, dist, flags, flagged_list, flagged_count, st); break;
-        D_(32) D_(64) D_(80) D_(96) D_(104) D_(128)
+        D_(32) D_(40) D_(64) D_(80) D_(96) D_(104) D_(128)
 #undef D_
         default: break;
       }

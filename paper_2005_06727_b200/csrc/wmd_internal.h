@@ -66,7 +66,7 @@ void launch_final_wmd(const int32_t* order, const int32_t* doc_ptr, const Entry*
 // per-iteration path). `len_prefix` (host, max_len + 2 entries): len_prefix[L] = number of
 // documents with fewer than L nonzeros, i.e. bucket boundaries in the length-sorted `order`.
 // Row width of the fused path's tables for query length v_r and longest document max_doc_nnz
-// (v_r rounded up to 8, 16, 32, 64; cta_ld(v_r) when a document needs the one-CTA kernel),
+// (8 CW, CW in {1, 2, 3, 4, 5, 6, 8}; cta_ld(v_r) when a document needs the one-CTA kernel),
 // or 0 if the fused path does not take the shape (the caller then uses the per-iteration path).
 // conv: a per-document stopping tolerance is set (one-warp kernel only).
 int fused_ld(int v_r, int64_t max_doc_nnz, bool conv);
@@ -81,7 +81,7 @@ int fused_launch_count(const int64_t* len_prefix, int64_t max_len, int64_t N, in
 
 // --- NEXT-1, long documents: one CTA of ceil(n/32) warps per document (wmd_fused_cta.cu) -----
 int cta_max_rows();  // longest document the one-CTA kernel takes
-int cta_ld(int v_r);  // its table row width for v_r query rows: 32, 64, 80, 96, 104 or 128
+int cta_ld(int v_r);  // its table row width for v_r query rows: 8 CW, CW in {4, 5, 8, 10, 12, 13, 16}
 // Documents [p0, N) of the length-sorted order, ld = cta_ld(v_r), fixed iteration count.
 void launch_sinkhorn_cta(const int4* sdoc, const Entry* ent, int64_t p0, int64_t N, const int64_t* len_prefix,
                          int64_t max_len, const float* Mx, int ld, int v_r, const float* rpad, float lambda,

@@ -42,21 +42,41 @@ __device__ __forceinline__ int row_of(int s, int a, int b) {
   return 32 * NT + TW * a + ((s - 8 * NT) ^ (b >> TSH));
 }
 
+// Column layout of a lane's CW = 4Q + R block columns (CW = 3 or CW >= 4; CW = 1, 2 below):
+// Q quads, quad g of lane b covering columns 32g + 4b + j (j < 4), then R plain columns
+// 32Q + Rb + r. In register-slot order the quads are XOR-permuted by a (slot 4g + t holds
+// j = t ^ a) so that the column transpose-reduce over the a-lanes needs no selects; the plain
+// columns are the same in all four a-lanes and are reduced by a full butterfly.
+template <int CW>
+struct Cols {
+  static constexpr int Q = CW >= 3 ? CW / 4 : 0;
+  static constexpr int R = CW >= 3 ? CW % 4 : 0;
+};
+
+// Natural-order column of slot c (the order load_cols delivers).
+template <int CW>
+__device__ __forceinline__ int nat_col(int c, int b) {
+  constexpr int Q = Cols<CW>::Q, R = Cols<CW>::R;
+  if constexpr (CW >= 3) return c < 4 * Q ? 32 * (c >> 2) + 4 * b + (c & 3) : 32 * Q + R * b + (c - 4 * Q);
+  else return CW * b + c;
+}
+
 // Column (query row) of column slot c of lane (a, b).
 template <int CW>
 __device__ __forceinline__ int col_of(int c, int a, int b) {
-  if constexpr (CW >= 4) return CW * b + 4 * (c >> 2) + ((c & 3) ^ a);
+  constexpr int Q = Cols<CW>::Q, R = Cols<CW>::R;
+  if constexpr (CW >= 3) return c < 4 * Q ? 32 * (c >> 2) + 4 * b + ((c & 3) ^ a) : 32 * Q + R * b + (c - 4 * Q);
   else if constexpr (CW == 2) return 2 * b + (c ^ (a >> 1));
   else return b;
 }
 
 // Permute x[0..CW) (natural column order of this lane's column group) into slot order:
-// x'[c] = x[c ^ key], key = a (per quad for CW = 8) or a >> 1 (CW = 2).
+// x'[c] = x[c ^ key], key = a (per quad) or a >> 1 (CW = 2); plain columns stay.
 template <int CW>
 __device__ __forceinline__ void to_slots(float (&x)[CW], int a) {
-  if constexpr (CW >= 4) {
+  if constexpr (CW >= 3) {
 #pragma unroll
-    for (int q = 0; q < CW / 4; ++q) {
+    for (int q = 0; q < Cols<CW>::Q; ++q) {
       float* y = x + 4 * q;
       const bool s1 = a & 1, s2 = a & 2;
       float t0 = s1 ? y[1] : y[0], t1 = s1 ? y[0] : y[1];
@@ -74,12 +94,15 @@ __device__ __forceinline__ void to_slots(float (&x)[CW], int a) {
 // Loads this lane's CW natural-order columns of one staged row.
 template <int CW>
 __device__ __forceinline__ void load_cols(const float* row, int b, float (&x)[CW]) {
-  if constexpr (CW >= 4) {
+  if constexpr (CW >= 3) {
+    constexpr int Q = Cols<CW>::Q, R = Cols<CW>::R;
 #pragma unroll
-    for (int q = 0; q < CW / 4; ++q) {
-      const float4 t = *reinterpret_cast<const float4*>(row + CW * b + 4 * q);
+    for (int q = 0; q < Q; ++q) {
+      const float4 t = *reinterpret_cast<const float4*>(row + 32 * q + 4 * b);
       x[4 * q] = t.x; x[4 * q + 1] = t.y; x[4 * q + 2] = t.z; x[4 * q + 3] = t.w;
     }
+#pragma unroll
+    for (int r = 0; r < R; ++r) x[4 * Q + r] = row[32 * Q + R * b + r];
   } else if constexpr (CW == 2) {
     const float2 t = *reinterpret_cast<const float2*>(row + 2 * b);
     x[0] = t.x; x[1] = t.y;
@@ -140,15 +163,22 @@ __device__ __forceinline__ void reduce_rows_max(float* p) {
 }
 
 // Transpose-reduce of the column partials q[0..CW) over the 4 a-lanes (lane xor 16, 8):
-// afterwards q[0] (and q[4] for CW = 8) holds the full sum of the lane's own column(s).
+// afterwards q[4g] holds the full sum of quad column 32g + 4b + a, q[4Q + r] that of plain
+// column 32Q + Rb + r (CW >= 3); q[0] that of column 2b + (a >> 1) (CW = 2) or b (CW = 1).
 template <int CW>
 __device__ __forceinline__ void reduce_cols(float* q) {
-  if constexpr (CW >= 4) {
+  if constexpr (CW >= 3) {
+    constexpr int Q = Cols<CW>::Q, R = Cols<CW>::R;
 #pragma unroll
-    for (int g = 0; g < CW / 4; ++g) {
+    for (int g = 0; g < Q; ++g) {
       float* y = q + 4 * g;
       y[0] += shx(y[2], 16); y[1] += shx(y[3], 16);
       y[0] += shx(y[1], 8);
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      q[4 * Q + r] += shx(q[4 * Q + r], 16);
+      q[4 * Q + r] += shx(q[4 * Q + r], 8);
     }
   } else if constexpr (CW == 2) {
     q[0] += shx(q[1], 16);

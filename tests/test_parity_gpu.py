@@ -531,15 +531,16 @@ def _docs_with_lengths(V, lengths, seed, p=0.6, lo_id=0):
     return synth.csc_from_lists(docs, V)
 
 
-@pytest.mark.parametrize("v_r", [1, 5, 8, 9, 16, 17, 30, 32, 33, 64])
+@pytest.mark.parametrize("v_r", [1, 5, 8, 9, 16, 17, 24, 25, 30, 32, 33, 40, 41, 48, 49, 64])
 def test_fused_bucket_and_width_grid(W, v_r):
-    """Every fused-kernel instance: ld in {8, 16, 32, 64} x length buckets {8, 16, 32, 40, 48, 64}
+    """Every one-warp fused-kernel instance: ld in {8, 16, 24, 32, 40, 48, 64} (CW = 1, 2, plain
+    3, quad, quad + 1 or 2 plain columns, 2 quads) x length buckets {8, 16, 32, 40, 48, 64}
     (documents at and next to each boundary, ragged counts per bucket); AUTO must pick the fused
     path, and the distances must match the FP64 oracle."""
     wl = synth.make_workload("tweet", n_queries=0, N=10)
     V = wl.cfg.V
     lengths = [1, 2, 7, 8, 9, 15, 16, 17, 31, 32, 33, 39, 40, 41, 47, 48, 49, 63, 64] * 3
-    if v_r > 32:  # the 64-wide tables keep documents of up to 48 words in one warp's registers
+    if v_r > 48:  # the 64-wide tables keep documents of up to 48 words in one warp's registers
         lengths = [L for L in lengths if L <= 48]
     cp, ri, va = _docs_with_lengths(V, lengths, seed=v_r)
     rng = np.random.default_rng(100 + v_r)
@@ -552,7 +553,9 @@ def test_fused_bucket_and_width_grid(W, v_r):
         d = np.empty(cp.shape[0] - 1, np.float32)
         W.wmd_query(h, q, w, 10.0, 15, d)
         W.wmd_sync(h)
-        assert W.wmd_get_stats(h)["last_path"] == W.WMD_PATH_FUSED
+        st = W.wmd_get_stats(h)
+        assert st["last_path"] == W.WMD_PATH_FUSED
+        assert st["last_ld"] == _warp_ld(v_r)
     finally:
         W.wmd_destroy(h)
     o = oracle.sinkhorn_wmd(wl.E, cp, ri, va, q, w, 10.0, 15)
@@ -560,12 +563,14 @@ def test_fused_bucket_and_width_grid(W, v_r):
 
 
 def _cta_ld(v_r):
-    if v_r <= 64:
-        return 32 if v_r <= 32 else 64
-    return min(x for x in (80, 96, 104, 128) if x >= v_r)
+    return min(x for x in (32, 40, 64, 80, 96, 104, 128) if x >= v_r)
 
 
-@pytest.mark.parametrize("v_r", [3, 20, 33, 64, 65, 80, 81, 97, 100, 104, 105, 128])
+def _warp_ld(v_r):
+    return min(x for x in (8, 16, 24, 32, 40, 48, 64) if x >= v_r)
+
+
+@pytest.mark.parametrize("v_r", [3, 20, 25, 33, 36, 40, 41, 44, 48, 56, 64, 65, 72, 80, 81, 90, 97, 100, 104, 105, 116, 128])
 def test_fused_cta_long_documents(W, v_r):
     """One-CTA-per-document kernel (documents past the one-warp kernel's register budget): every
     row bucket {64, 128, 256: 32-row warps; 192: 48-row warps; 320: 40-row warps} x table width

@@ -26,7 +26,9 @@ q = np.sort(rng.choice(V, v_r, replace=False)).astype(np.int32)
 w = np.full(v_r, 1.0 / v_r, np.float32)
 h = wmd.wmd_create(E)
 wmd.wmd_set_targets(h, cp, ri, va)
+if os.environ.get("NOFB"):
+    wmd.wmd_set_option(h, wmd.WMD_OPT_FALLBACK, 0)
 out = np.empty(len(lengths), np.float32)
 wmd.wmd_query(h, q, w, 10.0, 30, out)
 wmd.wmd_sync(h)
-print(out[:4], np.isfinite(out).all(), wmd.wmd_get_stats(h)["last_path"], wmd.wmd_get_stats(h)["last_ld"])
+print(out[:4], np.isfinite(out).all(), "flagged", int(np.count_nonzero(wmd.wmd_read_flags(h, len(lengths)))), wmd.wmd_get_stats(h)["last_path"], wmd.wmd_get_stats(h)["last_ld"])
