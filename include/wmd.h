@@ -96,7 +96,7 @@ typedef struct {
   int64_t fallback_docs;     /* documents recomputed in FP64, summed over queries (updated by wmd_sync) */
   int64_t flagged_docs;      /* documents of the last query flagged in FP32 (updated by wmd_sync) */
   int32_t last_v_r;
-  int32_t last_ld;           /* row width (floats) of the K~ / M tables: v_r rounded up to 8 (per-iteration path); on the fused path 8 CW with CW in {1, 2, 3, 4, 5, 6, 8} when every document fits the one-warp kernel, else in {4, 5, 8, 10, 12, 13, 16} */
+  int32_t last_ld;           /* row width (floats) of the K~ / M tables: v_r rounded up to 8 (per-iteration path); on the fused path 8 CW with CW in {1, 2, 3, 4, 5, 6, 8} when every document fits the one-warp kernel, else in {4, 5, 6, 8, 10, 12, 13, 16} */
   int32_t last_path;         /* wmd_path actually used by the last query */
   int32_t timing_valid;      /* 1 if the *_ms fields below are populated (WMD_OPT_TIMING) */
   double build_ms;           /* distance + kernel build (step a2), summed over queries */

@@ -68,11 +68,13 @@ struct CtaShape {
 // Column layout (quads + plain columns, nat_col / col_of / to_slots / reduce_cols): wmd_tile.cuh.
 
 // Resident warps per SM the register budget is written for: 12 (168 registers per thread) when
-// the block takes at most 96 registers per thread, else 8 (255): at 168 such instances spill,
-// and a spilling build faulted on some shapes.
+// the block takes at most 96 registers per thread, else 8 (255; at 168 those instances spill).
+#ifndef WMD_CTA_WPS_BIG
+#define WMD_CTA_WPS_BIG 8
+#endif
 template <int CW, int W, int TW>
 constexpr int cta_min_blocks() {
-  constexpr int wps = (8 + TW) * CW > 96 ? 8 : 12;
+  constexpr int wps = (8 + TW) * CW > 96 ? WMD_CTA_WPS_BIG : 12;
   return W < wps ? wps / W : 1;
 }
 
@@ -117,18 +119,19 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W, TW>()) sinkhorn_
   int64_t pos = pos0 + blockIdx.x;
   int pj = -1, pb = 0, pn = 0;
   int2 pe[EPT];
+  // (guarded loads read a clamped, always valid address: the compiler may hoist a guarded
+  // __ldg above its guard, and an out-of-range index past the last document faulted)
   auto stage1 = [&](int64_t p) {
-    pj = -1; pn = 0; pb = 0;
-    if (p < pos1) {
-      const int4 x = __ldg(sdoc + p);
-      pj = x.x; pb = x.y; pn = x.z;
-    }
+    const int4 x = __ldg(sdoc + (p < pos1 ? p : pos1 - 1));
+    const bool ok = p < pos1;
+    pj = ok ? x.x : -1; pb = ok ? x.y : 0; pn = ok ? x.z : 0;
   };
   auto stage2 = [&]() {
 #pragma unroll
     for (int x = 0; x < EPT; ++x) {
       const int e = tid + NT * x;
-      pe[x] = e < pn ? __ldg(ent2 + pb + e) : make_int2(0, 0);
+      const int2 v = __ldg(ent2 + pb + (e < pn ? e : 0));
+      pe[x] = e < pn ? v : make_int2(0, 0);
     }
   };
   stage1(pos);
@@ -555,13 +558,11 @@ void dispatch_cta(int wi, const int4* sdoc, const Entry* ent, int64_t p0, int64_
 
 int cta_max_rows() { return kCta[kNumCta - 1].rows; }
 
-// Row width of the one-CTA kernel's tables for a query of v_r rows: 8 CW with CW in {4, 5, 8,
-// 10, 12, 13, 16} (at v_r = 100: 104 columns, 4 padded, instead of 128); the one-warp kernel
+// Row width of the one-CTA kernel's tables for a query of v_r rows: 8 CW with CW in {4, 5, 6,
+// 8, 10, 12, 13, 16} (at v_r = 100: 104 columns, 4 padded, instead of 128); the one-warp kernel
 // shares it for the shorter documents of the same query.
 int cta_ld(int v_r) {
-  // (CW = 6 is left out: its 320-row instance faulted on 257-270-word documents in the
-  // optimised build, not in a -G build; DESIGN.md §5. v_r 41-48 uses CW = 8.)
-  for (int cw : {4, 5, 8, 10, 12, 13, 16})
+  for (int cw : {4, 5, 6, 8, 10, 12, 13, 16})
     if (8 * cw >= v_r) return 8 * cw;
   return 0;
 }
@@ -578,7 +579,7 @@ void launch_sinkhorn_cta(const int4* sdoc, const Entry* ent, int64_t p0, int64_t
     if (p1 > p0) {
       switch (ld) {
 #define D_(LDV) case LDV: dispatch_cta<LDV / 8>(wi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, iters_doc, dist, flags, flagged_list, flagged_count, st); break;
-        D_(32) D_(40) D_(64) D_(80) D_(96) D_(104) D_(128)
+        D_(32) D_(40) D_(48) D_(64) D_(80) D_(96) D_(104) D_(128)
 #undef D_
         default: break;
       }

@@ -21,6 +21,10 @@
 using wmd::Entry;
 
 namespace {
+constexpr int64_t kGuard = 1024;  // zeroed slack entries after ent / sdoc (see set_targets)
+}  // namespace
+
+namespace {
 
 constexpr double kWeightTol = 1e-5;  // |sum - 1| for FP32 weights summed in FP64 (R23)
 
@@ -511,7 +515,10 @@ wmd_status wmd_set_targets(wmd_handle* h, const int64_t* col_ptr, const int32_t*
   std::vector<Entry> en(nnz);
   for (int64_t q = 0; q < nnz; ++q) en[q] = Entry{row_idx[q], val[q]};
   CK(h, h->doc_ptr.ensure(N + 1));
-  CK(h, h->ent.ensure(nnz));
+  // + kGuard zeroed entries past the end: the fused kernels' guarded prefetch loads clamp their
+  // index, and the slack keeps any speculated read of the next row inside the allocation
+  CK(h, h->ent.ensure(nnz + kGuard));
+  CK(h, cudaMemsetAsync(h->ent.p + nnz, 0, kGuard * sizeof(Entry), h->stream));
   CK(h, h->order.ensure(N));
   CK(h, cudaMemcpyAsync(h->order.p, ord.data(), N * sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
   std::vector<int4> sd(N);
@@ -519,7 +526,8 @@ wmd_status wmd_set_targets(wmd_handle* h, const int64_t* col_ptr, const int32_t*
     const int32_t j = ord[p];
     sd[p] = make_int4(j, dp[j], dp[j + 1] - dp[j], 0);
   }
-  CK(h, h->sdoc.ensure(N));
+  CK(h, h->sdoc.ensure(N + kGuard));
+  CK(h, cudaMemsetAsync(h->sdoc.p + N, 0, kGuard * sizeof(int4), h->stream));
   CK(h, cudaMemcpyAsync(h->sdoc.p, sd.data(), N * sizeof(int4), cudaMemcpyHostToDevice, h->stream));
   CK(h, cudaMemcpyAsync(h->doc_ptr.p, dp.data(), (N + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
   CK(h, cudaMemcpyAsync(h->ent.p, en.data(), nnz * sizeof(Entry), cudaMemcpyHostToDevice, h->stream));

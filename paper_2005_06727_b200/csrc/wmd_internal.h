@@ -81,7 +81,7 @@ int fused_launch_count(const int64_t* len_prefix, int64_t max_len, int64_t N, in
 
 // --- NEXT-1, long documents: one CTA of ceil(n/32) warps per document (wmd_fused_cta.cu) -----
 int cta_max_rows();  // longest document the one-CTA kernel takes
-int cta_ld(int v_r);  // its table row width for v_r query rows: 8 CW, CW in {4, 5, 8, 10, 12, 13, 16}
+int cta_ld(int v_r);  // its table row width for v_r query rows: 8 CW, CW in {4, 5, 6, 8, 10, 12, 13, 16}
 // Documents [p0, N) of the length-sorted order, ld = cta_ld(v_r), fixed iteration count.
 void launch_sinkhorn_cta(const int4* sdoc, const Entry* ent, int64_t p0, int64_t N, const int64_t* len_prefix,
                          int64_t max_len, const float* Mx, int ld, int v_r, const float* rpad, float lambda,

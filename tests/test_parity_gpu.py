@@ -563,7 +563,7 @@ def test_fused_bucket_and_width_grid(W, v_r):
 
 
 def _cta_ld(v_r):
-    return min(x for x in (32, 40, 64, 80, 96, 104, 128) if x >= v_r)
+    return min(x for x in (32, 40, 48, 64, 80, 96, 104, 128) if x >= v_r)
 
 
 def _warp_ld(v_r):
