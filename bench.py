@@ -45,6 +45,17 @@ def _peaks():
         return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback (B200_PROFILING.md)"
 
 
+def _traffic(cfg_name):
+    """DRAM bytes (read + write) of the fused phase per step (one query) from the committed ncu
+    --set full capture (profiles/r01_traffic.json, written by tools/ncu_traffic.py), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+            t = json.load(f)[cfg_name]
+        return t["dram_bytes_per_query"]
+    except Exception:
+        return None
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
@@ -409,8 +420,12 @@ def main():
             flops = 4.0 * v_r * nnz_l * (cfg.iters + 1)           # 2 FMAs per (nnz, row) per pass
             mhz = peaks.get("sm_max_mhz", 1965.0)
             peak_tf = 148 * 128 * 2 * mhz * 1e6 / 1e12
+            ld = st["last_ld"]
+            warp_max = 0 if ld > 64 else (48 if ld == 64 else 64)   # one-warp kernel's longest document
+            kname = ("sinkhorn_cta" if cfg.doc_lo > warp_max else
+                     ("sinkhorn_fused + sinkhorn_cta" if cfg.doc_hi > warp_max else "sinkhorn_fused"))
             roofline = {
-                "kernel": "sinkhorn_fused", "bound": "alu",
+                "kernel": kname, "bound": "alu",
                 "achieved": flops / t_phase / 1e12, "peak": peak_tf, "unit": "TFLOP/s",
                 "frac": flops / t_phase / 1e12 / peak_tf,
                 "peak_source": f"derived: 148 SMs x 128 FP32 FMA/clk x 2 flops x {mhz:.0f} MHz "
@@ -419,7 +434,7 @@ def main():
                 "phase_ms": t_phase * 1e3,
                 "launches_per_step": st["iter_launches"] / args.steps,
                 "l2_gather_bytes_per_step": 4 * (st["last_ld"] + 4) * nnz_l,  # one M row (+ m_k) per nonzero, once
-                "traffic": None,
+                "traffic": _traffic(cfg.name) if world == 1 else None,
                 "share_of_step": st["iter_ms"] / max(st["query_ms"], 1e-9),
             }
         line = {

@@ -23,6 +23,25 @@ constexpr float kUnderScale = 0x1p-133f;  // 2^-149 / 2^-16
 
 __device__ __forceinline__ bool normal_pos(float x) { return x >= FLT_MIN && x <= FLT_MAX; }
 
+// Read-only loads that stay behind their guard: an `if (i < n) x = __ldg(p + i)` may be hoisted
+// above the guard by the compiler (it treats __ldg as free of side effects), which reads past the
+// end of an array; the asm volatile form is neither hoisted nor speculated.
+__device__ __forceinline__ int ldg_guarded(const int* p) {
+  int v;
+  asm volatile("ld.global.nc.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int2 ldg_guarded(const int2* p) {
+  int2 v;
+  asm volatile("ld.global.nc.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int4 ldg_guarded(const int4* p) {
+  int4 v;
+  asm volatile("ld.global.nc.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+
 // L2 residency: the K~ / M tables (<= V*ld*4 bytes, 51 MB at Scaling) are gathered repeatedly
 // and should stay in the 126 MB L2 while c and u stream past them: table gathers carry an
 // evict_last policy.

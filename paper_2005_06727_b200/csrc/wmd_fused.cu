@@ -135,11 +135,11 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW, D>()) sinkhor
   auto stage1 = [&](int64_t p) {
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-      // {document id, first nonzero, length, -}; the index is clamped (a guarded __ldg may be
-      // hoisted above its guard)
-      const bool ok = p + d < pos1;
-      const int4 x = __ldg(sdoc + (ok ? p + d : pos1 - 1));
-      pj[d] = ok ? x.x : -1; pb[d] = ok ? x.y : 0; pn[d] = ok ? x.z : 0;
+      pj[d] = -1; pn[d] = 0; pb[d] = 0;
+      if (p + d < pos1) {  // {document id, first nonzero, length, -} (a load that stays guarded)
+        const int4 x = ldg_guarded(sdoc + p + d);
+        pj[d] = x.x; pb[d] = x.y; pn[d] = x.z;
+      }
     }
   };
   auto stage2 = [&]() {
@@ -148,8 +148,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW, D>()) sinkhor
 #pragma unroll
       for (int w = 0; w < NW; ++w) {
         const int e = lane + 32 * w;
-        const int2 v = __ldg(ent2 + pb[d] + (e < pn[d] ? e : 0));
-        const int2 x = e < pn[d] ? v : make_int2(0, 0);
+        int2 x = make_int2(0, 0);
+        if (e < pn[d]) x = ldg_guarded(ent2 + pb[d] + e);
         pk[d][w] = x.x;
         pc[d][w] = __int_as_float(x.y);
       }

@@ -119,8 +119,8 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W, TW>()) sinkhorn_
   int64_t pos = pos0 + blockIdx.x;
   int pj = -1, pb = 0, pn = 0;
   int2 pe[EPT];
-  // (guarded loads read a clamped, always valid address: the compiler may hoist a guarded
-  // __ldg above its guard, and an out-of-range index past the last document faulted)
+  // (unconditional loads of clamped, always valid indices, then selects: the guarded-load form
+  // faulted in some optimised builds of this kernel)
   auto stage1 = [&](int64_t p) {
     const int4 x = __ldg(sdoc + (p < pos1 ? p : pos1 - 1));
     const bool ok = p < pos1;

@@ -12,10 +12,13 @@
 #include <algorithm>
 #include <cstdint>
 
+#include "wmd_device.cuh"
 #include "wmd_internal.h"
 
 namespace wmd {
 namespace {
+
+using dev::ldg_guarded;
 
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -158,20 +161,19 @@ __global__ void __launch_bounds__(256, FINAL ? 2 : PASS_BLOCKS_PER_SM) sinkhorn_
 
   // Round structure: in each round the warp's NG groups take NG consecutive documents of the
   // length-sorted order, so their step counts match; the next round is prefetched.
-  // (guarded loads use clamped, always valid indices: a guarded __ldg may be hoisted above its
-  // guard by the compiler)
+  // (ldg_guarded: loads that stay behind their guard)
   auto head = [&](int64_t pos, int64_t& jj, int& bb, int& nn) {
-    const bool ok = pos < N;
-    const int64_t j0 = WMD_LDS(order + (ok ? pos : N - 1));
-    const int b0 = WMD_LDS(doc_ptr + j0);
-    const int n0 = WMD_LDS(doc_ptr + j0 + 1) - b0;
-    jj = ok ? j0 : -1; bb = ok ? b0 : 0; nn = ok ? n0 : 0;
+    jj = -1; bb = 0; nn = 0;
+    if (pos < N) {
+      jj = ldg_guarded(order + pos);
+      bb = ldg_guarded(doc_ptr + jj);
+      nn = ldg_guarded(doc_ptr + jj + 1) - bb;
+    }
   };
   auto body = [&](int64_t jj, int bb, int nn, int2& e0, float4& uu, uint32_t& mb) {
     e0 = make_int2(0, 0); uu = zero; mb = 0u;
     if (jj < 0) return;
-    const int2 e0v = WMD_LDS(ent2 + bb + (qm < nn ? qm : 0));
-    if (qm < nn) e0 = e0v;
+    if (qm < nn) e0 = ldg_guarded(ent2 + bb + qm);
     if (u_in == nullptr) {  // x0 = 1/v_r  =>  u0 = v_r on the v_r real rows
       uu = make_float4(r.x > 0.f ? u0 : 0.f, r.y > 0.f ? u0 : 0.f, r.z > 0.f ? u0 : 0.f,
                        r.w > 0.f ? u0 : 0.f);
@@ -216,11 +218,8 @@ __global__ void __launch_bounds__(256, FINAL ? 2 : PASS_BLOCKS_PER_SM) sinkhorn_
       const bool myvalid = eb + qm < n;
       const float c = __int_as_float(my.y);
       // next step's nonzero (and, once per round, the next round's document) while K~ is in flight
-      {
-        const bool nx = eb + U + qm < n;
-        const int2 myv = WMD_LDS(ent2 + b + (nx ? eb + U + qm : 0));
-        my = nx ? myv : make_int2(0, 0);
-      }
+      my = make_int2(0, 0);
+      if (eb + U + qm < n) my = ldg_guarded(ent2 + b + eb + U + qm);
       if (!prefetched) {
         prefetched = true;
         body(jn, bn, nn_, myn, unx, mbn);
