@@ -213,7 +213,8 @@ WMD_API wmd_status wmd_reset_stats(wmd_handle* h);
  *   zero padded beyond v_r) and colmin[k] = min_i M_ik. Any output pointer may be NULL.
  * wmd_read_scaling: u after the last iteration, documents [j0, j0+count), ld floats each
  *   (gauge-scaled: only ratios within a document are meaningful). Per-iteration path only.
- * wmd_read_flags: flags[N] (bit0: FP32 iterate left the normal range; bit1: FP64 re-run). */
+ * wmd_read_flags: flags[N] (bit0: FP32 iterate left the normal range; bit1: FP64 re-run;
+ *   bit2: re-run in FP32 by the one-CTA kernel with re-anchoring, R33). */
 WMD_API wmd_status wmd_get_query_rows(wmd_handle* h, int32_t* sel, float* r);
 WMD_API wmd_status wmd_read_kernel(wmd_handle* h, int64_t k0, int64_t count, float* ktilde, float* m,
                            float* colmin);

@@ -78,12 +78,21 @@ constexpr int cta_min_blocks() {
   return W < wps ? wps / W : 1;
 }
 
-template <int CW, int W, int TW>
+// LIST: the documents are the ids of a device list (of *count entries) instead of a range of the
+// length-sorted order: the re-run of documents the one-warp kernel could not certify (DESIGN.md
+// R33); documents longer than the bucket go straight to the output list (the FP64 re-run).
+struct DocList {
+  const int32_t* ids;
+  const int32_t* count;
+  const int32_t* doc_ptr;
+};
+
+template <int CW, int W, int TW, bool LIST>
 __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W, TW>()) sinkhorn_cta_kernel(
     const int4* __restrict__ sdoc, const Entry* __restrict__ ent, int64_t pos0, int64_t pos1,
     const float* __restrict__ Mx, int v_r, const float* __restrict__ rpad, float lambda, int iters,
     int32_t* __restrict__ iters_doc, float* __restrict__ dist, uint8_t* __restrict__ flags,
-    int32_t* __restrict__ flagged_list, int32_t* __restrict__ flagged_count) {
+    int32_t* __restrict__ flagged_list, int32_t* __restrict__ flagged_count, DocList dl) {
   using S = CtaShape<CW, W, TW>;
   constexpr int LD = S::LD, Q = S::Q, R = S::R, P = S::P, CP = S::CP, RW = S::RW, RPW = S::RPW;
   constexpr int NOWN = S::NOWN, TSH = S::TSH, ROWS = S::ROWS, NT = 32 * W;
@@ -115,6 +124,10 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W, TW>()) sinkhorn_
   orow[0] = row0 + lane;
   if constexpr (TW > 0) orow[NOWN - 1] = row0 + 32 + TW * a + (b >> TSH);
 
+  if constexpr (LIST) {
+    pos1 = *dl.count;
+    if (pos1 <= 0) return;
+  }
   // ---- prefetch: header and this thread's entries (rows tid, tid + 32 W, ...) of the next document
   int64_t pos = pos0 + blockIdx.x;
   int pj = -1, pb = 0, pn = 0;
@@ -122,9 +135,18 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W, TW>()) sinkhorn_
   // (unconditional loads of clamped, always valid indices, then selects: the guarded-load form
   // faulted in some optimised builds of this kernel)
   auto stage1 = [&](int64_t p) {
-    const int4 x = __ldg(sdoc + (p < pos1 ? p : pos1 - 1));
     const bool ok = p < pos1;
-    pj = ok ? x.x : -1; pb = ok ? x.y : 0; pn = ok ? x.z : 0;
+    if constexpr (LIST) {
+      const int jj = __ldg(dl.ids + (ok ? p : pos1 - 1));
+      const int b0 = __ldg(dl.doc_ptr + jj), n0 = __ldg(dl.doc_ptr + jj + 1) - b0;
+      // a document longer than this bucket: id encoded as -2 - j, nothing to prefetch
+      pj = ok ? (n0 <= ROWS ? jj : -2 - jj) : -1;
+      pb = ok ? b0 : 0;
+      pn = ok && n0 <= ROWS ? n0 : 0;
+    } else {
+      const int4 x = __ldg(sdoc + (ok ? p : pos1 - 1));
+      pj = ok ? x.x : -1; pb = ok ? x.y : 0; pn = ok ? x.z : 0;
+    }
   };
   auto stage2 = [&]() {
 #pragma unroll
@@ -183,6 +205,13 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W, TW>()) sinkhorn_
     }
     stage1(pos + gridDim.x);
     __syncthreads();  // entries published; the previous document is done with shared memory
+    if constexpr (LIST) {
+      if (j <= -2) {  // too long for this bucket: on to the FP64 re-run (CTA-uniform branch)
+        if (tid == 0) flagged_list[atomicAdd(flagged_count, 1)] = -2 - j;
+        stage2();
+        continue;
+      }
+    }
 
     bool v_ok[NOWN];
     float c_own[NOWN], m_own[NOWN];
@@ -502,6 +531,8 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W, TW>()) sinkhorn_
       if (anybad || !(fabsf(total) <= FLT_MAX)) {
         flags[j] |= kFlagFp32Range;
         flagged_list[atomicAdd(flagged_count, 1)] = j;
+      } else if (LIST) {
+        flags[j] |= kFlagRerun;
       }
     }
   }
@@ -518,21 +549,40 @@ int num_sms_cta() {
   return sms;
 }
 
+template <int CW, int W, int TW, bool LIST>
+int cta_resident() {
+  constexpr size_t smem = sizeof(float) * CtaShape<CW, W, TW>::SMEM_FLOATS;
+  static int resident = 0;
+  if (!resident) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sinkhorn_cta_kernel<CW, W, TW, LIST>, 32 * W, smem);
+    resident = std::max(1, per_sm) * num_sms_cta();
+  }
+  return resident;
+}
+
 template <int CW, int W, int TW>
 void launch_cta_range(const int4* sdoc, const Entry* ent, int64_t p0, int64_t p1, const float* Mx, int v_r,
                       const float* rpad, float lambda, int iters, int32_t* itd, float* dist, uint8_t* flags,
                       int32_t* fl, int32_t* fc, cudaStream_t st) {
   if (p1 <= p0) return;
   constexpr size_t smem = sizeof(float) * CtaShape<CW, W, TW>::SMEM_FLOATS;
-  static int resident = 0;
-  if (!resident) {
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sinkhorn_cta_kernel<CW, W, TW>, 32 * W, smem);
-    resident = std::max(1, per_sm) * num_sms_cta();
-  }
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(p1 - p0, resident));
-  sinkhorn_cta_kernel<CW, W, TW><<<grid, 32 * W, smem, st>>>(sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters,
-                                                             itd, dist, flags, fl, fc);
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(p1 - p0, cta_resident<CW, W, TW, false>()));
+  sinkhorn_cta_kernel<CW, W, TW, false><<<grid, 32 * W, smem, st>>>(sdoc, ent, p0, p1, Mx, v_r, rpad, lambda,
+                                                                    iters, itd, dist, flags, fl, fc, DocList{});
+}
+
+// The re-run of a device list of documents (at most 64 words each are re-run; longer ones are
+// passed on) in 2-warp CTAs, one resident wave that loops over the list.
+template <int CW>
+void launch_cta_list(const int32_t* ids, const int32_t* count, const int32_t* doc_ptr, const Entry* ent,
+                     const float* Mx, int v_r, const float* rpad, float lambda, int iters, int32_t* itd,
+                     float* dist, uint8_t* flags, int32_t* out_list, int32_t* out_count, cudaStream_t st) {
+  constexpr size_t smem = sizeof(float) * CtaShape<CW, 2, 0>::SMEM_FLOATS;
+  const unsigned grid = (unsigned)cta_resident<CW, 2, 0, true>();
+  sinkhorn_cta_kernel<CW, 2, 0, true><<<grid, 64, smem, st>>>(nullptr, ent, 0, 0, Mx, v_r, rpad, lambda, iters,
+                                                             itd, dist, flags, out_list, out_count,
+                                                             DocList{ids, count, doc_ptr});
 }
 
 // Row buckets (rows = W x (32 + 4 TW)): 2 / 4 warps of 32 rows (64, 128), 4 warps of 48 rows
@@ -585,6 +635,20 @@ void launch_sinkhorn_cta(const int4* sdoc, const Entry* ent, int64_t p0, int64_t
       }
     }
     p0 = std::max(p0, p1);
+  }
+}
+
+bool cta_rerun_supported(int ld) { return ld == 32 || ld == 40 || ld == 48 || ld == 64; }
+
+void launch_cta_rerun(const int32_t* ids, const int32_t* count, const int32_t* doc_ptr, const Entry* ent,
+                      const float* Mx, int ld, int v_r, const float* rpad, float lambda, int iters,
+                      int32_t* iters_doc, float* dist, uint8_t* flags, int32_t* out_list, int32_t* out_count,
+                      cudaStream_t st) {
+  switch (ld) {
+#define R_(LDV) case LDV: launch_cta_list<LDV / 8>(ids, count, doc_ptr, ent, Mx, v_r, rpad, lambda, iters, iters_doc, dist, flags, out_list, out_count, st); break;
+    R_(32) R_(40) R_(48) R_(64)
+#undef R_
+    default: break;
   }
 }
 

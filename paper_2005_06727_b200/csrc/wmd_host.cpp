@@ -127,7 +127,9 @@ struct wmd_handle {
   DevBuf<int32_t> iters_doc; // N: x-updates per document of the last query
   DevBuf<uint8_t> conv;      // N: converged flags ("while x changes", per-iteration path)
   double tol = -1.0;         // "while x changes" relative tolerance; < 0: fixed iterations
-  DevBuf<int32_t> counters;  // [0] flagged count, [1] breakdown, [2] fallback count, [3] scratch
+  DevBuf<int32_t> flagged2;  // N: documents the one-CTA re-run could not certify either
+  DevBuf<int32_t> counters;  // [0] flagged count, [1] breakdown, [2] fallback count, [3] scratch,
+                             // [4] flagged2 count
   DevBuf<double> fb_scratch;
   // pinned staging for the query upload (double buffered)
   void* stage[2] = {nullptr, nullptr};
@@ -386,12 +388,12 @@ wmd_status wmd_create(const float* vocab_emb, int64_t V, int32_t d, int32_t devi
   const size_t n = (size_t)V * d;
   if (h->E.ensure((size_t)V * dp) != cudaSuccess) return bail(WMD_ERR_OUT_OF_MEMORY);
   if (cudaMemsetAsync(h->E.p, 0, (size_t)V * dp * sizeof(float), h->stream) != cudaSuccess) return bail(WMD_ERR_CUDA);
-  if (h->counters.ensure(4) != cudaSuccess) return bail(WMD_ERR_OUT_OF_MEMORY);
+  if (h->counters.ensure(6) != cudaSuccess) return bail(WMD_ERR_OUT_OF_MEMORY);
   if (is_device_ptr(vocab_emb)) {
     if (cudaMemcpy2DAsync(h->E.p, dp * sizeof(float), vocab_emb, d * sizeof(float), d * sizeof(float), V,
                           cudaMemcpyDeviceToDevice, h->stream) != cudaSuccess)
       return bail(WMD_ERR_CUDA);
-    cudaMemsetAsync(h->counters.p, 0, 4 * sizeof(int32_t), h->stream);
+    cudaMemsetAsync(h->counters.p, 0, 6 * sizeof(int32_t), h->stream);
     wmd::launch_check_finite(h->E.p, (int64_t)V * dp, h->counters.p + 3, h->stream);
     int32_t bad = 0;
     if (cudaMemcpyAsync(&bad, h->counters.p + 3, sizeof bad, cudaMemcpyDeviceToHost, h->stream) != cudaSuccess ||
@@ -407,7 +409,7 @@ wmd_status wmd_create(const float* vocab_emb, int64_t V, int32_t d, int32_t devi
       return bail(WMD_ERR_CUDA);
   }
   if (h->sel.ensure(WMD_MAX_VR) != cudaSuccess || h->rpad.ensure(WMD_MAX_VR) != cudaSuccess ||
-      h->counters.ensure(4) != cudaSuccess)
+      h->counters.ensure(6) != cudaSuccess)
     return bail(WMD_ERR_OUT_OF_MEMORY);
   if (cudaEventCreateWithFlags(&h->batch_ev, cudaEventDisableTiming) != cudaSuccess) return bail(WMD_ERR_CUDA);
   for (int s = 0; s < 2; ++s) {
@@ -436,7 +438,7 @@ void wmd_destroy(wmd_handle* h) {
   }
   h->E.release(); h->doc_ptr.release(); h->order.release(); h->sdoc.release(); h->ent.release(); h->sel.release(); h->rpad.release();
   h->Kt.release(); h->Mx.release(); h->ua.release(); h->ub.release(); h->umask.release();
-  h->dist_tmp.release(); h->flags.release(); h->flagged.release(); h->counters.release();
+  h->dist_tmp.release(); h->flags.release(); h->flagged.release(); h->flagged2.release(); h->counters.release();
   h->iters_doc.release(); h->conv.release();
   h->fb_scratch.release();
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
@@ -533,6 +535,7 @@ wmd_status wmd_set_targets(wmd_handle* h, const int64_t* col_ptr, const int32_t*
   CK(h, cudaMemcpyAsync(h->ent.p, en.data(), nnz * sizeof(Entry), cudaMemcpyHostToDevice, h->stream));
   CK(h, h->flags.ensure(N));
   CK(h, h->flagged.ensure(N));
+  CK(h, h->flagged2.ensure(N));
   CK(h, h->iters_doc.ensure(N));
   CK(h, h->conv.ensure(N));
   CK(h, h->dist_tmp.ensure(N));
@@ -627,10 +630,22 @@ wmd_status record_solve(wmd_handle* h, const float* d_r, int32_t v_r, float lamb
     ++launches;
     if (pe) CK(h, cudaEventRecord(pe->ev[3], st));
   }
-  // a6: FP64 re-run of flagged documents (device-side list; zero-cost when empty)
+  // a6: re-run of flagged documents (device-side lists; zero-cost when empty): on the fused path
+  // first in FP32 by the one-CTA kernel with re-anchoring (R33; fixed iteration count),
+  // then whatever is left in FP64
   if (h->opt_fallback) {
+    const int32_t* fl = h->flagged.p;
+    int32_t* fc = h->counters.p;
+    if (fused && tol < 0.f && wmd::cta_rerun_supported(ld)) {
+      CK(h, cudaMemsetAsync(h->counters.p + 4, 0, sizeof(int32_t), st));
+      wmd::launch_cta_rerun(h->flagged.p, h->counters.p, h->doc_ptr.p, h->ent.p, h->Mx.p, ld, v_r, d_r, lambda,
+                            iters, h->iters_doc.p, dist, h->flags.p, h->flagged2.p, h->counters.p + 4, st);
+      ++launches;
+      fl = h->flagged2.p;
+      fc = h->counters.p + 4;
+    }
     wmd::launch_fallback_fp64(h->Mx.p, ld, d_r, v_r, (double)lambda, iters, tol, h->iters_doc.p, h->doc_ptr.p,
-                              h->ent.p, h->flagged.p, h->counters.p, h->fb_scratch.p, h->max_doc_nnz, dist,
+                              h->ent.p, fl, fc, h->fb_scratch.p, h->max_doc_nnz, dist,
                               h->flags.p, h->counters.p + 1, h->counters.p + 2, st);
     ++launches;
   }

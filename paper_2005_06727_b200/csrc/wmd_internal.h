@@ -20,6 +20,7 @@ struct Entry {
 // Flag bits per document.
 constexpr uint8_t kFlagFp32Range = 1;  // an FP32 iterate left the normal range
 constexpr uint8_t kFlagFp64 = 2;       // recomputed in FP64
+constexpr uint8_t kFlagRerun = 4;      // recomputed in FP32 by the one-CTA kernel (re-anchoring)
 
 // Device-side per-query scalars the kernels read (written by one H2D copy per query).
 struct QueryDev {
@@ -88,6 +89,14 @@ void launch_sinkhorn_cta(const int4* sdoc, const Entry* ent, int64_t p0, int64_t
                          int iters, int32_t* iters_doc, float* dist, uint8_t* flags, int32_t* flagged_list,
                          int32_t* flagged_count, cudaStream_t st);
 int cta_launch_count(int64_t p0, int64_t N, const int64_t* len_prefix, int64_t max_len);
+// Re-run (FP32, re-anchoring) of the documents of a device list (ids[0 .. *count)) that the
+// one-warp kernel flagged, for ld in {32, 40, 48, 64}; documents that still fail (or are longer
+// than 64 words) are appended to out_list / *out_count for the FP64 re-run.
+bool cta_rerun_supported(int ld);
+void launch_cta_rerun(const int32_t* ids, const int32_t* count, const int32_t* doc_ptr, const Entry* ent,
+                      const float* Mx, int ld, int v_r, const float* rpad, float lambda, int iters,
+                      int32_t* iters_doc, float* dist, uint8_t* flags, int32_t* out_list, int32_t* out_count,
+                      cudaStream_t st);
 
 // --- a6: FP64 re-run of flagged documents (no CPU fallback) --------------------------------
 constexpr int kFallbackBlocks = 296;  // 2 per SM (1 per SM for documents whose K needs > 100 KB)

@@ -603,6 +603,35 @@ def test_fused_cta_long_documents(W, v_r):
         assert_parity(d, o, f"fused CTA v_r={v_r} lam={lam}")
 
 
+def test_warp_flagged_documents_rerun_with_reanchoring(W):
+    """Documents of 50-64 words against a 40-word query (the Long config's) at lambda = 10: the
+    one-warp kernel cannot certify a good share of them (dual potentials wider than the FP32
+    exponent, R33); they are re-run in FP32 by the one-CTA kernel with re-anchoring
+    (flag bit 2) before anything goes to the FP64 re-run, and every distance matches the oracle."""
+    wl = synth.make_workload("long", n_queries=1)
+    q, w = wl.queries[0]
+    q = q[:40]
+    w = (w[:40] / w[:40].sum()).astype(np.float32)
+    docs = np.nonzero(np.diff(wl.col_ptr) <= 64)[0][:300]
+    cp, ri, va = synth.subset_docs(wl.col_ptr, wl.row_idx, wl.val, docs)
+    lam, iters = 10.0, 30
+    h = W.wmd_create(wl.E)
+    try:
+        W.wmd_set_targets(h, cp, ri, va)
+        d = np.empty(docs.shape[0], np.float32)
+        W.wmd_query(h, q, w, lam, iters, d)
+        W.wmd_sync(h)
+        st = W.wmd_get_stats(h)
+        flags = W.wmd_read_flags(h, docs.shape[0])
+        assert st["last_path"] == W.WMD_PATH_FUSED and st["last_ld"] == 40
+    finally:
+        W.wmd_destroy(h)
+    assert np.count_nonzero(flags & 4) > 0, "expected documents re-run with re-anchoring"
+    assert np.count_nonzero(flags & 2) < np.count_nonzero(flags & 4)
+    o = oracle.sinkhorn_wmd(wl.E, cp, ri, va, q, w, lam, iters)
+    assert_parity(d, o, "re-anchored re-run")
+
+
 # ------------------------------------------------------------------ NEXT-2: query batches
 
 def test_query_batch_equals_single_queries_and_oracle(W):
