@@ -73,7 +73,7 @@ struct Shape {
 #define WMD_FUSED_DOCS_PER_WARP 1
 #endif
 #ifndef WMD_FUSED_REG_SLACK
-#define WMD_FUSED_REG_SLACK 36
+#define WMD_FUSED_REG_SLACK 8
 #endif
 template <int CW, int NT, int TW, int D>
 constexpr int min_blocks() {
