@@ -515,7 +515,7 @@ void launch_sinkhorn_fused(const int4* sdoc, const Entry* ent, int64_t N,
                            const int64_t* len_prefix, int64_t max_len, const float* Mx, int ld,
                            int v_r, const float* rpad, float lambda, int iters, float tol,
                            int32_t* iters_doc, float* dist, uint8_t* flags, int32_t* flagged_list,
-                           int32_t* flagged_count, cudaStream_t st) {
+                           int32_t* flagged_count, cudaStream_t st0, StreamRing* ring) {
   // len_prefix[L] = number of documents with fewer than L nonzeros: the length-sorted order
   // splits into buckets of at most 8 / 16 / 32 / 40 / 48 / 64 nonzeros (one-warp kernel, one
   // launch each) and, past warp_max_rows(ld), 64 / 128 / ... / 320 (one-CTA kernel).
@@ -525,6 +525,7 @@ void launch_sinkhorn_fused(const int4* sdoc, const Entry* ent, int64_t N,
     const int NE = kBuckets[bi].ne;
     const int64_t p1 = NE >= max_len ? N : len_prefix[NE + 1];
     if (p1 > p0) {
+      const cudaStream_t st = ring ? ring->next(st0) : st0;
       switch (ld) {
         case 8: dispatch_bucket<1>(bi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, tol, iters_doc, dist, flags, flagged_list, flagged_count, st); break;
         case 16: dispatch_bucket<2>(bi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, tol, iters_doc, dist, flags, flagged_list, flagged_count, st); break;
@@ -540,7 +541,7 @@ void launch_sinkhorn_fused(const int4* sdoc, const Entry* ent, int64_t N,
   }
   if (p0 < N)
     launch_sinkhorn_cta(sdoc, ent, p0, N, len_prefix, max_len, Mx, ld, v_r, rpad, lambda, iters, iters_doc,
-                        dist, flags, flagged_list, flagged_count, st);
+                        dist, flags, flagged_list, flagged_count, st0, ring);
 }
 
 int fused_launch_count(const int64_t* len_prefix, int64_t max_len, int64_t N, int ld) {

@@ -622,11 +622,12 @@ int cta_ld(int v_r) {
 void launch_sinkhorn_cta(const int4* sdoc, const Entry* ent, int64_t p0, int64_t N, const int64_t* len_prefix,
                          int64_t max_len, const float* Mx, int ld, int v_r, const float* rpad, float lambda,
                          int iters, int32_t* iters_doc, float* dist, uint8_t* flags, int32_t* flagged_list,
-                         int32_t* flagged_count, cudaStream_t st) {
+                         int32_t* flagged_count, cudaStream_t st0, StreamRing* ring) {
   for (int wi = 0; wi < kNumCta && p0 < N; ++wi) {
     const int rows = kCta[wi].rows;
     const int64_t p1 = rows >= max_len ? N : len_prefix[rows + 1];
     if (p1 > p0) {
+      const cudaStream_t st = ring ? ring->next(st0) : st0;
       switch (ld) {
 #define D_(LDV) case LDV: dispatch_cta<LDV / 8>(wi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, iters_doc, dist, flags, flagged_list, flagged_count, st); break;
         D_(32) D_(40) D_(48) D_(64) D_(80) D_(96) D_(104) D_(128)

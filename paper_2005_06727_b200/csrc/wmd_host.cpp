@@ -101,6 +101,9 @@ struct wmd_handle {
   int device = 0;
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
+  static constexpr int kLanes = 3;               // streams of the fused phase's length buckets
+  cudaStream_t lanes[kLanes] = {};
+  cudaEvent_t fork_ev = nullptr, join_ev[kLanes] = {};
   // embeddings
   DevBuf<float> E;
   int64_t V = 0;
@@ -412,6 +415,11 @@ wmd_status wmd_create(const float* vocab_emb, int64_t V, int32_t d, int32_t devi
       h->counters.ensure(6) != cudaSuccess)
     return bail(WMD_ERR_OUT_OF_MEMORY);
   if (cudaEventCreateWithFlags(&h->batch_ev, cudaEventDisableTiming) != cudaSuccess) return bail(WMD_ERR_CUDA);
+  if (cudaEventCreateWithFlags(&h->fork_ev, cudaEventDisableTiming) != cudaSuccess) return bail(WMD_ERR_CUDA);
+  for (int i = 0; i < wmd_handle::kLanes; ++i)
+    if (cudaStreamCreateWithFlags(&h->lanes[i], cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->join_ev[i], cudaEventDisableTiming) != cudaSuccess)
+      return bail(WMD_ERR_CUDA);
   for (int s = 0; s < 2; ++s) {
     if (cudaMallocHost(&h->stage[s], WMD_MAX_VR * 8) != cudaSuccess) return bail(WMD_ERR_OUT_OF_MEMORY);
     if (cudaEventCreateWithFlags(&h->stage_ev[s], cudaEventDisableTiming) != cudaSuccess) return bail(WMD_ERR_CUDA);
@@ -441,6 +449,11 @@ void wmd_destroy(wmd_handle* h) {
   h->dist_tmp.release(); h->flags.release(); h->flagged.release(); h->flagged2.release(); h->counters.release();
   h->iters_doc.release(); h->conv.release();
   h->fb_scratch.release();
+  for (int i = 0; i < wmd_handle::kLanes; ++i) {
+    if (h->lanes[i]) { cudaStreamSynchronize(h->lanes[i]); cudaStreamDestroy(h->lanes[i]); }
+    if (h->join_ev[i]) cudaEventDestroy(h->join_ev[i]);
+  }
+  if (h->fork_ev) cudaEventDestroy(h->fork_ev);
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
   delete h;
 }
@@ -603,9 +616,23 @@ wmd_status record_solve(wmd_handle* h, const float* d_r, int32_t v_r, float lamb
   int64_t launches = 0;
   const float tol = h->tol >= 0.0 ? (float)h->tol : -1.f;
   if (fused) {
+    // the length buckets run on the handle's lanes (forked from and joined to `st`), so one
+    // bucket's tail overlaps the next one's start
+    const int nb = wmd::fused_launch_count(h->len_prefix.data(), h->max_doc_nnz, N, ld);
+    wmd::StreamRing ring;
+    if (nb > 1) {
+      ring.s = h->lanes;
+      ring.n = std::min(nb, (int)wmd_handle::kLanes);
+      CK(h, cudaEventRecord(h->fork_ev, st));
+      for (int i = 0; i < ring.n; ++i) CK(h, cudaStreamWaitEvent(h->lanes[i], h->fork_ev, 0));
+    }
     wmd::launch_sinkhorn_fused(h->sdoc.p, h->ent.p, N, h->len_prefix.data(),
                                h->max_doc_nnz, h->Mx.p, ld, v_r, d_r, lambda, iters, tol, h->iters_doc.p,
-                               dist, h->flags.p, h->flagged.p, h->counters.p, st);
+                               dist, h->flags.p, h->flagged.p, h->counters.p, st, &ring);
+    for (int i = 0; i < ring.n; ++i) {
+      CK(h, cudaEventRecord(h->join_ev[i], h->lanes[i]));
+      CK(h, cudaStreamWaitEvent(st, h->join_ev[i], 0));
+    }
     launches += wmd::fused_launch_count(h->len_prefix.data(), h->max_doc_nnz, N, ld);
     if (pe) { CK(h, cudaEventRecord(pe->ev[2], st)); CK(h, cudaEventRecord(pe->ev[3], st)); }
   } else {

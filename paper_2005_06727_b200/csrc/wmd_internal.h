@@ -72,12 +72,20 @@ void launch_final_wmd(const int32_t* order, const int32_t* doc_ptr, const Entry*
 // conv: a per-document stopping tolerance is set (one-warp kernel only).
 int fused_ld(int v_r, int64_t max_doc_nnz, bool conv);
 int warp_max_rows(int ld);  // longest document of the one-warp kernel at row width ld
+// Streams the length buckets are launched on (round robin; the caller forks them from and joins
+// them to its stream) so that one bucket's tail overlaps the next bucket; n = 0: all on `st`.
+struct StreamRing {
+  const cudaStream_t* s = nullptr;
+  int n = 0;
+  int k = 0;
+  cudaStream_t next(cudaStream_t st) { return n ? s[k++ % n] : st; }
+};
 // sdoc[p] = {document id, first nonzero, length, 0} of the p-th document in length order.
 void launch_sinkhorn_fused(const int4* sdoc, const Entry* ent, int64_t N,
                            const int64_t* len_prefix, int64_t max_len, const float* Mx, int ld,
                            int v_r, const float* rpad, float lambda, int iters, float tol,
                            int32_t* iters_doc, float* dist, uint8_t* flags, int32_t* flagged_list,
-                           int32_t* flagged_count, cudaStream_t st);
+                           int32_t* flagged_count, cudaStream_t st, StreamRing* ring = nullptr);
 int fused_launch_count(const int64_t* len_prefix, int64_t max_len, int64_t N, int ld);
 
 // --- NEXT-1, long documents: one CTA of ceil(n/32) warps per document (wmd_fused_cta.cu) -----
@@ -87,7 +95,7 @@ int cta_ld(int v_r);  // its table row width for v_r query rows: 8 CW, CW in {4,
 void launch_sinkhorn_cta(const int4* sdoc, const Entry* ent, int64_t p0, int64_t N, const int64_t* len_prefix,
                          int64_t max_len, const float* Mx, int ld, int v_r, const float* rpad, float lambda,
                          int iters, int32_t* iters_doc, float* dist, uint8_t* flags, int32_t* flagged_list,
-                         int32_t* flagged_count, cudaStream_t st);
+                         int32_t* flagged_count, cudaStream_t st, StreamRing* ring = nullptr);
 int cta_launch_count(int64_t p0, int64_t N, const int64_t* len_prefix, int64_t max_len);
 // Re-run (FP32, re-anchoring) of the documents of a device list (ids[0 .. *count)) that the
 // one-warp kernel flagged, for ld in {32, 40, 48, 64}; documents that still fail (or are longer
