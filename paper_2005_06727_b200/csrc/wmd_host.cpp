@@ -104,6 +104,8 @@ struct wmd_handle {
   static constexpr int kLanes = 3;               // streams of the fused phase's length buckets
   cudaStream_t lanes[kLanes] = {};
   cudaEvent_t fork_ev = nullptr, join_ev[kLanes] = {};
+  cudaStream_t bstream = nullptr;                // wmd_query_batch: builds of the next queries
+  cudaEvent_t built_ev[2] = {}, solved_ev[2] = {};
   // embeddings
   DevBuf<float> E;
   int64_t V = 0;
@@ -121,6 +123,7 @@ struct wmd_handle {
   DevBuf<float> rpad;        // WMD_MAX_VR (zero padded to ld)
   DevBuf<float> Kt;          // V * ld: K~ (FP32, vocab-major; per-iteration path only)
   DevBuf<float> Mx;          // V * (ld + 4): M rows + m_k (FP32, vocab-major)
+  DevBuf<float> Mx2;         // the second table of wmd_query_batch's build/solve overlap
   bool kt_valid = false;     // Kt holds the last query's K~
   DevBuf<float> ua, ub;      // N * ld
   DevBuf<uint32_t> umask;    // N * ceil(ld/32): rows with an underflowed K~ entry, per doc
@@ -416,6 +419,11 @@ wmd_status wmd_create(const float* vocab_emb, int64_t V, int32_t d, int32_t devi
     return bail(WMD_ERR_OUT_OF_MEMORY);
   if (cudaEventCreateWithFlags(&h->batch_ev, cudaEventDisableTiming) != cudaSuccess) return bail(WMD_ERR_CUDA);
   if (cudaEventCreateWithFlags(&h->fork_ev, cudaEventDisableTiming) != cudaSuccess) return bail(WMD_ERR_CUDA);
+  if (cudaStreamCreateWithFlags(&h->bstream, cudaStreamNonBlocking) != cudaSuccess) return bail(WMD_ERR_CUDA);
+  for (int i = 0; i < 2; ++i)
+    if (cudaEventCreateWithFlags(&h->built_ev[i], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->solved_ev[i], cudaEventDisableTiming) != cudaSuccess)
+      return bail(WMD_ERR_CUDA);
   for (int i = 0; i < wmd_handle::kLanes; ++i)
     if (cudaStreamCreateWithFlags(&h->lanes[i], cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&h->join_ev[i], cudaEventDisableTiming) != cudaSuccess)
@@ -445,7 +453,7 @@ void wmd_destroy(wmd_handle* h) {
     if (h->stage_ev[s]) cudaEventDestroy(h->stage_ev[s]);
   }
   h->E.release(); h->doc_ptr.release(); h->order.release(); h->sdoc.release(); h->ent.release(); h->sel.release(); h->rpad.release();
-  h->Kt.release(); h->Mx.release(); h->ua.release(); h->ub.release(); h->umask.release();
+  h->Kt.release(); h->Mx.release(); h->Mx2.release(); h->ua.release(); h->ub.release(); h->umask.release();
   h->dist_tmp.release(); h->flags.release(); h->flagged.release(); h->flagged2.release(); h->counters.release();
   h->iters_doc.release(); h->conv.release();
   h->fb_scratch.release();
@@ -454,6 +462,11 @@ void wmd_destroy(wmd_handle* h) {
     if (h->join_ev[i]) cudaEventDestroy(h->join_ev[i]);
   }
   if (h->fork_ev) cudaEventDestroy(h->fork_ev);
+  if (h->bstream) { cudaStreamSynchronize(h->bstream); cudaStreamDestroy(h->bstream); }
+  for (int i = 0; i < 2; ++i) {
+    if (h->built_ev[i]) cudaEventDestroy(h->built_ev[i]);
+    if (h->solved_ev[i]) cudaEventDestroy(h->solved_ev[i]);
+  }
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
   delete h;
 }
@@ -859,10 +872,49 @@ wmd_status wmd_query_batch(wmd_handle* h, const int32_t* query_ids, const float*
   const bool dev_out = is_device_ptr(out_dist);
   if (!dev_out) CK(h, h->batch_dist.ensure((size_t)nq * h->N));
   float* dist = dev_out ? out_dist : h->batch_dist.p;
-  for (int32_t q = 0; q < nq; ++q) {
-    s = enqueue_query(h, h->bsel.p + (size_t)q * WMD_MAX_VR, h->brpad.p + (size_t)q * WMD_MAX_VR, nrow[q],
-                      lambda, iters, dist + (size_t)q * h->N);
-    if (s != WMD_OK) return s;
+  // Build/solve overlap: when every query takes the fused path, query q's
+  // table is built on the handle's build stream into one of two tables while query q-1 is
+  // solved on the main stream (the build is latency-bound and leaves most of the GPU idle).
+  bool overlap = nq > 1 && !h->opt_graph && h->opt_path != WMD_PATH_PER_ITER;
+  size_t mx_need = 0;
+  for (int32_t q = 0; overlap && q < nq; ++q) {
+    const int32_t ld = wmd::fused_ld(nrow[q], h->max_doc_nnz, h->tol >= 0.0);
+    if (ld <= 0) overlap = false;
+    mx_need = std::max(mx_need, (size_t)h->V * (ld + 4) + 128);
+  }
+  if (!overlap) {
+    for (int32_t q = 0; q < nq; ++q) {
+      s = enqueue_query(h, h->bsel.p + (size_t)q * WMD_MAX_VR, h->brpad.p + (size_t)q * WMD_MAX_VR, nrow[q],
+                        lambda, iters, dist + (size_t)q * h->N);
+      if (s != WMD_OK) return s;
+    }
+  } else {
+    CK(h, h->Mx.ensure(mx_need));
+    CK(h, h->Mx2.ensure(mx_need));
+    CK(h, cudaStreamWaitEvent(h->bstream, h->batch_ev, 0));  // the uploaded query rows
+    for (int32_t q = 0; q < nq; ++q) {
+      if (q > 0) std::swap(h->Mx, h->Mx2);  // h->Mx: the table of query q
+      const int32_t* d_sel = h->bsel.p + (size_t)q * WMD_MAX_VR;
+      const float* d_r = h->brpad.p + (size_t)q * WMD_MAX_VR;
+      bool fused = false;
+      int32_t ld = 0;
+      s = prepare_query(h, nrow[q], h->V, &fused, &ld);
+      if (s != WMD_OK) return s;
+      if (q >= 2) CK(h, cudaStreamWaitEvent(h->bstream, h->solved_ev[q & 1], 0));  // table free
+      cudaStream_t main = h->stream;
+      PhaseEvents* pe = new_phase_events(h);
+      h->stream = h->bstream;
+      s = record_build(h, d_sel, nrow[q], lambda, 0, h->V, fused, ld, pe);
+      h->stream = main;
+      if (s != WMD_OK) return s;
+      CK(h, cudaEventRecord(h->built_ev[q & 1], h->bstream));
+      CK(h, cudaStreamWaitEvent(main, h->built_ev[q & 1], 0));
+      int64_t launches = 0;
+      s = record_solve(h, d_r, nrow[q], lambda, iters, dist + (size_t)q * h->N, fused, ld, pe, &launches);
+      if (s != WMD_OK) return s;
+      CK(h, cudaEventRecord(h->solved_ev[q & 1], main));
+      note_query(h, d_sel, d_r, nrow[q], iters, fused, ld, launches + 1);
+    }
   }
   if (!dev_out) {
     CK(h, cudaMemcpyAsync(out_dist, dist, (size_t)nq * h->N * sizeof(float), cudaMemcpyDeviceToHost, st));
