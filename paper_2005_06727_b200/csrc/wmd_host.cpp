@@ -5,6 +5,7 @@
 // normalisation sums), sorts the query (Algorithm 1 line 1) and enqueues the
 // kernels of wmd_kernels.cu on the handle's stream. No arithmetic of the method runs here.
 #include <algorithm>
+#include <functional>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -104,8 +105,9 @@ struct wmd_handle {
   static constexpr int kLanes = 3;               // streams of the fused phase's length buckets
   cudaStream_t lanes[kLanes] = {};
   cudaEvent_t fork_ev = nullptr, join_ev[kLanes] = {};
-  cudaStream_t bstream = nullptr;                // wmd_query_batch: builds of the next queries
-  cudaEvent_t built_ev[2] = {}, solved_ev[2] = {};
+  cudaStream_t bstream = nullptr;                // builds of the next queries
+  bool opt_overlap = false;                      // single queries: overlap build(q+1) / solve(q)
+  cudaEvent_t built_ev = nullptr;
   // embeddings
   DevBuf<float> E;
   int64_t V = 0;
@@ -123,7 +125,12 @@ struct wmd_handle {
   DevBuf<float> rpad;        // WMD_MAX_VR (zero padded to ld)
   DevBuf<float> Kt;          // V * ld: K~ (FP32, vocab-major; per-iteration path only)
   DevBuf<float> Mx;          // V * (ld + 4): M rows + m_k (FP32, vocab-major)
-  DevBuf<float> Mx2;         // the second table of wmd_query_batch's build/solve overlap
+  // Query units: (Mx, sel, rpad, mx_free) and (Mx2, sel2, rpad2, mx2_free) swap per query in
+  // the overlapped paths, so the build of query q (build stream) overlaps the solve of q-1
+  DevBuf<float> Mx2;
+  DevBuf<int32_t> sel2;
+  DevBuf<float> rpad2;
+  cudaEvent_t mx_free = nullptr, mx2_free = nullptr;  // recorded after the unit's last solve
   bool kt_valid = false;     // Kt holds the last query's K~
   DevBuf<float> ua, ub;      // N * ld
   DevBuf<uint32_t> umask;    // N * ceil(ld/32): rows with an underflowed K~ entry, per doc
@@ -420,12 +427,15 @@ wmd_status wmd_create(const float* vocab_emb, int64_t V, int32_t d, int32_t devi
   if (cudaEventCreateWithFlags(&h->batch_ev, cudaEventDisableTiming) != cudaSuccess) return bail(WMD_ERR_CUDA);
   if (cudaEventCreateWithFlags(&h->fork_ev, cudaEventDisableTiming) != cudaSuccess) return bail(WMD_ERR_CUDA);
   if (cudaStreamCreateWithFlags(&h->bstream, cudaStreamNonBlocking) != cudaSuccess) return bail(WMD_ERR_CUDA);
-  for (int i = 0; i < 2; ++i)
-    if (cudaEventCreateWithFlags(&h->built_ev[i], cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&h->solved_ev[i], cudaEventDisableTiming) != cudaSuccess)
-      return bail(WMD_ERR_CUDA);
+  if (cudaEventCreateWithFlags(&h->built_ev, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->mx_free, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->mx2_free, cudaEventDisableTiming) != cudaSuccess ||
+      h->sel2.ensure(WMD_MAX_VR) != cudaSuccess || h->rpad2.ensure(WMD_MAX_VR) != cudaSuccess)
+    return bail(WMD_ERR_CUDA);
+  int prio_lo = 0, prio_hi = 0;  // the bucket lanes get the highest priority: the overlapped build
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);  // of the next query only fills gaps
   for (int i = 0; i < wmd_handle::kLanes; ++i)
-    if (cudaStreamCreateWithFlags(&h->lanes[i], cudaStreamNonBlocking) != cudaSuccess ||
+    if (cudaStreamCreateWithPriority(&h->lanes[i], cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
         cudaEventCreateWithFlags(&h->join_ev[i], cudaEventDisableTiming) != cudaSuccess)
       return bail(WMD_ERR_CUDA);
   for (int s = 0; s < 2; ++s) {
@@ -463,10 +473,10 @@ void wmd_destroy(wmd_handle* h) {
   }
   if (h->fork_ev) cudaEventDestroy(h->fork_ev);
   if (h->bstream) { cudaStreamSynchronize(h->bstream); cudaStreamDestroy(h->bstream); }
-  for (int i = 0; i < 2; ++i) {
-    if (h->built_ev[i]) cudaEventDestroy(h->built_ev[i]);
-    if (h->solved_ev[i]) cudaEventDestroy(h->solved_ev[i]);
-  }
+  if (h->built_ev) cudaEventDestroy(h->built_ev);
+  if (h->mx_free) cudaEventDestroy(h->mx_free);
+  if (h->mx2_free) cudaEventDestroy(h->mx2_free);
+  h->sel2.release(); h->rpad2.release();
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
   delete h;
 }
@@ -727,6 +737,51 @@ void note_query(wmd_handle* h, const int32_t* d_sel, const float* d_r, int32_t v
 // to WMD_MAX_VR) are already on the device. dist: device, N floats. Asynchronous on the handle's
 // stream. With WMD_OPT_GRAPH (and no timing) the stream work is captured once per distinct
 // (rows, output, lambda, iters, tolerance, path, options) and replayed as a CUDA graph.
+void swap_units(wmd_handle* h) {
+  std::swap(h->Mx, h->Mx2);
+  std::swap(h->sel, h->sel2);
+  std::swap(h->rpad, h->rpad2);
+  std::swap(h->mx_free, h->mx2_free);
+}
+
+// One fused-path query with its build on the build stream (after the unit's previous solve
+// freed it) and its solve on the main stream: consecutive queries overlap build and solve.
+// `upload` enqueues the copies of the query rows into d_sel / d_r on the given stream (or is
+// empty when they are already on the device). Returns false through *ok if the query does not
+// take the fused path (nothing enqueued).
+wmd_status enqueue_overlapped(wmd_handle* h, const int32_t* d_sel, const float* d_r, int32_t v_r, float lambda,
+                              int32_t iters, float* dist, const std::function<wmd_status(cudaStream_t)>& upload) {
+  bool fused = false;
+  int32_t ld = 0;
+  wmd_status s = prepare_query(h, v_r, h->V, &fused, &ld);
+  if (s != WMD_OK) return s;
+  cudaStream_t main = h->stream;
+  CK(h, cudaStreamWaitEvent(h->bstream, h->mx_free, 0));  // the unit's previous solve is done
+  if (upload) {
+    s = upload(h->bstream);
+    if (s != WMD_OK) return s;
+  }
+  PhaseEvents* pe = new_phase_events(h);
+  h->stream = h->bstream;
+  s = record_build(h, d_sel, v_r, lambda, 0, h->V, fused, ld, pe);
+  h->stream = main;
+  if (s != WMD_OK) return s;
+  CK(h, cudaEventRecord(h->built_ev, h->bstream));
+  CK(h, cudaStreamWaitEvent(main, h->built_ev, 0));
+  // phase timing: the solve starts here (build_ms then includes any wait for the previous solve)
+  if (pe) CK(h, cudaEventRecord(pe->ev[1], main));
+  int64_t launches = 0;
+  s = record_solve(h, d_r, v_r, lambda, iters, dist, fused, ld, pe, &launches);
+  if (s != WMD_OK) return s;
+  CK(h, cudaEventRecord(h->mx_free, main));
+  note_query(h, d_sel, d_r, v_r, iters, fused, ld, launches + 1);
+  return WMD_OK;
+}
+
+bool overlap_ok(wmd_handle* h, int32_t v_r) {
+  return !h->opt_graph && h->opt_path != WMD_PATH_PER_ITER && wmd::fused_ld(v_r, h->max_doc_nnz, h->tol >= 0.0) > 0;
+}
+
 wmd_status enqueue_query(wmd_handle* h, const int32_t* d_sel, const float* d_r, int32_t v_r,
                          float lambda, int32_t iters, float* dist) {
   bool fused = false;
@@ -808,14 +863,26 @@ wmd_status wmd_query(wmd_handle* h, const int32_t* query_ids, const float* query
   float* sr = (float*)((char*)h->stage[slot] + WMD_MAX_VR * 4);
   std::memset(h->stage[slot], 0, WMD_MAX_VR * 8);
   for (int32_t i = 0; i < n; ++i) { ssel[i] = h->h_sel[i]; sr[i] = h->h_r[i]; }
-  CK(h, cudaMemcpyAsync(h->sel.p, ssel, WMD_MAX_VR * 4, cudaMemcpyHostToDevice, st));
-  CK(h, cudaMemcpyAsync(h->rpad.p, sr, WMD_MAX_VR * 4, cudaMemcpyHostToDevice, st));
-  CK(h, cudaEventRecord(h->stage_ev[slot], st));
-
   const bool dev_out = is_device_ptr(out_dist);
   float* dist = dev_out ? out_dist : h->dist_tmp.p;
-  s = enqueue_query(h, h->sel.p, h->rpad.p, n, lambda, iters, dist);
-  if (s != WMD_OK) return s;
+  if (h->opt_overlap && overlap_ok(h, n)) {
+    // the other query unit: its build (and the upload) overlap the previous query's solve
+    // (off by default: measured slower at Scaling, the build's blocks delay the solve's)
+    swap_units(h);
+    s = enqueue_overlapped(h, h->sel.p, h->rpad.p, n, lambda, iters, dist, [&](cudaStream_t us) -> wmd_status {
+      CK(h, cudaMemcpyAsync(h->sel.p, ssel, WMD_MAX_VR * 4, cudaMemcpyHostToDevice, us));
+      CK(h, cudaMemcpyAsync(h->rpad.p, sr, WMD_MAX_VR * 4, cudaMemcpyHostToDevice, us));
+      CK(h, cudaEventRecord(h->stage_ev[slot], us));
+      return WMD_OK;
+    });
+    if (s != WMD_OK) return s;
+  } else {
+    CK(h, cudaMemcpyAsync(h->sel.p, ssel, WMD_MAX_VR * 4, cudaMemcpyHostToDevice, st));
+    CK(h, cudaMemcpyAsync(h->rpad.p, sr, WMD_MAX_VR * 4, cudaMemcpyHostToDevice, st));
+    CK(h, cudaEventRecord(h->stage_ev[slot], st));
+    s = enqueue_query(h, h->sel.p, h->rpad.p, n, lambda, iters, dist);
+    if (s != WMD_OK) return s;
+  }
   if (!dev_out) {
     CK(h, cudaMemcpyAsync(out_dist, dist, h->N * sizeof(float), cudaMemcpyDeviceToHost, st));
     CK(h, cudaStreamSynchronize(st));
@@ -875,7 +942,7 @@ wmd_status wmd_query_batch(wmd_handle* h, const int32_t* query_ids, const float*
   // Build/solve overlap: when every query takes the fused path, query q's
   // table is built on the handle's build stream into one of two tables while query q-1 is
   // solved on the main stream (the build is latency-bound and leaves most of the GPU idle).
-  bool overlap = nq > 1 && !h->opt_graph && h->opt_path != WMD_PATH_PER_ITER;
+  bool overlap = nq > 1 && !h->opt_graph && h->opt_path != WMD_PATH_PER_ITER;  // (see overlap_ok)
   size_t mx_need = 0;
   for (int32_t q = 0; overlap && q < nq; ++q) {
     const int32_t ld = wmd::fused_ld(nrow[q], h->max_doc_nnz, h->tol >= 0.0);
@@ -893,27 +960,10 @@ wmd_status wmd_query_batch(wmd_handle* h, const int32_t* query_ids, const float*
     CK(h, h->Mx2.ensure(mx_need));
     CK(h, cudaStreamWaitEvent(h->bstream, h->batch_ev, 0));  // the uploaded query rows
     for (int32_t q = 0; q < nq; ++q) {
-      if (q > 0) std::swap(h->Mx, h->Mx2);  // h->Mx: the table of query q
-      const int32_t* d_sel = h->bsel.p + (size_t)q * WMD_MAX_VR;
-      const float* d_r = h->brpad.p + (size_t)q * WMD_MAX_VR;
-      bool fused = false;
-      int32_t ld = 0;
-      s = prepare_query(h, nrow[q], h->V, &fused, &ld);
+      swap_units(h);
+      s = enqueue_overlapped(h, h->bsel.p + (size_t)q * WMD_MAX_VR, h->brpad.p + (size_t)q * WMD_MAX_VR,
+                             nrow[q], lambda, iters, dist + (size_t)q * h->N, nullptr);
       if (s != WMD_OK) return s;
-      if (q >= 2) CK(h, cudaStreamWaitEvent(h->bstream, h->solved_ev[q & 1], 0));  // table free
-      cudaStream_t main = h->stream;
-      PhaseEvents* pe = new_phase_events(h);
-      h->stream = h->bstream;
-      s = record_build(h, d_sel, nrow[q], lambda, 0, h->V, fused, ld, pe);
-      h->stream = main;
-      if (s != WMD_OK) return s;
-      CK(h, cudaEventRecord(h->built_ev[q & 1], h->bstream));
-      CK(h, cudaStreamWaitEvent(main, h->built_ev[q & 1], 0));
-      int64_t launches = 0;
-      s = record_solve(h, d_r, nrow[q], lambda, iters, dist + (size_t)q * h->N, fused, ld, pe, &launches);
-      if (s != WMD_OK) return s;
-      CK(h, cudaEventRecord(h->solved_ev[q & 1], main));
-      note_query(h, d_sel, d_r, nrow[q], iters, fused, ld, launches + 1);
     }
   }
   if (!dev_out) {
