@@ -167,10 +167,13 @@ constexpr int TC_M = 128;             // vocabulary rows per block (MMA M, TMEM 
 // d chunk (floats) and layout per query-tile width: swizzled 32-float chunks up to
 // WMD_TC_SWZ_MAX query rows, no-swizzle 16-float chunks beyond (shared memory per stage)
 #ifndef WMD_TC_SWZ_MAX
-#define WMD_TC_SWZ_MAX 32
+#define WMD_TC_SWZ_MAX 128
 #endif
-template <int NP> constexpr bool tc_swz() { return NP <= WMD_TC_SWZ_MAX; }
-template <int NP> constexpr int tc_k() { return tc_swz<NP>() ? 32 : 16; }
+#ifndef WMD_TC_SWZ_BYTES  // swizzle span of the swizzled layout: 128 (32-float chunks) or 64 (16)
+#define WMD_TC_SWZ_BYTES 64
+#endif
+template <int NP> constexpr int tc_swz() { return NP <= WMD_TC_SWZ_MAX ? WMD_TC_SWZ_BYTES : 0; }
+template <int NP> constexpr int tc_k() { return tc_swz<NP>() ? tc_swz<NP>() / 4 : 16; }
 #ifndef WMD_TC_STAGES
 #define WMD_TC_STAGES 3
 #endif
@@ -186,14 +189,18 @@ __device__ __forceinline__ uint32_t su32(const void* p) {
 }
 // byte offset of element (r, k) (k < 32) in a K-major no-swizzle tile of R rows: core matrices
 // of 8 rows x 4 floats; SBO = 128 B between 8-row groups, LBO = R/8 * 128 B between K quads
-// Operand layouts (K-major). SWZ: SWIZZLE_128B with 32-float chunks (one 128-byte row): 8-row
-// atoms of 1024 B, the 16-byte piece j of row r stored at piece j ^ (r % 8) (the tensor core
-// undoes the XOR; conflict-free). Else the no-swizzle core-matrix layout with 16-float chunks:
-// core matrices of 8 rows x 16 B, SBO = 128 B, LBO = R / 8 * 128 B (half the shared memory per
-// stage, which keeps two 128-query-row blocks per SM).
-template <bool SWZ>
+// Operand layouts (K-major). SWZ = 64 (default): SWIZZLE_64B with 16-float chunks (one 64-byte
+// row): 8-row atoms of 512 B, piece j of row r stored at piece j ^ ((r >> 1) % 4); SWZ = 128:
+// SWIZZLE_128B with 32-float chunks, 1024-B atoms, piece j at j ^ (r % 8) (the tensor core undoes
+// the XOR; conflict-free either way); SWZ = 0: the no-swizzle core-matrix layout (8 rows x 16 B,
+// SBO = 128 B, LBO = R / 8 * 128 B), which measured slowest. The 64-byte chunks halve the shared
+// memory per stage: four 32-query-row blocks per SM (latency-bound on the MMA-completion wait,
+// so occupancy is what counts: Scaling 0.30 (no swizzle) -> 0.26 (128 B) -> 0.19 ms (64 B)).
+template <int SWZ>
 __device__ __forceinline__ uint32_t km_off(int r, int k, int R) {
-  if constexpr (SWZ) return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((((k >> 2) ^ r) & 7) << 4) + (k & 3) * 4);
+  if constexpr (SWZ == 128) return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((((k >> 2) ^ r) & 7) << 4) + (k & 3) * 4);
+  // SWIZZLE_64B: 64-byte rows, 8-row atoms of 512 B, piece j of row r at j ^ ((r >> 1) & 3)
+  else if constexpr (SWZ == 64) return (uint32_t)((r >> 3) * 512 + (r & 7) * 64 + ((((k >> 2) ^ (r >> 1)) & 3) << 4) + (k & 3) * 4);
   else return (uint32_t)((k >> 2) * (R / 8 * 128) + (r >> 3) * 128 + (r & 7) * 16 + (k & 3) * 4);
 }
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -204,6 +211,11 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
 __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
   return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// SWIZZLE_64B K-major: SBO = 512 B between 8-row atoms, layout type 4
+__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(512 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
 }
 __device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
   asm volatile(
@@ -234,10 +246,10 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 }
 
 template <int NP>
-__global__ void __launch_bounds__(128, NP <= 32 ? 2 : 1) build_mx_tc_kernel(
+__global__ void __launch_bounds__(128, NP <= 32 ? (WMD_TC_SWZ_BYTES == 64 ? 4 : 2) : (NP <= 64 && WMD_TC_SWZ_MAX >= 64 ? 2 : 1)) build_mx_tc_kernel(
     const float* __restrict__ E, int64_t row0, int64_t V, int dp, const int32_t* __restrict__ sel,
     int v_r, int ld, float lambda, float* __restrict__ Kt, float* __restrict__ Mx) {
-  constexpr bool SWZ = tc_swz<NP>();
+  constexpr int SWZ = tc_swz<NP>();
   constexpr int TC_K = tc_k<NP>();
   constexpr int A_BYTES = TC_M * TC_K * 4, B_BYTES = NP * TC_K * 4;
   constexpr int STAGE = A_BYTES + B_BYTES;                  // one chunk: A rows, then B rows
@@ -350,9 +362,12 @@ __global__ void __launch_bounds__(128, NP <= 32 ? 2 : 1) build_mx_tc_kernel(
 #pragma unroll
         for (int kk = 0; kk < TC_K; kk += 8) {
           uint64_t da, db;
-          if constexpr (SWZ) {
+          if constexpr (SWZ == 128) {
             da = umma_desc_sw128(a + 4 * kk);
             db = umma_desc_sw128(b + 4 * kk);
+          } else if constexpr (SWZ == 64) {
+            da = umma_desc_sw64(a + 4 * kk);
+            db = umma_desc_sw64(b + 4 * kk);
           } else {
             da = umma_desc(a + (kk >> 2) * (TC_M / 8 * 128), TC_M / 8 * 128, 128);
             db = umma_desc(b + (kk >> 2) * (NP / 8 * 128), NP / 8 * 128, 128);
