@@ -148,3 +148,25 @@ def test_fused_kernels_keep_the_block_in_registers(W):
     sass = subprocess.run(["cuobjdump", "-sass", obj], capture_output=True, text=True).stdout
     if sass:
         assert "slowpath" not in sass and " CALL" not in sass
+
+
+def _build_c_consumer(W, tmp_path):
+    """Compile tests/c/abi_consumer.c with gcc against include/wmd.h, linked to the in-tree
+    library (no Python or torch in the consumer)."""
+    import subprocess
+    exe = str(tmp_path / "abi_consumer")
+    lib_dir = os.path.dirname(W.LIB_PATH)
+    cmd = ["gcc", "-O1", "-std=c11", "-I", os.path.join(ROOT, "include"),
+           os.path.join(ROOT, "tests", "c", "abi_consumer.c"), "-o", exe,
+           lib_dir + "/libwmd_b200.so", "-Wl,-rpath," + lib_dir, "-lm"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    assert res.returncode == 0, res.stderr
+    return exe
+
+
+def test_plain_c_consumer_links_and_runs_host_entry_points(W, tmp_path):
+    import subprocess
+    exe = _build_c_consumer(W, tmp_path)
+    res = subprocess.run([exe], capture_output=True, text=True, timeout=60)
+    assert res.returncode == 0, res.stdout + res.stderr
+    assert "abi_consumer host ok" in res.stdout

@@ -805,3 +805,14 @@ def test_two_phase_errors(W):
         assert e.value.status == W.WMD_ERR_INVALID_ARGUMENT
     finally:
         W.wmd_destroy(h)
+
+
+def test_plain_c_consumer_query(W, tmp_path):
+    """The C ABI from a plain C program (tests/c/abi_consumer.c): one query on the GPU, checked
+    in C against the single-query-word closed form (sum_e c_e M_e)."""
+    import subprocess
+    import test_abi_host
+    exe = test_abi_host._build_c_consumer(W, tmp_path)
+    res = subprocess.run([exe, "gpu"], capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stdout + res.stderr
+    assert "abi_consumer gpu ok" in res.stdout
