@@ -106,7 +106,6 @@ struct wmd_handle {
   cudaStream_t lanes[kLanes] = {};
   cudaEvent_t fork_ev = nullptr, join_ev[kLanes] = {};
   cudaStream_t bstream = nullptr;                // builds of the next queries
-  bool opt_overlap = false;                      // single queries: overlap build(q+1) / solve(q)
   cudaEvent_t built_ev = nullptr;
   // embeddings
   DevBuf<float> E;
@@ -778,9 +777,6 @@ wmd_status enqueue_overlapped(wmd_handle* h, const int32_t* d_sel, const float* 
   return WMD_OK;
 }
 
-bool overlap_ok(wmd_handle* h, int32_t v_r) {
-  return !h->opt_graph && h->opt_path != WMD_PATH_PER_ITER && wmd::fused_ld(v_r, h->max_doc_nnz, h->tol >= 0.0) > 0;
-}
 
 wmd_status enqueue_query(wmd_handle* h, const int32_t* d_sel, const float* d_r, int32_t v_r,
                          float lambda, int32_t iters, float* dist) {
@@ -865,24 +861,13 @@ wmd_status wmd_query(wmd_handle* h, const int32_t* query_ids, const float* query
   for (int32_t i = 0; i < n; ++i) { ssel[i] = h->h_sel[i]; sr[i] = h->h_r[i]; }
   const bool dev_out = is_device_ptr(out_dist);
   float* dist = dev_out ? out_dist : h->dist_tmp.p;
-  if (h->opt_overlap && overlap_ok(h, n)) {
-    // the other query unit: its build (and the upload) overlap the previous query's solve
-    // (off by default: measured slower at Scaling, the build's blocks delay the solve's)
-    swap_units(h);
-    s = enqueue_overlapped(h, h->sel.p, h->rpad.p, n, lambda, iters, dist, [&](cudaStream_t us) -> wmd_status {
-      CK(h, cudaMemcpyAsync(h->sel.p, ssel, WMD_MAX_VR * 4, cudaMemcpyHostToDevice, us));
-      CK(h, cudaMemcpyAsync(h->rpad.p, sr, WMD_MAX_VR * 4, cudaMemcpyHostToDevice, us));
-      CK(h, cudaEventRecord(h->stage_ev[slot], us));
-      return WMD_OK;
-    });
-    if (s != WMD_OK) return s;
-  } else {
-    CK(h, cudaMemcpyAsync(h->sel.p, ssel, WMD_MAX_VR * 4, cudaMemcpyHostToDevice, st));
-    CK(h, cudaMemcpyAsync(h->rpad.p, sr, WMD_MAX_VR * 4, cudaMemcpyHostToDevice, st));
-    CK(h, cudaEventRecord(h->stage_ev[slot], st));
-    s = enqueue_query(h, h->sel.p, h->rpad.p, n, lambda, iters, dist);
-    if (s != WMD_OK) return s;
-  }
+  // (single queries run build and solve on one stream: overlapping the next query's build with
+  // this solve, as wmd_query_batch does, measured slower at Scaling)
+  CK(h, cudaMemcpyAsync(h->sel.p, ssel, WMD_MAX_VR * 4, cudaMemcpyHostToDevice, st));
+  CK(h, cudaMemcpyAsync(h->rpad.p, sr, WMD_MAX_VR * 4, cudaMemcpyHostToDevice, st));
+  CK(h, cudaEventRecord(h->stage_ev[slot], st));
+  s = enqueue_query(h, h->sel.p, h->rpad.p, n, lambda, iters, dist);
+  if (s != WMD_OK) return s;
   if (!dev_out) {
     CK(h, cudaMemcpyAsync(out_dist, dist, h->N * sizeof(float), cudaMemcpyDeviceToHost, st));
     CK(h, cudaStreamSynchronize(st));
@@ -942,7 +927,7 @@ wmd_status wmd_query_batch(wmd_handle* h, const int32_t* query_ids, const float*
   // Build/solve overlap: when every query takes the fused path, query q's
   // table is built on the handle's build stream into one of two tables while query q-1 is
   // solved on the main stream (the build is latency-bound and leaves most of the GPU idle).
-  bool overlap = nq > 1 && !h->opt_graph && h->opt_path != WMD_PATH_PER_ITER;  // (see overlap_ok)
+  bool overlap = nq > 1 && !h->opt_graph && h->opt_path != WMD_PATH_PER_ITER;
   size_t mx_need = 0;
   for (int32_t q = 0; overlap && q < nq; ++q) {
     const int32_t ld = wmd::fused_ld(nrow[q], h->max_doc_nnz, h->tol >= 0.0);
