@@ -72,6 +72,9 @@ struct Shape {
 #ifndef WMD_FUSED_DOCS_PER_WARP
 #define WMD_FUSED_DOCS_PER_WARP 1
 #endif
+#ifndef WMD_STREAM_ENTRIES
+#define WMD_STREAM_ENTRIES 1
+#endif
 #ifndef WMD_FUSED_REG_SLACK
 #define WMD_FUSED_REG_SLACK 8
 #endif
@@ -109,6 +112,12 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW, D>()) sinkhor
   for (int d = 0; d < D; ++d) buf[d] = smem + (wib * D + d) * S::BUF;
   const int64_t stride = (int64_t)gridDim.x * kWarps * D;
   const uint64_t keep = l2_evict_last_policy();
+#if WMD_STREAM_ENTRIES  // c is read once: evict_first, so the Mx rows keep their L2 lines
+  const uint64_t stream_pol = l2_evict_first_policy();
+#define WMD_ENT_LOAD(p) ldg_guarded_stream((p), stream_pol)
+#else
+#define WMD_ENT_LOAD(p) ldg_guarded(p)
+#endif
   const int2* ent2 = reinterpret_cast<const int2*>(ent);
   const float alpha = lambda * kLog2e;          // exp(-lambda x) = 2^(-alpha x)
   const float kv_s = (float)v_r * kUnder;
@@ -149,7 +158,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW, D>()) sinkhor
       for (int w = 0; w < NW; ++w) {
         const int e = lane + 32 * w;
         int2 x = make_int2(0, 0);
-        if (e < pn[d]) x = ldg_guarded(ent2 + pb[d] + e);
+        if (e < pn[d]) x = WMD_ENT_LOAD(ent2 + pb[d] + e);
         pk[d][w] = x.x;
         pc[d][w] = __int_as_float(x.y);
       }
