@@ -109,6 +109,8 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W, TW>()) sinkhorn_
   const int a = lane >> 3, b = lane & 7;
   const int row0 = RPW * warp;                             // first row of this warp's block
   const int2* ent2 = reinterpret_cast<const int2*>(ent);
+  const uint64_t keep = l2_evict_last_policy();         // the gathered M rows stay in L2
+  const uint64_t stream_pol = l2_evict_first_policy();  // the entries are read once
   const float alpha = lambda * kLog2eC;
   const float ia = -rcp_fast(alpha);  // (approximate: no IEEE-division slow-path call)
   const float kv_s = (float)v_r * kUnderC;
@@ -152,7 +154,7 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W, TW>()) sinkhorn_
 #pragma unroll
     for (int x = 0; x < EPT; ++x) {
       const int e = tid + NT * x;
-      const int2 v = __ldg(ent2 + pb + (e < pn ? e : 0));
+      const int2 v = ldg2_hint(ent2 + pb + (e < pn ? e : 0), stream_pol);  // read once
       pe[x] = e < pn ? v : make_int2(0, 0);
     }
   };
@@ -182,7 +184,7 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W, TW>()) sinkhorn_
       float x[CW];
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
-        const float4 t = __ldg(reinterpret_cast<const float4*>(row + 32 * q + 4 * b));
+        const float4 t = ldg4_hint(reinterpret_cast<const float4*>(row + 32 * q + 4 * b), keep);
         x[4 * q] = t.x; x[4 * q + 1] = t.y; x[4 * q + 2] = t.z; x[4 * q + 3] = t.w;
       }
 #pragma unroll
