@@ -3,12 +3,12 @@
 # then the launch lists of the bench commands
 set -x
 python -m paper_2005_06727_b200.build > gpurun_out/build.log 2>&1 || exit 1
-mkdir -p /tmp/reps gpurun_out/prof
+rm -rf /tmp/reps; mkdir -p /tmp/reps gpurun_out/prof
 python tools/pass_timing.py scaling auto 1 > gpurun_out/prof/plain_scaling.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:sinkhorn_fused -s 6 -c 3 -o /tmp/reps/r01_full_scaling_fused python tools/pass_timing.py scaling auto 1 > gpurun_out/prof/ncu1.log 2>&1; echo ncu1=$?
+ncu -f --set full --clock-control none --import-source on -k regex:sinkhorn_fused -s 6 -c 3 -o /tmp/reps/r01_full_scaling_fused python tools/pass_timing.py scaling auto 1 > gpurun_out/prof/ncu1.log 2>&1; echo ncu1=$?
 python tools/pass_timing.py long auto 1 > gpurun_out/prof/plain_long.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:sinkhorn_cta -s 10 -c 5 -o /tmp/reps/r01_full_long_cta python tools/pass_timing.py long auto 1 > gpurun_out/prof/ncu2.log 2>&1; echo ncu2=$?
-ncu --set full --clock-control none --import-source on -k regex:build_mx_tc -s 2 -c 1 -o /tmp/reps/r01_full_scaling_build python tools/pass_timing.py scaling auto 1 > gpurun_out/prof/ncu3.log 2>&1; echo ncu3=$?
+ncu -f --set full --clock-control none --import-source on -k regex:sinkhorn_cta -s 10 -c 5 -o /tmp/reps/r01_full_long_cta python tools/pass_timing.py long auto 1 > gpurun_out/prof/ncu2.log 2>&1; echo ncu2=$?
+ncu -f --set full --clock-control none --import-source on -k regex:build_mx_tc -s 2 -c 1 -o /tmp/reps/r01_full_scaling_build python tools/pass_timing.py scaling auto 1 > gpurun_out/prof/ncu3.log 2>&1; echo ncu3=$?
 for r in r01_full_scaling_fused r01_full_long_cta r01_full_scaling_build; do
   python tools/ncu_summary.py /tmp/reps/$r.ncu-rep --raw > gpurun_out/prof/${r}_summary.txt 2>&1
 done
