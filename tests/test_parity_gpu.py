@@ -816,3 +816,33 @@ def test_plain_c_consumer_query(W, tmp_path):
     res = subprocess.run([exe, "gpu"], capture_output=True, text=True, timeout=300)
     assert res.returncode == 0, res.stdout + res.stderr
     assert "abi_consumer gpu ok" in res.stdout
+
+
+@pytest.mark.parametrize("case", range(12))
+def test_random_shapes_against_oracle(W, case):
+    """Seeded random shapes across every kernel family: query width 1-128, 40 documents of
+    1-320 words (mixed lengths, so one query runs the one-warp buckets, the one-CTA buckets and
+    the re-runs together), lambda in {0.5, 5, 10, 25}, 0-30 iterations."""
+    rng = np.random.default_rng(9000 + case)
+    wl = synth.make_workload("tweet", n_queries=0, N=10)
+    V = wl.cfg.V
+    v_r = int(rng.integers(1, 129))
+    lengths = [int(x) for x in rng.integers(1, 321, size=40)]
+    lengths[:3] = [1, 16, 64]
+    cp, ri, va = _docs_with_lengths(V, lengths, seed=9100 + case)
+    q = np.sort(rng.choice(4000, v_r, replace=False)).astype(np.int32)
+    cnt = rng.geometric(0.5, v_r).astype(np.float64)
+    w = (cnt / cnt.sum()).astype(np.float32)
+    lam = float(rng.choice([0.5, 5.0, 10.0, 25.0]))
+    iters = int(rng.choice([0, 1, 7, 30]))
+    h = W.wmd_create(wl.E)
+    try:
+        W.wmd_set_targets(h, cp, ri, va)
+        d = np.empty(cp.shape[0] - 1, np.float32)
+        W.wmd_query(h, q, w, lam, iters, d)
+        W.wmd_sync(h)
+        assert W.wmd_get_stats(h)["last_path"] == W.WMD_PATH_FUSED
+    finally:
+        W.wmd_destroy(h)
+    o = oracle.sinkhorn_wmd(wl.E, cp, ri, va, q, w, lam, iters)
+    assert_parity(d, o, f"random case {case}: v_r={v_r} lambda={lam} iters={iters}")
