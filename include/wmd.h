@@ -158,8 +158,11 @@ WMD_API wmd_status wmd_query(wmd_handle* h, const int32_t* query_ids, const floa
  * out_dist: nq x N floats row-major (row q = query q), host or device as in wmd_query.
  * Every query is validated before any work is enqueued (all-or-nothing; the message names the
  * first bad query). The rows of all queries go to the device in one copy; the queries then run
- * back to back on the handle's stream (each: build, Sinkhorn, final, FP64 fallback), with no
- * host round trip between them. Results equal nq separate wmd_query calls bit for bit.
+ * back to back with no host round trip between them (each: build, Sinkhorn, final, re-runs).
+ * When every query takes the fused path (and graph mode is off), query q's table is built on a
+ * second internal stream into one of two tables while query q-1 is solved on the handle's
+ * stream; the call's work is complete on the handle's stream when it returns (device output) or
+ * synchronised (host output). Results equal nq separate wmd_query calls bit for bit.
  * Errors: as wmd_query, plus INVALID_ARGUMENT for nq < 1 or bad q_ptr. */
 WMD_API wmd_status wmd_query_batch(wmd_handle* h, const int32_t* query_ids, const float* query_weights,
                            const int64_t* q_ptr, int32_t nq, float lambda, int32_t iters,
