@@ -66,9 +66,10 @@ typedef enum {
 
 /* Execution path of the Sinkhorn loop (wmd_set_option(WMD_OPT_PATH, ...)). */
 typedef enum {
-  WMD_PATH_AUTO = 0,       /* library choice: WMD_PATH_FUSED when it supports the shape (v_r <= 128 and
+  WMD_PATH_AUTO = 0,       /* library choice: WMD_PATH_FUSED when it supports the shape (v_r <= 128,
                               every document <= 320 words; <= 64 words while a stopping tolerance is
-                              set), else WMD_PATH_PER_ITER */
+                              set; lambda >= 1e-3, below which its final step's recovery of M from
+                              the FP32 block loses accuracy), else WMD_PATH_PER_ITER */
   WMD_PATH_PER_ITER = 1,   /* one fused SDDMM_SpMM launch per iteration + final kernel */
   WMD_PATH_FUSED = 2       /* all iterations + final in one launch per length bucket, per-document
                               state on chip (one warp per document up to 64 words, one CTA per
@@ -85,9 +86,27 @@ typedef enum {
                               tolerance, path, output pointer and buffers repeat (the query rows are
                               re-uploaded every call); per-phase timing is off in this mode.
                               Default 0 */
-  WMD_OPT_BUILD = 5        /* distance build (a2): 0 = tensor cores, 3xTF32 GEMM form (default);
-                              1 = SIMT direct difference (PAPER.md:259-268 compares the two forms) */
+  WMD_OPT_BUILD = 5,       /* distance build (a2), a wmd_build value; default WMD_BUILD_DIRECT */
+  WMD_OPT_LAYOUT_DOC_NNZ = 6 /* >= 0: the path and table-width decision of every query assumes the
+                              longest document has max(this, local longest) words. A document-
+                              sharded run passes the GLOBAL longest document on every
+                              rank, so all ranks pick the same path and row width (their tables
+                              are then all-gatherable and their results bitwise equal to an
+                              unsharded run). Default 0 (the local targets decide) */
 } wmd_option;
+
+/* Distance build (a2) kernels, wmd_set_option(WMD_OPT_BUILD, ...). PAPER.md:259-268 (§6) compares
+ * a dot-type and a GEMM-type distance kernel; both are here:
+ *  WMD_BUILD_DIRECT: M_ik = sqrt(sum_t (E[sel_i,t] - E[k,t])^2) in FP32 SIMT (direct difference).
+ *    Accurate for any embedding geometry (relative error of M ~1e-7); the default.
+ *  WMD_BUILD_TENSOR_CORE: M^2 = |e|^2 + |q|^2 - 2 e.q with e.q on the tcgen05 tensor cores in
+ *    3xTF32, near pairs recomputed directly. Faster, but the expansion's absolute error
+ *    ~eps (|e|^2 + |q|^2) reaches lambda*dM ~ 1e-2 on clustered embeddings of varied norm, where
+ *    distances end up ~1e-4 off (R34); accurate on isotropic (N(0,1)-like) data. */
+typedef enum {
+  WMD_BUILD_TENSOR_CORE = 0,
+  WMD_BUILD_DIRECT = 1
+} wmd_build;
 
 typedef struct {
   int64_t queries;           /* wmd_query calls since create / wmd_reset_stats */
@@ -217,7 +236,9 @@ WMD_API wmd_status wmd_reset_stats(wmd_handle* h);
  * wmd_read_scaling: u after the last iteration, documents [j0, j0+count), ld floats each
  *   (gauge-scaled: only ratios within a document are meaningful). Per-iteration path only.
  * wmd_read_flags: flags[N] (bit0: FP32 iterate left the normal range; bit1: FP64 re-run;
- *   bit2: re-run in FP32 by the one-CTA kernel with re-anchoring, R33). */
+ *   bit2: re-run in FP32 by the one-CTA kernel with re-anchoring, R33; bit4: the
+ *   one-warp kernel's FP32 block had entries below FLT_MIN, so its range certificate was in
+ *   force). */
 WMD_API wmd_status wmd_get_query_rows(wmd_handle* h, int32_t* sel, float* r);
 WMD_API wmd_status wmd_read_kernel(wmd_handle* h, int64_t k0, int64_t count, float* ktilde, float* m,
                            float* colmin);

@@ -57,6 +57,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = Non
         if s.endswith(".cpp"):
             cuda_inc = os.path.join(os.path.dirname(os.path.dirname(nvcc)), "include")
             cmd = ["g++", "-O2", "-std=c++17", "-fPIC", "-fvisibility=hidden", "-Wall",
+                   *[f"-D{d}" for d in defines],
                    "-I", os.path.join(ROOT, "include"), "-I", cuda_inc, "-c", src, "-o", obj]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
@@ -78,6 +79,25 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = Non
         raise RuntimeError(f"link failed:\n{res.stderr}")
     os.replace(tmp, lib)
     return lib
+
+
+ROOFBENCH_SRC = os.path.join(ROOT, "tools", "microbench", "roofbench.cu")
+ROOFBENCH_LIB = os.path.join(ROOT, "tools", "microbench", "libroofbench.so")
+
+
+def build_roofbench(force: bool = False) -> str:
+    """bench.py's in-run roofline microbenchmarks (L2 row gathers, HBM stream, FP32 FMA):
+    a measurement tool outside the product library, built the same way (sm_100a, in-tree)."""
+    if not force and os.path.exists(ROOFBENCH_LIB) and os.path.getmtime(ROOFBENCH_LIB) >= os.path.getmtime(ROOFBENCH_SRC):
+        return ROOFBENCH_LIB
+    tmp = ROOFBENCH_LIB + ".tmp"
+    cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+           "-Xcompiler", "-fPIC", "-shared", "-cudart", "static", "-o", tmp, ROOFBENCH_SRC]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"nvcc failed for roofbench.cu:\n{res.stderr}")
+    os.replace(tmp, ROOFBENCH_LIB)
+    return ROOFBENCH_LIB
 
 
 if __name__ == "__main__":

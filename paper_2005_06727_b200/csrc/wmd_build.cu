@@ -455,11 +455,8 @@ void launch_build_ktilde(const float* E, int64_t row0, int64_t row1, int dp, con
   if (!use_tc) {
     constexpr size_t smem = sizeof(float) * 2 * kStageFloats;
     static_assert(BW * kMsPitch <= 2 * kStageFloats, "M tile must fit in the staging buffers");
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(build_mx_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = true;
-    }
+    static PerDevice attr;
+    attr.get([&] { return (int)cudaFuncSetAttribute(build_mx_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
     const int64_t grid = (row1 - row0 + BW - 1) / BW;
     build_mx_kernel<<<(unsigned)grid, kThreads, smem, st>>>(E, row0, row1, dp, sel, v_r, ld, lambda, Kt, Mx);
     return;
@@ -468,8 +465,8 @@ void launch_build_ktilde(const float* E, int64_t row0, int64_t row1, int dp, con
 #define TC_(NP)                                                                                       \
   {                                                                                                   \
     constexpr size_t sm = (TC_NS + TC_LO) * (TC_M + NP) * tc_k<NP>() * 4 + 1024;                    \
-    static bool a = false;                                                                            \
-    if (!a) { cudaFuncSetAttribute(build_mx_tc_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); a = true; } \
+    static PerDevice a;                                                                               \
+    a.get([&] { return (int)cudaFuncSetAttribute(build_mx_tc_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); }); \
     build_mx_tc_kernel<NP><<<grid, 128, sm, st>>>(E, row0, row1, dp, sel, v_r, ld, lambda, Kt, Mx);  \
   }
   if (v_r <= 32) TC_(32)

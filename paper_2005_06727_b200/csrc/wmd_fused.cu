@@ -38,6 +38,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <cstdint>
+#include <type_traits>
 
 #include "wmd_tile.cuh"
 
@@ -66,31 +67,19 @@ struct Shape {
   static constexpr int REGS = RW * CW;
 };
 
-#ifndef WMD_FUSED_DOCS_PER_WARP_SMALL  // documents per warp in the <= 16-row buckets
-#define WMD_FUSED_DOCS_PER_WARP_SMALL 1
-#endif
-#ifndef WMD_FUSED_DOCS_PER_WARP
-#define WMD_FUSED_DOCS_PER_WARP 1
-#endif
-#ifndef WMD_STREAM_ENTRIES
-#define WMD_STREAM_ENTRIES 1
-#endif
 #ifndef WMD_FUSED_REG_SLACK
 #define WMD_FUSED_REG_SLACK 8
 #endif
-template <int CW, int NT, int TW, int D>
+template <int CW, int NT, int TW>
 constexpr int min_blocks() {
   using S = Shape<CW, NT, TW>;
-  constexpr int regs = ((D * (S::REGS + 3 * S::RW + 2 * CW + 16) + WMD_FUSED_REG_SLACK) + 7) / 8 * 8;
+  constexpr int regs = ((S::REGS + 3 * S::RW + 2 * CW + 16 + WMD_FUSED_REG_SLACK) + 7) / 8 * 8;
   constexpr int b = 65536 / (kThreads * regs);
   return b < 1 ? 1 : (b > 8 ? 8 : b);
 }
 
-// D: documents per warp, interleaved in one instruction stream (more independent work per warp
-// to cover the shuffle / MUFU / reduction latencies). D = 2 needs CONV = false (both documents
-// then run exactly `iters` updates).
-template <int CW, int NT, int TW, bool CONV, int D>
-__global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW, D>()) sinkhorn_fused_kernel(
+template <int CW, int NT, int TW, bool CONV>
+__global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW>()) sinkhorn_fused_kernel(
     const int4* __restrict__ sdoc, const Entry* __restrict__ ent, int64_t pos0, int64_t pos1,
     const float* __restrict__ Mx, int v_r, const float* __restrict__ rpad, float lambda, int iters,
     float tol, int32_t* __restrict__ iters_doc, float* __restrict__ dist,
@@ -103,21 +92,13 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW, D>()) sinkhor
   // columns 32Q + Rb + r (CW >= 3), else column 2b + (a >> 1) (CW = 2) or b (CW = 1)
   constexpr int CQ = Cols<CW>::Q, CR = Cols<CW>::R;
   constexpr int NCO = CW >= 3 ? CQ + CR : 1;
-  static_assert(D == 1 || !CONV, "per-document stopping runs one document per warp");
   extern __shared__ __align__(16) float smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int a = lane >> 3, b = lane & 7;
-  float* buf[D];                                 // the staged M rows of each document slot
-#pragma unroll
-  for (int d = 0; d < D; ++d) buf[d] = smem + (wib * D + d) * S::BUF;
-  const int64_t stride = (int64_t)gridDim.x * kWarps * D;
-  const uint64_t keep = l2_evict_last_policy();
-#if WMD_STREAM_ENTRIES  // c is read once: evict_first, so the Mx rows keep their L2 lines
-  const uint64_t stream_pol = l2_evict_first_policy();
-#define WMD_ENT_LOAD(p) ldg_guarded_stream((p), stream_pol)
-#else
-#define WMD_ENT_LOAD(p) ldg_guarded(p)
-#endif
+  float* const buf = smem + wib * S::BUF;        // the staged M rows of the warp's document
+  const int64_t stride = (int64_t)gridDim.x * kWarps;
+  const uint64_t keep = l2_evict_last_policy();         // the gathered M rows stay in L2
+  const uint64_t stream_pol = l2_evict_first_policy();  // c is read once
   const int2* ent2 = reinterpret_cast<const int2*>(ent);
   const float alpha = lambda * kLog2e;          // exp(-lambda x) = 2^(-alpha x)
   const float kv_s = (float)v_r * kUnder;
@@ -137,47 +118,40 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW, D>()) sinkhor
   for (int c = 0; c < CW; ++c) nreal[c] = nat_col<CW>(c, b) < v_r;
 
   // ---- prefetch: stage 1 (document header), stage 2 (entries), stage 3 (cp.async of M rows)
-  int64_t pos = pos0 + ((int64_t)blockIdx.x * kWarps + wib) * D;
-  int pj[D], pb[D], pn[D];
-  int pk[D][NW];
-  float pc[D][NW];
+  int64_t pos = pos0 + (int64_t)blockIdx.x * kWarps + wib;
+  int pj = -1, pb = 0, pn = 0;
+  int pk[NW];
+  float pc[NW];
   auto stage1 = [&](int64_t p) {
-#pragma unroll
-    for (int d = 0; d < D; ++d) {
-      pj[d] = -1; pn[d] = 0; pb[d] = 0;
-      if (p + d < pos1) {  // {document id, first nonzero, length, -} (a load that stays guarded)
-        const int4 x = ldg_guarded(sdoc + p + d);
-        pj[d] = x.x; pb[d] = x.y; pn[d] = x.z;
-      }
+    pj = -1; pn = 0; pb = 0;
+    if (p < pos1) {  // {document id, first nonzero, length, -} (a load that stays guarded)
+      const int4 x = ldg_guarded(sdoc + p);
+      pj = x.x; pb = x.y; pn = x.z;
     }
   };
   auto stage2 = [&]() {
 #pragma unroll
-    for (int d = 0; d < D; ++d)
-#pragma unroll
-      for (int w = 0; w < NW; ++w) {
-        const int e = lane + 32 * w;
-        int2 x = make_int2(0, 0);
-        if (e < pn[d]) x = WMD_ENT_LOAD(ent2 + pb[d] + e);
-        pk[d][w] = x.x;
-        pc[d][w] = __int_as_float(x.y);
-      }
+    for (int w = 0; w < NW; ++w) {
+      const int e = lane + 32 * w;
+      int2 x = make_int2(0, 0);
+      if (e < pn) x = ldg_guarded_stream(ent2 + pb + e, stream_pol);
+      pk[w] = x.x;
+      pc[w] = __int_as_float(x.y);   // 0 on rows past the document: v = 0 there
+    }
   };
   auto stage3 = [&]() {
 #pragma unroll
-    for (int d = 0; d < D; ++d)
+    for (int w = 0; w < NW; ++w) {
+      const int e = lane + 32 * w;
+      if (e < pn) {
+        uint32_t k;  // opaque copy: keeps the address arithmetic (and its wait on the entry
+        asm volatile("mov.b32 %0, %1;" : "=r"(k) : "r"(pk[w]));  // load) at this point
+        const float* src = Mx + (size_t)k * P;
+        const uint32_t dst = smem_u32(buf + e * P);
 #pragma unroll
-      for (int w = 0; w < NW; ++w) {
-        const int e = lane + 32 * w;
-        if (e < pn[d]) {
-          uint32_t k;  // opaque copy: keeps the address arithmetic (and its wait on the entry
-          asm volatile("mov.b32 %0, %1;" : "=r"(k) : "r"(pk[d][w]));  // load) at this point
-          const float* src = Mx + (size_t)k * P;
-          const uint32_t dst = smem_u32(buf[d] + e * P);
-#pragma unroll
-          for (int q = 0; q < P / 4; ++q) cp_async16(dst + 16 * q, src + 4 * q, keep);
-        }
+        for (int q = 0; q < P / 4; ++q) cp_async16(dst + 16 * q, src + 4 * q, keep);
       }
+    }
     cp_async_commit();
   };
 
@@ -186,36 +160,29 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW, D>()) sinkhor
   stage3();
 
   for (; pos < pos1; pos += stride) {
-    int j[D], n[D];
-    float c_own[D][NOWN];
-    bool v_ok[D][NOWN];
+    const int j = pj, n = pn;
+    // c of the lane's own rows: row 32T + lane (full tiles), tail row 32NT + TW a + (b >> TSH)
+    float c_own[NOWN];
+    bool v_ok[NOWN];
 #pragma unroll
-    for (int d = 0; d < D; ++d) {
-      j[d] = pj[d];
-      n[d] = pn[d];
-      // c of the lane's own rows: row 32T + lane (full tiles), tail row 32NT + TW a + (b >> TSH)
-#pragma unroll
-      for (int T = 0; T < NT; ++T) {
-        c_own[d][T] = pc[d][T];
-        v_ok[d][T] = 32 * T + lane < n[d];
-      }
-      if constexpr (TW > 0) {
-        const int tr = TW * a + (b >> S::TSH);
-        c_own[d][NT] = __shfl_sync(kFull, pc[d][NT], tr);
-        v_ok[d][NT] = 32 * NT + tr < n[d];
-      }
+    for (int T = 0; T < NT; ++T) {
+      c_own[T] = pc[T];
+      v_ok[T] = 32 * T + lane < n;
+    }
+    if constexpr (TW > 0) {
+      const int tr = TW * a + (b >> S::TSH);
+      c_own[NT] = __shfl_sync(kFull, pc[NT], tr);
+      v_ok[NT] = 32 * NT + tr < n;
     }
     stage1(pos + stride);
     cp_async_wait_all();
     __syncwarp();
 
-    // ---- block tiles: D = M - m, mu = column minima over the document, Kh = 2^(-alpha (D - mu))
-    float K[D][RW][CW];
-    float u[D][CW], mu_s[D][CW], m_own[D][NOWN];
-    bool und[D];
-#pragma unroll
-    for (int d = 0; d < D; ++d) {
-      const float* Sb = buf[d];
+    // ---- block tile: D = M - m, mu = column minima over the document, Kh = 2^(-alpha (D - mu))
+    float K[RW][CW];
+    float u[CW], mu_s[CW], m_own[NOWN];
+    bool und;
+    {
       float mu[CW];
 #pragma unroll
       for (int c = 0; c < CW; ++c) mu[c] = FLT_MAX;
@@ -223,15 +190,15 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW, D>()) sinkhor
 #pragma unroll
       for (int s = 0; s < RW; ++s) {
         const int e = row_of<NT, TW>(s, a, b);
-        const bool ok = e < n[d];
-        const float* row = Sb + (ok ? e : 0) * P;
+        const bool ok = e < n;
+        const float* row = buf + (ok ? e : 0) * P;
         float x[CW];
         load_cols<CW>(row, b, x);
         const float me = row[LD];
 #pragma unroll
         for (int c = 0; c < CW; ++c) {
-          K[d][s][c] = ok ? x[c] - me : FLT_MAX;   // rows past n: FLT_MAX (Kh = 0 below)
-          mu[c] = fminf(mu[c], K[d][s][c]);
+          K[s][c] = ok ? x[c] - me : FLT_MAX;   // rows past n: FLT_MAX until Kh is formed
+          mu[c] = fminf(mu[c], K[s][c]);
         }
       }
 #pragma unroll
@@ -247,100 +214,95 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW, D>()) sinkhor
       for (int s = 0; s < RW; ++s) {
 #pragma unroll
         for (int c = 0; c < CW; ++c) {
-          const float dd = K[d][s][c];
-          const float kx = ex2_ftz(fmaf(-alpha, dd, amu[c]));   // rows past n: 2^-huge = 0
+          const float dd = K[s][c];
+          const float kx = ex2_ftz(fmaf(-alpha, dd, amu[c]));
           flushed |= nreal[c] && kx < FLT_MIN && dd != FLT_MAX;
-          K[d][s][c] = nreal[c] ? kx : (dd != FLT_MAX ? 1.f : 0.f);  // padded columns: 1 on real rows
+          // padded columns (u = 0) and rows past n (c = 0, so v = 0) hold 1: every row sum s
+          // stays positive and no select is needed in the loop
+          K[s][c] = (nreal[c] && dd != FLT_MAX) ? kx : 1.f;
         }
-        to_slots<CW>(K[d][s], a);
+        to_slots<CW>(K[s], a);
       }
-      und[d] = __any_sync(kFull, flushed);
+      und = __any_sync(kFull, flushed);
       // for the final step (which then needs no M): m of the own rows, mu in slot order
 #pragma unroll
-      for (int T = 0; T < NT; ++T) m_own[d][T] = v_ok[d][T] ? Sb[(32 * T + lane) * P + LD] : 0.f;
+      for (int T = 0; T < NT; ++T) m_own[T] = v_ok[T] ? buf[(32 * T + lane) * P + LD] : 0.f;
       if constexpr (TW > 0)
-        m_own[d][NT] = v_ok[d][NT] ? Sb[(32 * NT + TW * a + (b >> S::TSH)) * P + LD] : 0.f;
+        m_own[NT] = v_ok[NT] ? buf[(32 * NT + TW * a + (b >> S::TSH)) * P + LD] : 0.f;
 #pragma unroll
-      for (int c = 0; c < CW; ++c) mu_s[d][c] = mu[c];
-      to_slots<CW>(mu_s[d], a);
+      for (int c = 0; c < CW; ++c) mu_s[c] = mu[c];
+      to_slots<CW>(mu_s, a);
       // uh0 = v_r 2^(-alpha mu) on real columns (slot order)
 #pragma unroll
-      for (int c = 0; c < CW; ++c) u[d][c] = nreal[c] ? (float)v_r * ex2_ftz(-alpha * mu[c]) : 0.f;
-      to_slots<CW>(u[d], a);
+      for (int c = 0; c < CW; ++c) u[c] = nreal[c] ? (float)v_r * ex2_ftz(-alpha * mu[c]) : 0.f;
+      to_slots<CW>(u, a);
     }
-    __syncwarp();  // every lane is done with the staged rows: the buffers take the next documents
-    // the next documents' entries (their header loads were issued above)
-    stage2();
-    bool staged = false;
+    __syncwarp();  // every lane is done with the staged rows: the buffer takes the next document
+    stage2();      // the next document's entries (its header load was issued above)
 
     // ---- iterations, then the final step
-    float umax_k[D];
-    bool bad[D], done = false;
-    uint32_t badu[D];
-    float v_own[D][NOWN], s_own[D][NOWN];
-#pragma unroll
-    for (int d = 0; d < D; ++d) {
-      umax_k[d] = (float)v_r * kv_s;   // v_r * max(uh) * 2^-110 (max uh0 <= v_r)
-      bad[d] = false;
-      badu[d] = 0u;
-    }
+    float v_own[NOWN], s_own[NOWN];
+    bool bad = false;          // range certificate failed (blocks with flushed entries only)
+    float umin = FLT_MAX;      // smallest real uh after a gauge: must stay normal
+    uint32_t umax_all = 0u;    // largest uh before a gauge (bits): must stay finite
+    bool done = false;         // "while x changes" (CONV)
     int it = 0;
-    for (;; ++it) {
-      // SDDMM: row partials over this lane's columns, then the reduce over the b-lanes
-      uint32_t vmax_b[D];
-#pragma unroll
-      for (int d = 0; d < D; ++d) {
+    // The loop is instantiated twice: blocks without a flushed entry (the common case) carry no
+    // certificate arithmetic; the stage-3 prefetch of the next document is peeled out of the
+    // loop, so the loop body has no divergent branch.
+    auto iterate = [&](auto und_tag) {
+      constexpr bool UND = decltype(und_tag)::value;
+      float umax_k = (float)v_r * kv_s;   // v_r * max(uh) * 2^-110 (max uh0 <= v_r)
+      uint32_t vmax_b = 0u;
+      // SDDMM: row partials over this lane's columns, the reduce over the b-lanes, v = c / s
+      auto row_step = [&]() {
         float p[RW];
 #pragma unroll
         for (int s = 0; s < RW; ++s) {
-          float acc = K[d][s][0] * u[d][0];
+          float acc = K[s][0] * u[0];
 #pragma unroll
-          for (int c = 1; c < CW; ++c) acc = fmaf(K[d][s][c], u[d][c], acc);
+          for (int c = 1; c < CW; ++c) acc = fmaf(K[s][c], u[c], acc);
           p[s] = acc;
         }
         reduce_rows<NT, TW>(p);
-        vmax_b[d] = 0u;
+        vmax_b = 0u;
 #pragma unroll
         for (int o = 0; o < NOWN; ++o) {
           const float sv = p[8 * o];
-          s_own[d][o] = sv;
-          v_own[d][o] = v_ok[d][o] ? c_own[d][o] * rcp_fast(sv) : 0.f;
-          bad[d] |= v_ok[d][o] && und[d] && umax_k[d] > sv;
-          vmax_b[d] = max(vmax_b[d], __float_as_uint(v_own[d][o]));
+          s_own[o] = sv;
+          v_own[o] = c_own[o] * rcp_fast(sv);
+          if constexpr (UND) {
+            bad |= v_ok[o] && umax_k > sv;
+            vmax_b = max(vmax_b, __float_as_uint(v_own[o]));
+          }
         }
-      }
-      if (it == iters || (CONV && done)) break;
-      if (it == 1) {  // the next documents' entries have landed: start their row copies
-        staged = true;
-        stage3();
-      }
-#pragma unroll
-      for (int d = 0; d < D; ++d) {
-        vmax_b[d] = __reduce_max_sync(kFull, vmax_b[d]);
-        // distribute vh to the row slots
+      };
+      // SpMM: column partials over this lane's rows, the reduce over the a-lanes, u = r / acc,
+      // the exact power-of-two gauge, redistribution of u to the column slots
+      auto col_step = [&]() {
+        float vcap = 0.f;
+        if constexpr (UND) vcap = (float)n * __uint_as_float(__reduce_max_sync(kFull, vmax_b)) * kUnder;
         float vs[RW];
 #pragma unroll
         for (int T = 0; T < NT; ++T) {
-          vs[8 * T] = v_own[d][T];
+          vs[8 * T] = v_own[T];
 #pragma unroll
-          for (int t = 1; t < 8; ++t) vs[8 * T + t] = shx(v_own[d][T], t);
+          for (int t = 1; t < 8; ++t) vs[8 * T + t] = shx(v_own[T], t);
         }
         if constexpr (TW > 0) {
-          vs[8 * NT] = v_own[d][NT];
+          vs[8 * NT] = v_own[NT];
 #pragma unroll
-          for (int t = 1; t < TW; ++t) vs[8 * NT + t] = shx(v_own[d][NT], t << S::TSH);
+          for (int t = 1; t < TW; ++t) vs[8 * NT + t] = shx(v_own[NT], t << S::TSH);
         }
-        // SpMM: column partials over this lane's rows, then the reduce over the a-lanes
         float q[CW];
 #pragma unroll
         for (int c = 0; c < CW; ++c) {
-          float q0 = K[d][0][c] * vs[0];
+          float q0 = K[0][c] * vs[0];
 #pragma unroll
-          for (int s = 1; s < RW; ++s) q0 = fmaf(K[d][s][c], vs[s], q0);
+          for (int s = 1; s < RW; ++s) q0 = fmaf(K[s][c], vs[s], q0);
           q[c] = q0;
         }
         reduce_cols<CW>(q);
-        const float vcap = (float)n[d] * __uint_as_float(vmax_b[d]) * kUnder;
         uint32_t umax_b = 0u, chg_b = 0u;
         float uo[NCO];
 #pragma unroll
@@ -349,116 +311,123 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW, D>()) sinkhor
           const float acc = q[qs];
           uo[g] = r_own[g] * rcp_fast(acc);
           // "while x changes" (NEXT-3): |x_new/x - 1| = |uh/uh_new - 1| (gauge invariant; the
-          // own column's current uh sits in column slot 4g); NaN compares above every float
-          if (CONV && oreal[g]) chg_b = max(chg_b, __float_as_uint(fabsf(u[d][qs] / uo[g] - 1.f)));
-          bad[d] |= und[d] && vcap > acc;
+          // own column's current uh sits in column slot qs); NaN compares above every float
+          if (CONV && oreal[g]) chg_b = max(chg_b, __float_as_uint(fabsf(u[qs] / uo[g] - 1.f)));
+          if constexpr (UND) bad |= vcap > acc;
           umax_b = max(umax_b, __float_as_uint(uo[g]));
         }
-        // gauge: max uh -> [1, 2) by an exact power of two (positive floats order like their
-        // bits); the lanes check their own uh stay normal
+        // gauge: max uh -> [1, 2) by an exact power of two (positive floats order like their bits)
         umax_b = __reduce_max_sync(kFull, umax_b);
-        badu[d] |= umax_b > 0x7f7fffffu;
+        umax_all = max(umax_all, umax_b);
         if (CONV) done = __uint_as_float(__reduce_max_sync(kFull, chg_b)) <= tol;
         const float sc = __uint_as_float((254u - min(umax_b >> 23, 253u)) << 23);
-        umax_k[d] = 2.f * kv_s;
+        if constexpr (UND) umax_k = 2.f * kv_s;
 #pragma unroll
         for (int g = 0; g < NCO; ++g) {
           uo[g] *= sc;
-          bad[d] |= oreal[g] && !(uo[g] >= FLT_MIN);
+          umin = fminf(umin, oreal[g] ? uo[g] : 1.f);
         }
-        // distribute uh to the column slots
         if constexpr (CW >= 3) {
 #pragma unroll
           for (int g = 0; g < CQ; ++g) {
-            u[d][4 * g] = uo[g];
+            u[4 * g] = uo[g];
 #pragma unroll
-            for (int c = 1; c < 4; ++c) u[d][4 * g + c] = shx(uo[g], 8 * c);
+            for (int c = 1; c < 4; ++c) u[4 * g + c] = shx(uo[g], 8 * c);
           }
 #pragma unroll
-          for (int r = 0; r < CR; ++r) u[d][4 * CQ + r] = uo[CQ + r];
+          for (int r = 0; r < CR; ++r) u[4 * CQ + r] = uo[CQ + r];
         } else if constexpr (CW == 2) {
-          u[d][0] = uo[0];
-          u[d][1] = shx(uo[0], 16);
+          u[0] = uo[0];
+          u[1] = shx(uo[0], 16);
         } else {
-          u[d][0] = uo[0];
+          u[0] = uo[0];
         }
+      };
+      row_step();
+      if (iters > 0) {
+        col_step();
+        it = 1;
+        row_step();
+        stage3();  // the next document's entries have landed: start its row copies
+        while (it != iters && !(CONV && done)) {
+          col_step();
+          ++it;
+          row_step();
+        }
+      } else {
+        stage3();
       }
-    }
-    if (!staged) stage3();
+    };
+    if (und) iterate(std::true_type{});
+    else iterate(std::false_type{});
+
     // ---- final step: WMD_j = sum_e vh_e q_e,  q_e = sum_i Kh_ei M_ie uh_i
     // M is recovered from the block itself: Kh = 2^(-alpha (D - mu)) gives
     //   M_ie = D_ei + m_e = mu_i + m_e - log2(Kh_ei) / alpha,
     // so q_e = sum_i Kh_ei uh_i (mu_i - log2(Kh_ei)/alpha) + m_e s_e with s_e = Kh uh from the
-    // last SDDMM. Entries flushed to 0 contribute 0 (Kh log2 Kh -> 0).
-    const float ia = -rcp_fast(alpha);  // (approximate: no IEEE-division slow-path call)
-#pragma unroll
-    for (int d = 0; d < D; ++d) {
-      float p[RW];
+    // last SDDMM. Entries flushed to 0 contribute 0 (Kh log2 Kh -> 0). The recovery's absolute
+    // error in D is ~2^-22 / alpha: below lambda = kFusedMinLambda (wmd_internal.h) the host
+    // routes the query to the per-iteration path, whose final step reads M.
+    float p[RW];
+    {
+      const float ia = -rcp_fast(alpha);  // (approximate: no IEEE-division slow-path call)
 #pragma unroll
       for (int s = 0; s < RW; ++s) {
         float acc = 0.f;
 #pragma unroll
         for (int c = 0; c < CW; ++c) {
-          const float k = K[d][s][c];
+          const float k = K[s][c];
           const float kl = k > 0.f ? k * lg2_approx(k) : 0.f;
-          acc = fmaf(fmaf(kl, ia, k * mu_s[d][c]), u[d][c], acc);
+          acc = fmaf(fmaf(kl, ia, k * mu_s[c]), u[c], acc);
         }
         p[s] = acc;
       }
-      reduce_rows<NT, TW>(p);
-      float wsum = 0.f;
+    }
+    reduce_rows<NT, TW>(p);
+    float wsum = 0.f;
 #pragma unroll
-      for (int T = 0; T < NT; ++T)
-        if (v_ok[d][T]) wsum = fmaf(v_own[d][T], fmaf(m_own[d][T], s_own[d][T], p[8 * T]), wsum);
-      if constexpr (TW > 0) {  // each tail row is held by 2^TSH lanes: count it once
-        if (v_ok[d][NT] && (b & ((1 << S::TSH) - 1)) == 0)
-          wsum = fmaf(v_own[d][NT], fmaf(m_own[d][NT], s_own[d][NT], p[8 * NT]), wsum);
-      }
+    for (int T = 0; T < NT; ++T)
+      if (v_ok[T]) wsum = fmaf(v_own[T], fmaf(m_own[T], s_own[T], p[8 * T]), wsum);
+    if constexpr (TW > 0) {  // each tail row is held by 2^TSH lanes: count it once
+      if (v_ok[NT] && (b & ((1 << S::TSH) - 1)) == 0)
+        wsum = fmaf(v_own[NT], fmaf(m_own[NT], s_own[NT], p[8 * NT]), wsum);
+    }
 #pragma unroll
-      for (int off = 16; off; off >>= 1) wsum += shx(wsum, off);
-      const bool flag = __any_sync(kFull, bad[d]) || badu[d] || !(fabsf(wsum) <= FLT_MAX);
-      if (lane == 0 && j[d] >= 0) {
-        dist[j[d]] = wsum;
-        if (iters_doc) iters_doc[j[d]] = it;
-        if (flag) {
-          flags[j[d]] |= kFlagFp32Range;
-          flagged_list[atomicAdd(flagged_count, 1)] = j[d];
-        }
+    for (int off = 16; off; off >>= 1) wsum += shx(wsum, off);
+    const bool flag = __any_sync(kFull, bad || !(umin >= FLT_MIN)) || umax_all > 0x7f7fffffu ||
+                      !(fabsf(wsum) <= FLT_MAX);
+    if (lane == 0) {
+      dist[j] = wsum;
+      if (iters_doc) iters_doc[j] = it;
+      uint8_t f = und ? kFlagUnderflow : 0;
+      if (flag) {
+        f |= kFlagFp32Range;
+        flagged_list[atomicAdd(flagged_count, 1)] = j;
       }
+      if (f) flags[j] |= f;
     }
   }
   cp_async_wait_all();  // nothing may be in flight when the warp exits
 }
 
-int num_sms() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
-  return sms;
-}
-
-template <int CW, int NT, int TW, bool CONV, int D>
+template <int CW, int NT, int TW, bool CONV>
 void launch_fused_range_t(const int4* sdoc, const Entry* ent, int64_t p0,
                         int64_t p1, const float* Mx, int v_r, const float* rpad, float lambda,
                         int iters, float tol, int32_t* itd, float* dist, uint8_t* flags, int32_t* fl,
                         int32_t* fc, cudaStream_t st) {
   if (p1 <= p0) return;
-  constexpr size_t smem = sizeof(float) * Shape<CW, NT, TW>::BUF * kWarps * D;
-  static int resident = 0;
-  if (!resident) {
-    cudaFuncSetAttribute(sinkhorn_fused_kernel<CW, NT, TW, CONV, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(sinkhorn_fused_kernel<CW, NT, TW, CONV, D>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  constexpr size_t smem = sizeof(float) * Shape<CW, NT, TW>::BUF * kWarps;
+  static PerDevice cache;
+  const int resident = cache.get([&] {
+    cudaFuncSetAttribute(sinkhorn_fused_kernel<CW, NT, TW, CONV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(sinkhorn_fused_kernel<CW, NT, TW, CONV>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sinkhorn_fused_kernel<CW, NT, TW, CONV, D>, kThreads, smem);
-    resident = std::max(1, per_sm) * num_sms();
-  }
-  const int64_t need = (p1 - p0 + kWarps * D - 1) / (kWarps * D);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sinkhorn_fused_kernel<CW, NT, TW, CONV>, kThreads, smem);
+    return std::max(1, per_sm) * device_sms();
+  });
+  const int64_t need = (p1 - p0 + kWarps - 1) / kWarps;
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, resident));
-  sinkhorn_fused_kernel<CW, NT, TW, CONV, D><<<grid, kThreads, smem, st>>>(sdoc, ent, p0, p1, Mx, v_r, rpad,
+  sinkhorn_fused_kernel<CW, NT, TW, CONV><<<grid, kThreads, smem, st>>>(sdoc, ent, p0, p1, Mx, v_r, rpad,
                                                                    lambda, iters, tol, itd, dist, flags, fl, fc);
 }
 
@@ -467,10 +436,9 @@ void launch_fused_range(const int4* sdoc, const Entry* ent, int64_t p0, int64_t 
                         const float* rpad, float lambda, int iters, float tol, int32_t* itd, float* dist,
                         uint8_t* flags, int32_t* fl, int32_t* fc, cudaStream_t st) {
   if (tol >= 0.f)
-    launch_fused_range_t<CW, NT, TW, true, 1>(sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, tol, itd, dist, flags, fl, fc, st);
+    launch_fused_range_t<CW, NT, TW, true>(sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, tol, itd, dist, flags, fl, fc, st);
   else
-    launch_fused_range_t<CW, NT, TW, false, (NT == 0 ? WMD_FUSED_DOCS_PER_WARP_SMALL : WMD_FUSED_DOCS_PER_WARP)>(
-        sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, tol, itd, dist, flags, fl, fc, st);
+    launch_fused_range_t<CW, NT, TW, false>(sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, tol, itd, dist, flags, fl, fc, st);
 }
 
 // Length buckets (rows covered: 8, 16, 32, 40, 48, 64) over the length-sorted order.

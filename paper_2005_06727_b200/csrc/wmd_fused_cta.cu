@@ -47,6 +47,9 @@ constexpr float kLog2eC = 1.4426950408889634f;
 #define WMD_CTA_MAX_ANCHORS 4
 #endif
 constexpr int kMaxAnchors = WMD_CTA_MAX_ANCHORS;
+#ifndef WMD_CTA_GUARDED_LOADS
+#define WMD_CTA_GUARDED_LOADS 0
+#endif
 
 template <int CW, int W, int TW>
 struct CtaShape {
@@ -138,6 +141,16 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W, TW>()) sinkhorn_
   // faulted in some optimised builds of this kernel)
   auto stage1 = [&](int64_t p) {
     const bool ok = p < pos1;
+#if WMD_CTA_GUARDED_LOADS  // the round-1 form (sanitizer study only, tools/cta_fault_study.py)
+    if constexpr (!LIST) {
+      pj = -1; pn = 0; pb = 0;
+      if (ok) {
+        const int4 x = __ldg(sdoc + p);
+        pj = x.x; pb = x.y; pn = x.z;
+      }
+      return;
+    }
+#endif
     if constexpr (LIST) {
       const int jj = __ldg(dl.ids + (ok ? p : pos1 - 1));
       const int b0 = __ldg(dl.doc_ptr + jj), n0 = __ldg(dl.doc_ptr + jj + 1) - b0;
@@ -154,8 +167,12 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W, TW>()) sinkhorn_
 #pragma unroll
     for (int x = 0; x < EPT; ++x) {
       const int e = tid + NT * x;
+#if WMD_CTA_GUARDED_LOADS
+      pe[x] = e < pn ? __ldg(ent2 + pb + e) : make_int2(0, 0);
+#else
       const int2 v = ldg2_hint(ent2 + pb + (e < pn ? e : 0), stream_pol);  // read once
       pe[x] = e < pn ? v : make_int2(0, 0);
+#endif
     }
   };
   stage1(pos);
@@ -493,7 +510,8 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W, TW>()) sinkhorn_
 #pragma unroll
       for (int r = 0; r < R; ++r) ur[r] = unr[r];
     }
-    // ---- final step: D = (beta + gamma - log2 Kh) / alpha (PAPER.md:64-66 with M = m + D)
+    // ---- final step: D = (beta + gamma - log2 Kh) / alpha (PAPER.md:64-66 with M = m + D); the
+    // recovery's absolute error ~2^-22 / alpha sets kFusedMinLambda (wmd_internal.h)
     {
       float p[RW];
 #pragma unroll
@@ -540,27 +558,15 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W, TW>()) sinkhorn_
   }
 }
 
-int num_sms_cta() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
-  return sms;
-}
-
 template <int CW, int W, int TW, bool LIST>
 int cta_resident() {
   constexpr size_t smem = sizeof(float) * CtaShape<CW, W, TW>::SMEM_FLOATS;
-  static int resident = 0;
-  if (!resident) {
+  static PerDevice cache;
+  return cache.get([&] {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sinkhorn_cta_kernel<CW, W, TW, LIST>, 32 * W, smem);
-    resident = std::max(1, per_sm) * num_sms_cta();
-  }
-  return resident;
+    return std::max(1, per_sm) * device_sms();
+  });
 }
 
 template <int CW, int W, int TW>

@@ -9,7 +9,9 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <new>
 #include <numeric>
 #include <string>
@@ -21,8 +23,11 @@
 
 using wmd::Entry;
 
+#ifndef WMD_GUARD_ENTRIES
+#define WMD_GUARD_ENTRIES 1024
+#endif
 namespace {
-constexpr int64_t kGuard = 1024;  // zeroed slack entries after ent / sdoc (see set_targets)
+constexpr int64_t kGuard = WMD_GUARD_ENTRIES;  // zeroed slack entries after ent / sdoc (see set_targets)
 }  // namespace
 
 namespace {
@@ -72,7 +77,8 @@ struct DevBuf {
 };
 
 struct PhaseEvents {
-  cudaEvent_t ev[5];  // start, after build, after iterations, after final, after fallback
+  cudaEvent_t ev[5];      // start, after build, after iterations, after final, after fallback
+  bool complete = false;  // ev[4] recorded: the query's whole stream work is enqueued
 };
 
 // What a captured query graph depends on (WMD_OPT_GRAPH).
@@ -174,10 +180,18 @@ struct wmd_handle {
   int64_t graph_launches = 0;
   int64_t targets_gen = 0;   // bumped by every wmd_set_targets (buffers may move)
   // options
-  int64_t opt_path = WMD_PATH_AUTO, opt_timing = 0, opt_fallback = 1, opt_graph = 0, opt_build = 0;
+  int64_t opt_path = WMD_PATH_AUTO, opt_timing = 0, opt_fallback = 1, opt_graph = 0;
+  int64_t opt_build = WMD_BUILD_DIRECT;  // WMD_OPT_BUILD
+  int64_t opt_layout_nnz = 0;  // WMD_OPT_LAYOUT_DOC_NNZ
   // stats
   wmd_stats st{};
-  std::vector<PhaseEvents> events;
+  // per-phase timing (WMD_OPT_TIMING): events of queries in flight (a deque: push_back /
+  // pop_front keep the other entries' addresses, which pq.pe holds across begin / finish),
+  // folded into phase_ms as they complete and recycled through event_pool
+  std::deque<PhaseEvents> events;
+  std::vector<PhaseEvents> event_pool;
+  double phase_ms[5] = {};  // build, iterations, final, fallback, whole query
+  int64_t phase_n = 0;
   std::string err;
 };
 
@@ -203,10 +217,25 @@ wmd_status cuda_fail(wmd_handle* h, cudaError_t e, const char* what) {
   return fail(h, WMD_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }
 
+// WMD_DEBUG_SYNC=1 (environment): synchronise and check after every phase's launches, naming the
+// phase in the error (debugging aid; off by default, never inside a graph capture).
+bool debug_sync() {
+  static const bool on = [] { const char* e = std::getenv("WMD_DEBUG_SYNC"); return e && e[0] == '1'; }();
+  return on;
+}
+
 #define CK(h, call)                                                    \
   do {                                                                 \
     cudaError_t e_ = (call);                                           \
     if (e_ != cudaSuccess) return cuda_fail((h), e_, #call);           \
+  } while (0)
+#define DBG_PHASE(h, st, what)                                         \
+  do {                                                                 \
+    if (debug_sync()) {                                                \
+      cudaError_t e_ = cudaDeviceSynchronize();                        \
+      if (e_ == cudaSuccess) e_ = cudaGetLastError();                  \
+      if (e_ != cudaSuccess) return cuda_fail((h), e_, what);          \
+    }                                                                  \
   } while (0)
 
 int32_t round_up8(int32_t x) { return (x + 7) / 8 * 8; }
@@ -401,11 +430,13 @@ wmd_status wmd_create(const float* vocab_emb, int64_t V, int32_t d, int32_t devi
   if (h->E.ensure((size_t)V * dp) != cudaSuccess) return bail(WMD_ERR_OUT_OF_MEMORY);
   if (cudaMemsetAsync(h->E.p, 0, (size_t)V * dp * sizeof(float), h->stream) != cudaSuccess) return bail(WMD_ERR_CUDA);
   if (h->counters.ensure(6) != cudaSuccess) return bail(WMD_ERR_OUT_OF_MEMORY);
+  // every counter starts at zero whichever branch below runs (cudaMalloc may recycle memory of an
+  // earlier handle: a stale breakdown latch would surface as a spurious error at wmd_sync)
+  if (cudaMemsetAsync(h->counters.p, 0, 6 * sizeof(int32_t), h->stream) != cudaSuccess) return bail(WMD_ERR_CUDA);
   if (is_device_ptr(vocab_emb)) {
     if (cudaMemcpy2DAsync(h->E.p, dp * sizeof(float), vocab_emb, d * sizeof(float), d * sizeof(float), V,
                           cudaMemcpyDeviceToDevice, h->stream) != cudaSuccess)
       return bail(WMD_ERR_CUDA);
-    cudaMemsetAsync(h->counters.p, 0, 6 * sizeof(int32_t), h->stream);
     wmd::launch_check_finite(h->E.p, (int64_t)V * dp, h->counters.p + 3, h->stream);
     int32_t bad = 0;
     if (cudaMemcpyAsync(&bad, h->counters.p + 3, sizeof bad, cudaMemcpyDeviceToHost, h->stream) != cudaSuccess ||
@@ -454,6 +485,8 @@ void wmd_destroy(wmd_handle* h) {
   if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
   for (auto& pe : h->events)
     for (auto& e : pe.ev) cudaEventDestroy(e);
+  for (auto& pe : h->event_pool)
+    for (auto& e : pe.ev) cudaEventDestroy(e);
   if (h->batch_stage) cudaFreeHost(h->batch_stage);
   if (h->batch_ev) cudaEventDestroy(h->batch_ev);
   h->bsel.release(); h->brpad.release(); h->batch_dist.release();
@@ -497,8 +530,12 @@ wmd_status wmd_set_option(wmd_handle* h, int32_t option, int64_t value) {
     case WMD_OPT_FALLBACK: h->opt_fallback = value != 0; return WMD_OK;
     case WMD_OPT_GRAPH: h->opt_graph = value != 0; return WMD_OK;
     case WMD_OPT_BUILD:
-      if (value < 0 || value > 1) return fail(h, WMD_ERR_INVALID_ARGUMENT, "bad build kernel");
+      if (value != WMD_BUILD_TENSOR_CORE && value != WMD_BUILD_DIRECT) return fail(h, WMD_ERR_INVALID_ARGUMENT, "bad build kernel");
       h->opt_build = value;
+      return WMD_OK;
+    case WMD_OPT_LAYOUT_DOC_NNZ:
+      if (value < 0) return fail(h, WMD_ERR_INVALID_ARGUMENT, "negative layout document length");
+      h->opt_layout_nnz = value;
       return WMD_OK;
   }
   return fail(h, WMD_ERR_INVALID_ARGUMENT, "unknown option %d", option);
@@ -555,7 +592,7 @@ wmd_status wmd_set_targets(wmd_handle* h, const int64_t* col_ptr, const int32_t*
   // + kGuard zeroed entries past the end: the fused kernels' guarded prefetch loads clamp their
   // index, and the slack keeps any speculated read of the next row inside the allocation
   CK(h, h->ent.ensure(nnz + kGuard));
-  CK(h, cudaMemsetAsync(h->ent.p + nnz, 0, kGuard * sizeof(Entry), h->stream));
+  if (kGuard) CK(h, cudaMemsetAsync(h->ent.p + nnz, 0, kGuard * sizeof(Entry), h->stream));
   CK(h, h->order.ensure(N));
   CK(h, cudaMemcpyAsync(h->order.p, ord.data(), N * sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
   std::vector<int4> sd(N);
@@ -564,7 +601,7 @@ wmd_status wmd_set_targets(wmd_handle* h, const int64_t* col_ptr, const int32_t*
     sd[p] = make_int4(j, dp[j], dp[j + 1] - dp[j], 0);
   }
   CK(h, h->sdoc.ensure(N + kGuard));
-  CK(h, cudaMemsetAsync(h->sdoc.p + N, 0, kGuard * sizeof(int4), h->stream));
+  if (kGuard) CK(h, cudaMemsetAsync(h->sdoc.p + N, 0, kGuard * sizeof(int4), h->stream));
   CK(h, cudaMemcpyAsync(h->sdoc.p, sd.data(), N * sizeof(int4), cudaMemcpyHostToDevice, h->stream));
   CK(h, cudaMemcpyAsync(h->doc_ptr.p, dp.data(), (N + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
   CK(h, cudaMemcpyAsync(h->ent.p, en.data(), nnz * sizeof(Entry), cudaMemcpyHostToDevice, h->stream));
@@ -589,17 +626,23 @@ wmd_status wmd_set_targets(wmd_handle* h, const int64_t* col_ptr, const int32_t*
 
 namespace {
 
+// Longest document the path / table-width decision assumes: the local maximum, or the larger
+// WMD_OPT_LAYOUT_DOC_NNZ (every rank of a sharded run passes the global maximum, so all ranks
+// choose the same path and row width and their tables can be all-gathered).
+int64_t layout_doc_nnz(const wmd_handle* h) { return std::max(h->max_doc_nnz, h->opt_layout_nnz); }
+
 // Path decision and buffer allocation for one query (never inside a graph capture). The tables
 // get max(V, table_rows) rows (a sharded build all-gathers equal row slices, which may pad).
-wmd_status prepare_query(wmd_handle* h, int32_t v_r, int64_t table_rows, bool* fused_out, int32_t* ld_out) {
+wmd_status prepare_query(wmd_handle* h, int32_t v_r, float lambda, int64_t table_rows, bool* fused_out,
+                         int32_t* ld_out) {
   const int64_t N = h->N;
   // fused path: ld = v_r rounded up to a power of two (the 2-D lane tiling); per-iteration
   // path: v_r rounded up to 8
-  const int32_t fld = wmd::fused_ld(v_r, h->max_doc_nnz, h->tol >= 0.0);
+  const int32_t fld = lambda >= wmd::kFusedMinLambda ? wmd::fused_ld(v_r, layout_doc_nnz(h), h->tol >= 0.0) : 0;
   const bool fused = (h->opt_path == WMD_PATH_FUSED || h->opt_path == WMD_PATH_AUTO) && fld > 0;
   if (h->opt_path == WMD_PATH_FUSED && !fused)
-    return fail(h, WMD_ERR_INVALID_ARGUMENT, "fused path does not support v_r=%d, max doc nnz=%lld", v_r,
-                (long long)h->max_doc_nnz);
+    return fail(h, WMD_ERR_INVALID_ARGUMENT, "fused path does not support v_r=%d, max doc nnz=%lld, lambda=%g",
+                v_r, (long long)layout_doc_nnz(h), (double)lambda);
   const int32_t ld = fused ? fld : round_up8(v_r);
   const int64_t rows = std::max(h->V, table_rows);
   // +128 floats: the pass kernels gather unpredicated float4s up to 4*32 floats past a row
@@ -622,7 +665,8 @@ wmd_status record_build(wmd_handle* h, const int32_t* d_sel, int32_t v_r, float 
   if (pe) CK(h, cudaEventRecord(pe->ev[0], st));
   // M (+ m), and K~ for the per-iteration path
   wmd::launch_build_ktilde(h->E.p, row0, row1, h->dp, d_sel, v_r, ld, lambda, fused ? nullptr : h->Kt.p,
-                           h->Mx.p, h->opt_build == 0, st);
+                           h->Mx.p, h->opt_build == WMD_BUILD_TENSOR_CORE, st);
+  DBG_PHASE(h, st, "distance build");
   if (pe) CK(h, cudaEventRecord(pe->ev[1], st));
   CK(h, cudaGetLastError());
   return WMD_OK;
@@ -651,6 +695,7 @@ wmd_status record_solve(wmd_handle* h, const float* d_r, int32_t v_r, float lamb
     wmd::launch_sinkhorn_fused(h->sdoc.p, h->ent.p, N, h->len_prefix.data(),
                                h->max_doc_nnz, h->Mx.p, ld, v_r, d_r, lambda, iters, tol, h->iters_doc.p,
                                dist, h->flags.p, h->flagged.p, h->counters.p, st, &ring);
+    DBG_PHASE(h, st, "fused Sinkhorn kernels");
     for (int i = 0; i < ring.n; ++i) {
       CK(h, cudaEventRecord(h->join_ev[i], h->lanes[i]));
       CK(h, cudaStreamWaitEvent(st, h->join_ev[i], 0));
@@ -690,6 +735,7 @@ wmd_status record_solve(wmd_handle* h, const float* d_r, int32_t v_r, float lamb
       wmd::launch_cta_rerun(h->flagged.p, h->counters.p, h->doc_ptr.p, h->ent.p, h->Mx.p, ld, v_r, d_r, lambda,
                             iters, h->iters_doc.p, dist, h->flags.p, h->flagged2.p, h->counters.p + 4, st);
       ++launches;
+      DBG_PHASE(h, st, "FP32 re-run of flagged documents");
       fl = h->flagged2.p;
       fc = h->counters.p + 4;
     }
@@ -697,18 +743,63 @@ wmd_status record_solve(wmd_handle* h, const float* d_r, int32_t v_r, float lamb
                               h->ent.p, fl, fc, h->fb_scratch.p, h->max_doc_nnz, dist,
                               h->flags.p, h->counters.p + 1, h->counters.p + 2, st);
     ++launches;
+    DBG_PHASE(h, st, "FP64 re-run");
   }
-  if (pe) CK(h, cudaEventRecord(pe->ev[4], st));
+  if (pe) {
+    CK(h, cudaEventRecord(pe->ev[4], st));
+    pe->complete = true;
+  }
   CK(h, cudaGetLastError());
   *launches_out = launches;
   return WMD_OK;
 }
 
+// Folds the completed queries at the front of h->events into h->phase_ms (wait: block on each
+// one, else stop at the first still running) and recycles their events.
+cudaError_t fold_events(wmd_handle* h, bool wait) {
+  while (!h->events.empty() && h->events.front().complete) {
+    PhaseEvents& pe = h->events.front();
+    if (wait) {
+      const cudaError_t e = cudaEventSynchronize(pe.ev[4]);
+      if (e != cudaSuccess) return e;
+    } else if (cudaEventQuery(pe.ev[4]) != cudaSuccess) {
+      cudaGetLastError();  // cudaErrorNotReady is not sticky, but clear it anyway
+      break;
+    }
+    float t[5];
+    for (int q = 0; q < 4; ++q) {
+      const cudaError_t e = cudaEventElapsedTime(&t[q], pe.ev[q], pe.ev[q + 1]);
+      if (e != cudaSuccess) return e;
+    }
+    const cudaError_t e = cudaEventElapsedTime(&t[4], pe.ev[0], pe.ev[4]);
+    if (e != cudaSuccess) return e;
+    for (int q = 0; q < 5; ++q) h->phase_ms[q] += t[q];
+    ++h->phase_n;
+    pe.complete = false;
+    h->event_pool.push_back(pe);
+    h->events.pop_front();
+  }
+  return cudaSuccess;
+}
+
 PhaseEvents* new_phase_events(wmd_handle* h) {
   if (!h->opt_timing) return nullptr;
+  // a query that failed after taking its events never completes them: recycle it (unless it is
+  // the begun two-phase query, whose events wmd_query_finish still records)
+  if (!h->events.empty() && !h->events.back().complete && !(h->pq.active && h->pq.pe == &h->events.back())) {
+    h->event_pool.push_back(h->events.back());
+    h->events.pop_back();
+  }
+  if (h->events.size() >= 16) fold_events(h, false);  // bounded: completed queries fold as we go
   PhaseEvents e{};
-  for (auto& x : e.ev)
-    if (cudaEventCreate(&x) != cudaSuccess) return nullptr;
+  if (!h->event_pool.empty()) {
+    e = h->event_pool.back();
+    h->event_pool.pop_back();
+  } else {
+    for (auto& x : e.ev)
+      if (cudaEventCreate(&x) != cudaSuccess) return nullptr;
+  }
+  e.complete = false;
   h->events.push_back(e);
   return &h->events.back();
 }
@@ -752,7 +843,7 @@ wmd_status enqueue_overlapped(wmd_handle* h, const int32_t* d_sel, const float* 
                               int32_t iters, float* dist, const std::function<wmd_status(cudaStream_t)>& upload) {
   bool fused = false;
   int32_t ld = 0;
-  wmd_status s = prepare_query(h, v_r, h->V, &fused, &ld);
+  wmd_status s = prepare_query(h, v_r, lambda, h->V, &fused, &ld);
   if (s != WMD_OK) return s;
   cudaStream_t main = h->stream;
   CK(h, cudaStreamWaitEvent(h->bstream, h->mx_free, 0));  // the unit's previous solve is done
@@ -782,7 +873,7 @@ wmd_status enqueue_query(wmd_handle* h, const int32_t* d_sel, const float* d_r, 
                          float lambda, int32_t iters, float* dist) {
   bool fused = false;
   int32_t ld = 0;
-  wmd_status s = prepare_query(h, v_r, h->V, &fused, &ld);
+  wmd_status s = prepare_query(h, v_r, lambda, h->V, &fused, &ld);
   if (s != WMD_OK) return s;
   int64_t launches = 0;
   if (h->opt_graph && !h->opt_timing) {
@@ -930,7 +1021,7 @@ wmd_status wmd_query_batch(wmd_handle* h, const int32_t* query_ids, const float*
   bool overlap = nq > 1 && !h->opt_graph && h->opt_path != WMD_PATH_PER_ITER;
   size_t mx_need = 0;
   for (int32_t q = 0; overlap && q < nq; ++q) {
-    const int32_t ld = wmd::fused_ld(nrow[q], h->max_doc_nnz, h->tol >= 0.0);
+    const int32_t ld = lambda >= wmd::kFusedMinLambda ? wmd::fused_ld(nrow[q], layout_doc_nnz(h), h->tol >= 0.0) : 0;
     if (ld <= 0) overlap = false;
     mx_need = std::max(mx_need, (size_t)h->V * (ld + 4) + 128);
   }
@@ -987,7 +1078,7 @@ wmd_status wmd_query_begin(wmd_handle* h, const int32_t* query_ids, const float*
   CK(h, cudaEventRecord(h->stage_ev[slot], st));
   bool fused = false;
   int32_t ld = 0;
-  s = prepare_query(h, n, table_rows, &fused, &ld);
+  s = prepare_query(h, n, lambda, table_rows, &fused, &ld);
   if (s != WMD_OK) return s;
   PhaseEvents* pe = new_phase_events(h);
   s = record_build(h, h->sel.p, n, lambda, row_begin, row_end, fused, ld, pe);
@@ -1054,19 +1145,14 @@ wmd_status wmd_sync(wmd_handle* h) {
 wmd_status wmd_get_stats(wmd_handle* h, wmd_stats* out) {
   if (!h || !out) return WMD_ERR_INVALID_ARGUMENT;
   DeviceGuard g(h->device);
+  CK(h, fold_events(h, true));
   wmd_stats s = h->st;
-  s.build_ms = s.iter_ms = s.final_ms = s.fallback_ms = s.query_ms = 0.0;
-  s.timing_valid = 0;
-  if (!h->events.empty()) {
-    CK(h, cudaEventSynchronize(h->events.back().ev[4]));
-    for (auto& pe : h->events) {
-      float t[4], all;
-      for (int q = 0; q < 4; ++q) CK(h, cudaEventElapsedTime(&t[q], pe.ev[q], pe.ev[q + 1]));
-      CK(h, cudaEventElapsedTime(&all, pe.ev[0], pe.ev[4]));
-      s.build_ms += t[0]; s.iter_ms += t[1]; s.final_ms += t[2]; s.fallback_ms += t[3]; s.query_ms += all;
-    }
-    s.timing_valid = 1;
-  }
+  s.build_ms = h->phase_ms[0];
+  s.iter_ms = h->phase_ms[1];
+  s.final_ms = h->phase_ms[2];
+  s.fallback_ms = h->phase_ms[3];
+  s.query_ms = h->phase_ms[4];
+  s.timing_valid = h->phase_n > 0;
   *out = s;
   return WMD_OK;
 }
@@ -1075,9 +1161,21 @@ wmd_status wmd_reset_stats(wmd_handle* h) {
   if (!h) return WMD_ERR_INVALID_ARGUMENT;
   DeviceGuard g(h->device);
   cudaStreamSynchronize(h->stream);
-  for (auto& pe : h->events)
-    for (auto& e : pe.ev) cudaEventDestroy(e);
-  h->events.clear();
+  for (auto& pe : h->events) {
+    if (h->pq.active && h->pq.pe == &pe) continue;  // still owned by a begun two-phase query
+    pe.complete = false;
+    h->event_pool.push_back(pe);
+  }
+  if (h->pq.active && h->pq.pe) {
+    PhaseEvents keep = *h->pq.pe;
+    h->events.clear();
+    h->events.push_back(keep);
+    h->pq.pe = &h->events.back();
+  } else {
+    h->events.clear();
+  }
+  for (double& x : h->phase_ms) x = 0.0;
+  h->phase_n = 0;
   h->st = wmd_stats{};
   return WMD_OK;
 }

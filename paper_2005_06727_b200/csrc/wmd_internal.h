@@ -1,6 +1,7 @@
 // Internal interface between the host runtime (wmd_host.cpp) and the CUDA kernels
 // (wmd_kernels.cu). Not installed; not part of the C ABI (include/wmd.h is).
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -9,6 +10,37 @@
 #define WMD_MAX_VR_DEV WMD_MAX_VR
 
 namespace wmd {
+
+// Per-device cache of a launch setting (function attributes and occupancy belong to a device
+// context, so a handle on a second GPU in the same process must not reuse the first GPU's).
+// Slot dev holds value + 1 once computed; `compute` runs on the current device. Two threads
+// racing on an empty slot both compute (cudaFuncSetAttribute is idempotent) and store the
+// same value. Static instances are zero-initialised (trivial std::atomic constructor).
+struct PerDevice {
+  static constexpr int kMaxDevices = 64;
+  std::atomic<int> slot[kMaxDevices];
+  template <class F>
+  int get(F&& compute) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return compute();
+    const int x = slot[dev].load(std::memory_order_acquire);
+    if (x) return x - 1;
+    const int v = compute();
+    slot[dev].store(v + 1, std::memory_order_release);
+    return v;
+  }
+};
+
+// Multiprocessor count of the current device (148 on B200).
+inline int device_sms() {
+  static PerDevice cache;
+  return cache.get([] {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms > 0 ? sms : 148;
+  });
+}
 
 // One CSC nonzero of the target matrix c: vocabulary word k and weight c_kj, packed so a
 // lane fetches both with one 8-byte load (D1 in SURVEY.md §2.4).
@@ -21,6 +53,8 @@ struct Entry {
 constexpr uint8_t kFlagFp32Range = 1;  // an FP32 iterate left the normal range
 constexpr uint8_t kFlagFp64 = 2;       // recomputed in FP64
 constexpr uint8_t kFlagRerun = 4;      // recomputed in FP32 by the one-CTA kernel (re-anchoring)
+constexpr uint8_t kFlagUnderflow = 16; // the one-warp kernel's FP32 block had entries below
+                                       // FLT_MIN: the range certificate was in force
 
 // Device-side per-query scalars the kernels read (written by one H2D copy per query).
 struct QueryDev {
@@ -63,6 +97,10 @@ void launch_final_wmd(const int32_t* order, const int32_t* doc_ptr, const Entry*
                       int32_t* flagged_list, int32_t* flagged_count, cudaStream_t st);
 
 // --- NEXT-1: all iterations + final step in one launch (wmd_fused.cu) ------------------------
+// The fused kernels recover M from the block in the final step (D = mu - log2(Kh) / alpha), whose
+// absolute error ~2^-22 / alpha grows as lambda shrinks (1.5e-3 of the distance at lambda = 1e-6,
+// ~1e-6 at 1e-3): below kFusedMinLambda the per-iteration path, whose final step reads M, runs.
+constexpr float kFusedMinLambda = 1e-3f;
 // Returns false if the shape is not supported by the fused kernel (the caller then uses the
 // per-iteration path). `len_prefix` (host, max_len + 2 entries): len_prefix[L] = number of
 // documents with fewer than L nonzeros, i.e. bucket boundaries in the length-sorted `order`.

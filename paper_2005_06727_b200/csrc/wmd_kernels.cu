@@ -493,13 +493,7 @@ int lanes_per_row(int ld) {
 // Persistent grid for the pass kernels: `per_sm` resident 256-thread blocks per SM, or fewer if
 // the documents (groups_per_warp per warp) do not need them.
 unsigned pass_grid(int64_t N, int ld, int per_sm) {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
+  const int sms = device_sms();
   const int ng = 32 / lanes_per_row(ld);
   const int64_t warps = (N + ng - 1) / ng;
   const int64_t need = (warps + 7) / 8;
@@ -558,11 +552,8 @@ void launch_fallback_fp64(const float* Mt, int ld, const float* rpad, int v_r,
   const int64_t need = max_doc_nnz * (v_r + 1) * 8;
   const int smem = (int)std::min<int64_t>(need, kFallbackSmem);
   const int blocks = smem <= kFallbackSmem / 2 ? kFallbackBlocks : kFallbackBlocks / 2;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(fallback_fp64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFallbackSmem);
-    attr = true;
-  }
+  static PerDevice attr;
+  attr.get([] { return (int)cudaFuncSetAttribute(fallback_fp64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFallbackSmem); });
   fallback_fp64_kernel<<<blocks, 256, smem, st>>>(Mt, ld, rpad, v_r, lambda, iters, tol, iters_doc, doc_ptr, ent,
                                                   flagged_list, flagged_count, scratch, max_doc_nnz, dist, flags,
                                                   breakdown, fallback_count, smem);
@@ -578,7 +569,7 @@ void launch_fill_i32(int32_t* p, int64_t n, int32_t v, cudaStream_t st) {
 }
 
 void launch_check_finite(const float* x, int64_t n, int32_t* bad, cudaStream_t st) {
-  check_finite_kernel<<<148 * 4, 256, 0, st>>>(x, n, bad);
+  check_finite_kernel<<<device_sms() * 4, 256, 0, st>>>(x, n, bad);
 }
 
 }  // namespace wmd

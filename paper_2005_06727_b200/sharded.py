@@ -37,6 +37,13 @@ def local_shard(col_ptr, row_idx, val, bounds, rank: int) -> Tuple[np.ndarray, n
     return cp, np.ascontiguousarray(row_idx[e0:e1]), np.ascontiguousarray(val[e0:e1])
 
 
+def global_max_doc_nnz(col_ptr) -> int:
+    """Longest document of the whole corpus (integer bookkeeping; the layout every rank of a
+    sharded run assumes, WMD_OPT_LAYOUT_DOC_NNZ)."""
+    cp = np.asarray(col_ptr, np.int64)
+    return int(np.diff(cp).max()) if cp.shape[0] > 1 else 0
+
+
 def gather_distances(local, bounds, group=None, out=None):
     """All-gather the ranks' local distance vectors (lengths bounds[g+1]-bounds[g]) into the
     global order. `local` is a 1-D float32 tensor on this rank's device (CUDA for NCCL, CPU for
@@ -108,6 +115,10 @@ class ShardedEngine:
         self.nnz_local = int(cp[-1])
         self.engine: Optional[wmd.Engine] = None
         self.engine = wmd.Engine(vocab_emb, device=device, path=path, timing=timing)
+        # every rank decides path and table width from the GLOBAL longest document (all ranks
+        # hold the global col_ptr), so the ranks agree on the layout whatever their shard holds
+        self.global_max_doc_nnz = global_max_doc_nnz(col_ptr)
+        self.engine.set_option(wmd.WMD_OPT_LAYOUT_DOC_NNZ, self.global_max_doc_nnz)
         if self.n_local > 0:
             self.engine.set_targets(cp, ri, va)
         elif self.shard_build:  # no documents, but this rank still builds and gathers its rows

@@ -32,6 +32,7 @@ import numpy as np
 __all__ = [
     "Config", "CONFIGS", "Workload", "make_workload", "make_embeddings",
     "make_corpus", "make_query", "zipf_cdf", "csc_from_lists", "subset_docs",
+    "digest", "load_manifest", "check_manifest", "make_clustered_embeddings",
 ]
 
 
@@ -214,3 +215,64 @@ def subset_docs(col_ptr, row_idx, val, docs):
     np.cumsum(lens, out=ptr[1:])
     idx = np.concatenate([np.arange(col_ptr[j], col_ptr[j + 1]) for j in docs]) if docs.size else np.zeros(0, np.int64)
     return ptr, row_idx[idx], val[idx]
+
+
+# --------------------------------------------------------------------------- input manifest
+# numpy's Generator method streams are not guaranteed stable across numpy versions, so every
+# config's generated arrays are pinned by a committed sha256 manifest (synth/manifest.json,
+# written by tools/write_manifest.py). Tests and the bench check it before comparing anything:
+# a regenerated workload that differs is an error, not a silent change of inputs.
+
+import hashlib  # noqa: E402
+import json  # noqa: E402
+import os  # noqa: E402
+
+MANIFEST = os.path.join(os.path.dirname(os.path.abspath(__file__)), "manifest.json")
+
+
+def digest(wl: "Workload") -> dict:
+    """sha256 of each generated array (little-endian bytes as stored) and of the queries."""
+    def h(*arrs):
+        m = hashlib.sha256()
+        for a in arrs:
+            m.update(np.ascontiguousarray(a).tobytes())
+        return m.hexdigest()
+    return {
+        "E": h(wl.E), "col_ptr": h(wl.col_ptr), "row_idx": h(wl.row_idx), "val": h(wl.val),
+        "queries": h(*[x for qw in wl.queries for x in qw]),
+        "shape": {"V": int(wl.E.shape[0]), "d": int(wl.E.shape[1]), "N": wl.N, "nnz": wl.nnz,
+                  "n_queries": len(wl.queries)},
+        "numpy": np.__version__,
+    }
+
+
+def load_manifest() -> dict:
+    with open(MANIFEST) as f:
+        return json.load(f)
+
+
+def check_manifest(wl: "Workload") -> None:
+    """Raises if the workload's arrays differ from the committed manifest entry of its config
+    (only full configs generated with their default N and query count are listed)."""
+    ref = load_manifest()[wl.cfg.name]
+    got = digest(wl)
+    bad = [k for k in ("E", "col_ptr", "row_idx", "val", "queries") if got[k] != ref[k]]
+    if bad or got["shape"] != ref["shape"]:
+        raise AssertionError(f"{wl.cfg.name}: generated inputs differ from synth/manifest.json in {bad or 'shape'} "
+                             f"(numpy {np.__version__}; manifest written with numpy {ref.get('numpy')})")
+
+
+def make_clustered_embeddings(seed: int, V: int, d: int, n_clusters: int = 64, spread: float = 0.15,
+                              norm_lo: float = 0.25, norm_hi: float = 4.0) -> np.ndarray:
+    """Structured embeddings (not N(0,1)): V words in n_clusters clusters, word = centre +
+    spread * N(0,1) noise, then scaled by a per-word norm factor log-uniform in [norm_lo,
+    norm_hi]. Distances then span near-zero (same cluster, similar norm) to large (different
+    clusters / norms), unlike i.i.d. Gaussians whose off-diagonal distances concentrate near
+    sqrt(2d); this stresses the FP32 range machinery (rescales, certificate, re-anchoring,
+    FP64 re-run). Random numbers only; FP64 drawn, rounded once to FP32."""
+    rng = np.random.Generator(np.random.PCG64(np.random.SeedSequence([seed, 7])))
+    centres = rng.standard_normal((n_clusters, d))
+    lab = rng.integers(0, n_clusters, size=V)
+    x = centres[lab] + spread * rng.standard_normal((V, d))
+    x *= np.exp(rng.uniform(np.log(norm_lo), np.log(norm_hi), size=V))[:, None]
+    return np.ascontiguousarray(x.astype(np.float32))

@@ -125,11 +125,32 @@ def test_create_rejects_bad_arguments_before_touching_cuda(W):
     assert e.value.status == W.WMD_ERR_INVALID_ARGUMENT
 
 
+def _innermost_loops(sass_fn):
+    """(start, end, body lines) of the innermost loops of one kernel's SASS: backward branches
+    (BRA / BRA.U to a lower address) whose body holds no other backward branch's range. Branches
+    back from the out-of-line divergence stubs after EXIT are not loops (their range spans EXIT)."""
+    lines = []
+    for ln in sass_fn.split("\n"):
+        m = re.match(r"\s+/\*([0-9a-f]{4,5})\*/\s+(.*?);", ln)
+        if m:
+            lines.append((int(m.group(1), 16), m.group(2)))
+    loops = []
+    for pc, ins in lines:
+        m = re.search(r"\bBRA(?:\.U)?\s+(?:!?U?P\d,\s*)?0x([0-9a-f]+)", ins)
+        if m and int(m.group(1), 16) < pc:
+            t = int(m.group(1), 16)
+            if not any("EXIT" in x for p2, x in lines if t <= p2 <= pc):
+                loops.append((t, pc))
+    inner = [(t, e) for t, e in loops if not any((t2, e2) != (t, e) and t <= t2 and e2 <= e for t2, e2 in loops)]
+    return [(t, e, [ins for pc, ins in lines if t <= pc <= e]) for t, e in inner]
+
+
 def test_fused_kernels_keep_the_block_in_registers(W):
-    """Resource check of the built fused kernels (ptxas -v of the in-tree build): every
-    instance keeps its Kh block in registers (at most 128 B of spill, all in the once-per-document
-    setup; a heavily spilling build faulted), and no kernel calls the IEEE-division
-    slow path on the device."""
+    """Resource check of the built fused kernels (the in-tree build's ptxas -v log and SASS): the
+    iteration loop of every fused-kernel instance (each innermost loop with >= 32 FFMA) runs
+    without a local-memory access, i.e. the Kh block stays in registers where the time goes;
+    spills are confined to the once-per-document setup and bounded; and no kernel calls the
+    IEEE-division slow path on the device."""
     import subprocess
     from paper_2005_06727_b200 import build
     logs = {s: os.path.join(build.PKG, "build", s + ".ptxas.txt") for s in ("wmd_fused.cu", "wmd_fused_cta.cu")}
@@ -142,8 +163,21 @@ def test_fused_kernels_keep_the_block_in_registers(W):
             name, spill = m.group(1), int(m.group(2))
             if "sinkhorn" in name:
                 checked += 1
-                assert spill <= 128, (src, name, spill)
+                assert spill <= 256, (src, name, spill)
     assert checked >= 20
+    loops_checked = 0
+    for src in ("wmd_fused.cu", "wmd_fused_cta.cu"):
+        sass = subprocess.run(["cuobjdump", "-sass", os.path.join(build.PKG, "build", src + ".o")],
+                              capture_output=True, text=True).stdout
+        for fn in re.split(r"\n\s*Function : ", sass)[1:]:
+            if "sinkhorn" not in fn.split("\n")[0]:
+                continue
+            for t, e, body in _innermost_loops(fn):
+                if sum(1 for ins in body if "FFMA" in ins) >= 32:
+                    loops_checked += 1
+                    bad = [ins for ins in body if re.search(r"\b(LDL|STL)\b", ins)]
+                    assert not bad, (src, fn.split("\n")[0][:120], hex(t), hex(e), bad[:3])
+    assert loops_checked >= 20
     obj = os.path.join(build.PKG, "build", "wmd_fused_cta.cu.o")
     sass = subprocess.run(["cuobjdump", "-sass", obj], capture_output=True, text=True).stdout
     if sass:

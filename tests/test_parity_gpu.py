@@ -2,6 +2,7 @@
 inputs. Distances: |gpu - oracle| <= 1e-4 |oracle| + 1e-5 (north_star 1e-4 relative, with the
 absolute floor of DESIGN.md R22 for near-zero distances). Bookkeeping (query compaction,
 partition, shard concatenation, determinism): bit-exact."""
+import os
 import numpy as np
 import pytest
 
@@ -846,3 +847,208 @@ def test_random_shapes_against_oracle(W, case):
         W.wmd_destroy(h)
     o = oracle.sinkhorn_wmd(wl.E, cp, ri, va, q, w, lam, iters)
     assert_parity(d, o, f"random case {case}: v_r={v_r} lambda={lam} iters={iters}")
+
+
+# ------------------------------------------------------------------ sharded layout agreement
+
+def _mixed_corpus(V, with_giant, seed=3):
+    """Short documents (10-40 words), then long ones (100-300), then optionally one 400-word
+    document: a 3-way nnz partition puts shards on both sides of the one-warp (64-word) and
+    one-CTA (320-word) limits."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    parts = [synth.make_corpus(rng, V, 900, 10, 40, 1.07, 0.6), synth.make_corpus(rng, V, 60, 100, 300, 1.07, 0.3)]
+    if with_giant:
+        parts.append(synth.make_corpus(rng, V, 1, 400, 400, 1.07, 0.3))
+    cps, ris, vas, off = [np.zeros(1, np.int64)], [], [], 0
+    for cp, ri, va in parts:
+        cps.append(cp[1:] + off)
+        off += int(cp[-1])
+        ris.append(ri)
+        vas.append(va)
+    return np.concatenate(cps), np.concatenate(ris), np.concatenate(vas)
+
+
+@pytest.mark.parametrize("with_giant", [False, True])
+def test_sharded_layout_agrees_across_length_thresholds(W, with_giant):
+    """Every rank sets WMD_OPT_LAYOUT_DOC_NNZ to the global longest document, so ranks whose
+    shards hold only short (or only long) documents still choose the unsharded run's path and
+    row width: the emulated table all-gather is consistent and the distances are bitwise those
+    of one handle over all documents. (Without the option, a short-document shard at v_r = 20
+    would take the one-warp width 24 while the others use the one-CTA width 32, or the fused
+    path while the others run per iteration.)"""
+    import torch
+    from paper_2005_06727_b200 import sharded
+    wl = synth.make_workload("tweet", n_queries=1, N=50)
+    V = wl.cfg.V
+    cp, ri, va = _mixed_corpus(V, with_giant)
+    rng = np.random.Generator(np.random.PCG64(9))
+    q, w = synth.make_query(rng, V, 20, 1.07, 0.6)
+    gmax = sharded.global_max_doc_nnz(cp)
+    h0 = W.wmd_create(wl.E)
+    try:
+        W.wmd_set_targets(h0, cp, ri, va)
+        ref = np.empty(cp.shape[0] - 1, np.float32)
+        W.wmd_query(h0, q, w, 10.0, 15, ref)
+        W.wmd_sync(h0)
+        st0 = W.wmd_get_stats(h0)
+    finally:
+        W.wmd_destroy(h0)
+    assert st0["last_path"] == (W.WMD_PATH_PER_ITER if with_giant else W.WMD_PATH_FUSED)
+    P = 3
+    bounds = sharded.shard_bounds(cp, P)
+    hs = []
+    try:
+        for g in range(P):
+            h = W.wmd_create(wl.E)
+            W.wmd_set_option(h, W.WMD_OPT_LAYOUT_DOC_NNZ, gmax)
+            c, r_, v_ = sharded.local_shard(cp, ri, va, bounds, g)
+            W.wmd_set_targets(h, c, r_, v_)
+            hs.append(h)
+        tabs = []
+        for g, h in enumerate(hs):
+            b, e, R = sharded.build_rows(V, P, g)
+            W.wmd_query_begin(h, q, w, 10.0, 15, b, e, table_rows=P * R)
+            tabs.append(W.wmd_query_tables(h, P * R))
+        assert len({(t[1], t[3]) for t in tabs}) == 1, "ranks disagree on the table layout"
+        torch.cuda.synchronize()
+        for g in range(P):
+            b, e, R = sharded.build_rows(V, P, g)
+            for t in (0, 2):
+                if tabs[g][t] is None:
+                    continue
+                wdt = tabs[g][t + 1]
+                for dst in range(P):
+                    if dst != g:
+                        tabs[dst][t][b * wdt:e * wdt].copy_(tabs[g][t][b * wdt:e * wdt])
+        torch.cuda.synchronize()
+        got = []
+        for g, h in enumerate(hs):
+            d = np.empty(int(bounds[g + 1] - bounds[g]), np.float32)
+            W.wmd_query_finish(h, d)
+            W.wmd_sync(h)
+            st = W.wmd_get_stats(h)
+            assert (st["last_path"], st["last_ld"]) == (st0["last_path"], st0["last_ld"])
+            got.append(d)
+    finally:
+        for h in hs:
+            W.wmd_destroy(h)
+    assert np.array_equal(np.concatenate(got), ref)
+
+
+def test_two_handles_and_counters_start_clean(W):
+    """Handles created and destroyed back to back (device memory recycled by cudaMalloc) start
+    with zeroed counters whether the embeddings come from the host or the device: no spurious
+    NUMERICAL_BREAKDOWN at the first wmd_sync."""
+    import torch
+    wl = synth.make_workload("tiny")
+    q, w = wl.queries[0]
+    for src in ("host", "device", "host"):
+        E = wl.E if src == "host" else torch.from_numpy(wl.E).cuda()
+        h = W.wmd_create(E)
+        try:
+            W.wmd_set_targets(h, wl.col_ptr, wl.row_idx, wl.val)
+            d = np.empty(wl.N, np.float32)
+            W.wmd_query(h, q, w, 10.0, 15, d)
+            W.wmd_sync(h)
+            assert W.wmd_get_stats(h)["fallback_docs"] == 0
+        finally:
+            W.wmd_destroy(h)
+
+
+def test_timing_events_are_bounded_and_fold(W):
+    """WMD_OPT_TIMING over many queries: phase times fold as queries complete (bounded event
+    count), and a begun two-phase query keeps its events across other calls."""
+    wl = synth.make_workload("tiny")
+    q, w = wl.queries[0]
+    h = W.wmd_create(wl.E)
+    try:
+        W.wmd_set_option(h, W.WMD_OPT_TIMING, 1)
+        W.wmd_set_targets(h, wl.col_ptr, wl.row_idx, wl.val)
+        d = np.empty(wl.N, np.float32)
+        for _ in range(200):
+            W.wmd_query(h, q, w, 10.0, 15, d)
+        st = W.wmd_get_stats(h)
+        assert st["timing_valid"] and st["queries"] == 200 and st["query_ms"] > 0
+        W.wmd_reset_stats(h)
+        W.wmd_query_begin(h, q, w, 10.0, 15, 0, wl.cfg.V)
+        W.wmd_get_stats(h)
+        W.wmd_query_finish(h, d)
+        st = W.wmd_get_stats(h)
+        assert st["timing_valid"] and st["queries"] == 1 and st["build_ms"] > 0
+    finally:
+        W.wmd_destroy(h)
+
+
+def test_handles_on_every_visible_device(W):
+    """One handle per visible GPU in one process (per-device launch attributes); skips with one GPU."""
+    import torch
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("one GPU visible")
+    wl = synth.make_workload("tweet", N=300)
+    q, w = wl.queries[0]
+    outs = []
+    hs = [W.wmd_create(wl.E, device=dev) for dev in range(n)]
+    try:
+        for h in hs:
+            W.wmd_set_targets(h, wl.col_ptr, wl.row_idx, wl.val)
+            d = np.empty(wl.N, np.float32)
+            W.wmd_query(h, q, w, 10.0, 15, d)
+            W.wmd_sync(h)
+            outs.append(d)
+    finally:
+        for h in hs:
+            W.wmd_destroy(h)
+    for d in outs[1:]:
+        assert np.array_equal(d, outs[0])
+
+
+def test_nccl_single_rank_group(W):
+    """The multi-GPU plumbing on a real NCCL communicator (world size 1, the only size one GPU
+    allows): ShardedEngine.query, gather_distances, the in-place table all-gather of the
+    sharded build, and the query-parallel row gather, each against the plain single-handle run."""
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_2005_06727_b200 import sharded
+    if dist.is_initialized():
+        pytest.skip("a process group already exists")
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+    try:
+        assert dist.get_backend() == "nccl"
+        wl = synth.make_workload("tweet", n_queries=3, N=800)
+        q, w = wl.queries[0]
+        ref = run_gpu(W, wl.E, wl.col_ptr, wl.row_idx, wl.val, q, w, 10.0, 15, path=0)
+        E = torch.from_numpy(wl.E).cuda()
+        eng = sharded.ShardedEngine(E, wl.col_ptr, wl.row_idx, wl.val, 0, 1, 0)
+        got = eng.query(q, w, 10.0, 15)
+        torch.cuda.synchronize()
+        assert np.array_equal(got.cpu().numpy(), ref)
+        out = sharded.gather_distances(got, np.array([0, wl.N], np.int64))
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), ref)
+        # sharded-build plumbing: the one rank builds every row, gathers in place, solves
+        h = eng.engine.h
+        b, e, R = sharded.build_rows(wl.cfg.V, 1, 0)
+        W.wmd_query_begin(h, q, w, 10.0, 15, b, e, table_rows=R)
+        mx, wm, kt, wk = W.wmd_query_tables(h, R, 0)
+        sharded.gather_table(mx, R, wm, 1, 0)
+        d = torch.empty(wl.N, dtype=torch.float32, device="cuda:0")
+        W.wmd_query_finish(h, d)
+        torch.cuda.synchronize()
+        assert np.array_equal(d.cpu().numpy(), ref)
+        eng.close()
+        qp = sharded.QueryParallelEngine(E, wl.col_ptr, wl.row_idx, wl.val, 0, 1, 0)
+        rows = qp.engine.query_batch(wl.queries, 10.0, 15)
+        full = sharded.gather_query_rows(rows, len(wl.queries), 1)
+        torch.cuda.synchronize()
+        assert np.array_equal(full.cpu().numpy(), rows.cpu().numpy())
+        assert np.array_equal(full[0].cpu().numpy(), ref)
+        qp.close()
+    finally:
+        dist.destroy_process_group()
