@@ -95,7 +95,10 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW>()) sinkhorn_f
   extern __shared__ __align__(16) float smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int a = lane >> 3, b = lane & 7;
-  float* const buf = smem + wib * S::BUF;        // the staged M rows of the warp's document
+  // the staged M rows: two buffers per warp, the current document's (read again by the final
+  // step) and the next document's (filled by cp.async while the current one iterates)
+  float* const buf0 = smem + 2 * wib * S::BUF;
+  int cur = 0;                                   // buffer of the current document
   const int64_t stride = (int64_t)gridDim.x * kWarps;
   const uint64_t keep = l2_evict_last_policy();         // the gathered M rows stay in L2
   const uint64_t stream_pol = l2_evict_first_policy();  // c is read once
@@ -147,7 +150,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW>()) sinkhorn_f
         uint32_t k;  // opaque copy: keeps the address arithmetic (and its wait on the entry
         asm volatile("mov.b32 %0, %1;" : "=r"(k) : "r"(pk[w]));  // load) at this point
         const float* src = Mx + (size_t)k * P;
-        const uint32_t dst = smem_u32(buf + e * P);
+        const uint32_t dst = smem_u32(buf0 + (cur ^ 1) * S::BUF + e * P);
 #pragma unroll
         for (int q = 0; q < P / 4; ++q) cp_async16(dst + 16 * q, src + 4 * q, keep);
       }
@@ -155,11 +158,14 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW>()) sinkhorn_f
     cp_async_commit();
   };
 
+  cur = 1;       // the first document's rows go to buffer 0 (cur ^ 1)
   stage1(pos);
   stage2();
   stage3();
 
   for (; pos < pos1; pos += stride) {
+    cur ^= 1;      // this document's rows are in buffer cur; the next one's go to cur ^ 1
+    const float* const buf = buf0 + cur * S::BUF;
     const int j = pj, n = pn;
     // c of the lane's own rows: row 32T + lane (full tiles), tail row 32NT + TW a + (b >> TSH)
     float c_own[NOWN];
@@ -180,24 +186,26 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW>()) sinkhorn_f
 
     // ---- block tile: D = M - m, mu = column minima over the document, Kh = 2^(-alpha (D - mu))
     float K[RW][CW];
-    float u[CW], mu_s[CW], m_own[NOWN];
+    float u[CW];
     bool und;
     {
       float mu[CW];
 #pragma unroll
-      for (int c = 0; c < CW; ++c) mu[c] = FLT_MAX;
-      // branch-free: rows past n read a staged row (stale contents) and are masked by selects
+      for (int c = 0; c < CW; ++c) mu[c] = INFINITY;
+      // branch-free: rows past n read a staged row (stale contents); their D is +inf through the
+      // per-row bias (so they drop out of the minima) and their Kh is set to 1 below
+      bool rok[RW];
 #pragma unroll
       for (int s = 0; s < RW; ++s) {
         const int e = row_of<NT, TW>(s, a, b);
-        const bool ok = e < n;
-        const float* row = buf + (ok ? e : 0) * P;
+        rok[s] = e < n;
+        const float* row = buf + (rok[s] ? e : 0) * P;
         float x[CW];
         load_cols<CW>(row, b, x);
-        const float me = row[LD];
+        const float bias = rok[s] ? -row[LD] : INFINITY;
 #pragma unroll
         for (int c = 0; c < CW; ++c) {
-          K[s][c] = ok ? x[c] - me : FLT_MAX;   // rows past n: FLT_MAX until Kh is formed
+          K[s][c] = x[c] + bias;   // D = M - m
           mu[c] = fminf(mu[c], K[s][c]);
         }
       }
@@ -206,42 +214,36 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW>()) sinkhorn_f
         mu[c] = fminf(mu[c], shx(mu[c], 8));
         mu[c] = fminf(mu[c], shx(mu[c], 16));
       }
-      float amu[CW];
+      float amu[CW], kmin[CW];
 #pragma unroll
-      for (int c = 0; c < CW; ++c) amu[c] = alpha * mu[c];
-      bool flushed = false;
+      for (int c = 0; c < CW; ++c) {
+        amu[c] = alpha * mu[c];
+        kmin[c] = 1.f;
+      }
 #pragma unroll
       for (int s = 0; s < RW; ++s) {
 #pragma unroll
         for (int c = 0; c < CW; ++c) {
-          const float dd = K[s][c];
-          const float kx = ex2_ftz(fmaf(-alpha, dd, amu[c]));
-          flushed |= nreal[c] && kx < FLT_MIN && dd != FLT_MAX;
-          // padded columns (u = 0) and rows past n (c = 0, so v = 0) hold 1: every row sum s
-          // stays positive and no select is needed in the loop
-          K[s][c] = (nreal[c] && dd != FLT_MAX) ? kx : 1.f;
+          // rows past n hold 1 (their c = 0 makes v = 0, and every row sum s stays positive);
+          // padded columns keep their finite value (their uh = 0 cancels it everywhere)
+          K[s][c] = rok[s] ? ex2_ftz(fmaf(-alpha, K[s][c], amu[c])) : 1.f;
+          kmin[c] = fminf(kmin[c], K[s][c]);
         }
         to_slots<CW>(K[s], a);
       }
+      bool flushed = false;   // a real entry flushed to 0 (true value < 2^-126)
+#pragma unroll
+      for (int c = 0; c < CW; ++c) flushed |= nreal[c] && kmin[c] < FLT_MIN;
       und = __any_sync(kFull, flushed);
-      // for the final step (which then needs no M): m of the own rows, mu in slot order
-#pragma unroll
-      for (int T = 0; T < NT; ++T) m_own[T] = v_ok[T] ? buf[(32 * T + lane) * P + LD] : 0.f;
-      if constexpr (TW > 0)
-        m_own[NT] = v_ok[NT] ? buf[(32 * NT + TW * a + (b >> S::TSH)) * P + LD] : 0.f;
-#pragma unroll
-      for (int c = 0; c < CW; ++c) mu_s[c] = mu[c];
-      to_slots<CW>(mu_s, a);
       // uh0 = v_r 2^(-alpha mu) on real columns (slot order)
 #pragma unroll
       for (int c = 0; c < CW; ++c) u[c] = nreal[c] ? (float)v_r * ex2_ftz(-alpha * mu[c]) : 0.f;
       to_slots<CW>(u, a);
     }
-    __syncwarp();  // every lane is done with the staged rows: the buffer takes the next document
     stage2();      // the next document's entries (its header load was issued above)
 
     // ---- iterations, then the final step
-    float v_own[NOWN], s_own[NOWN];
+    float v_own[NOWN];
     bool bad = false;          // range certificate failed (blocks with flushed entries only)
     float umin = FLT_MAX;      // smallest real uh after a gauge: must stay normal
     uint32_t umax_all = 0u;    // largest uh before a gauge (bits): must stay finite
@@ -269,7 +271,6 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW>()) sinkhorn_f
 #pragma unroll
         for (int o = 0; o < NOWN; ++o) {
           const float sv = p[8 * o];
-          s_own[o] = sv;
           v_own[o] = c_own[o] * rcp_fast(sv);
           if constexpr (UND) {
             bad |= v_ok[o] && umax_k > sv;
@@ -361,36 +362,26 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW>()) sinkhorn_f
     if (und) iterate(std::true_type{});
     else iterate(std::false_type{});
 
-    // ---- final step: WMD_j = sum_e vh_e q_e,  q_e = sum_i Kh_ei M_ie uh_i
-    // M is recovered from the block itself: Kh = 2^(-alpha (D - mu)) gives
-    //   M_ie = D_ei + m_e = mu_i + m_e - log2(Kh_ei) / alpha,
-    // so q_e = sum_i Kh_ei uh_i (mu_i - log2(Kh_ei)/alpha) + m_e s_e with s_e = Kh uh from the
-    // last SDDMM. Entries flushed to 0 contribute 0 (Kh log2 Kh -> 0). The recovery's absolute
-    // error in D is ~2^-22 / alpha: below lambda = kFusedMinLambda (wmd_internal.h) the host
-    // routes the query to the per-iteration path, whose final step reads M.
+    // ---- final step: WMD_j = sum_e vh_e q_e,  q_e = sum_i Kh_ei M_ie uh_i, with
+    // M read back from the document's staged rows (still in buffer cur): each slot's column is
+    // read directly at its XOR-permuted position (col_of), matching Kh and uh slot by slot.
+    // (rows past n read a staged row and are left out of the sum below)
     float p[RW];
-    {
-      const float ia = -rcp_fast(alpha);  // (approximate: no IEEE-division slow-path call)
 #pragma unroll
-      for (int s = 0; s < RW; ++s) {
-        float acc = 0.f;
+    for (int s = 0; s < RW; ++s) {
+      const float* row = buf + row_of<NT, TW>(s, a, b) * P;
+      float acc = 0.f;
 #pragma unroll
-        for (int c = 0; c < CW; ++c) {
-          const float k = K[s][c];
-          const float kl = k > 0.f ? k * lg2_approx(k) : 0.f;
-          acc = fmaf(fmaf(kl, ia, k * mu_s[c]), u[c], acc);
-        }
-        p[s] = acc;
-      }
+      for (int c = 0; c < CW; ++c) acc = fmaf(K[s][c] * u[c], row[col_of<CW>(c, a, b)], acc);
+      p[s] = acc;
     }
     reduce_rows<NT, TW>(p);
     float wsum = 0.f;
 #pragma unroll
     for (int T = 0; T < NT; ++T)
-      if (v_ok[T]) wsum = fmaf(v_own[T], fmaf(m_own[T], s_own[T], p[8 * T]), wsum);
+      if (v_ok[T]) wsum = fmaf(v_own[T], p[8 * T], wsum);
     if constexpr (TW > 0) {  // each tail row is held by 2^TSH lanes: count it once
-      if (v_ok[NT] && (b & ((1 << S::TSH) - 1)) == 0)
-        wsum = fmaf(v_own[NT], fmaf(m_own[NT], s_own[NT], p[8 * NT]), wsum);
+      if (v_ok[NT] && (b & ((1 << S::TSH) - 1)) == 0) wsum = fmaf(v_own[NT], p[8 * NT], wsum);
     }
 #pragma unroll
     for (int off = 16; off; off >>= 1) wsum += shx(wsum, off);
@@ -416,7 +407,7 @@ void launch_fused_range_t(const int4* sdoc, const Entry* ent, int64_t p0,
                         int iters, float tol, int32_t* itd, float* dist, uint8_t* flags, int32_t* fl,
                         int32_t* fc, cudaStream_t st) {
   if (p1 <= p0) return;
-  constexpr size_t smem = sizeof(float) * Shape<CW, NT, TW>::BUF * kWarps;
+  constexpr size_t smem = sizeof(float) * Shape<CW, NT, TW>::BUF * kWarps * 2;  // two row buffers per warp
   static PerDevice cache;
   const int resident = cache.get([&] {
     cudaFuncSetAttribute(sinkhorn_fused_kernel<CW, NT, TW, CONV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
