@@ -87,6 +87,11 @@ typedef enum {
                               re-uploaded every call); per-phase timing is off in this mode.
                               Default 0 */
   WMD_OPT_BUILD = 5,       /* distance build (a2), a wmd_build value; default WMD_BUILD_DIRECT */
+  WMD_OPT_BATCH = 7,       /* wmd_query_batch, queries per fused pass (NEXT-2 (ii)): 0 = automatic
+                              (as many tables as fit in half the L2, at most 16; default),
+                              1 = one query at a time, 2..64 = that many. Applies when every query
+                              takes the one-warp kernel for every document, no tolerance is set and
+                              graph mode is off; results are bitwise those of single queries */
   WMD_OPT_LAYOUT_DOC_NNZ = 6 /* >= 0: the path and table-width decision of every query assumes the
                               longest document has max(this, local longest) words. A document-
                               sharded run passes the GLOBAL longest document on every
@@ -178,10 +183,15 @@ WMD_API wmd_status wmd_query(wmd_handle* h, const int32_t* query_ids, const floa
  * Every query is validated before any work is enqueued (all-or-nothing; the message names the
  * first bad query). The rows of all queries go to the device in one copy; the queries then run
  * back to back with no host round trip between them (each: build, Sinkhorn, final, re-runs).
- * When every query takes the fused path (and graph mode is off), query q's table is built on a
+ * When every query takes the one-warp fused kernel (documents of at most 64 words at v_r <= 64,
+ * no tolerance, no graph mode), the queries are solved B at a time (WMD_OPT_BATCH): one fused
+ * pass per length bucket serves B queries, reading each document's entries once for all of them
+ * (NEXT-2 (ii)). Otherwise, when every query takes the fused path, query q's table is built on a
  * second internal stream into one of two tables while query q-1 is solved on the handle's
- * stream; the call's work is complete on the handle's stream when it returns (device output) or
- * synchronised (host output). Results equal nq separate wmd_query calls bit for bit.
+ * stream. The call's work is complete on the handle's stream when it returns (device output) or
+ * synchronised (host output). Results equal nq separate wmd_query calls bit for bit; the
+ * introspection calls (wmd_read_flags, wmd_get_query_rows, wmd_sync's counts) report the last
+ * query.
  * Errors: as wmd_query, plus INVALID_ARGUMENT for nq < 1 or bad q_ptr. */
 WMD_API wmd_status wmd_query_batch(wmd_handle* h, const int32_t* query_ids, const float* query_weights,
                            const int64_t* q_ptr, int32_t nq, float lambda, int32_t iters,

@@ -78,13 +78,14 @@ constexpr int min_blocks() {
   return b < 1 ? 1 : (b > 8 ? 8 : b);
 }
 
+// Items: (document, query) pairs, document-major: a warp takes a document (grid stride over the
+// length-sorted positions) and solves it for the qs.nq queries in turn, so the document's
+// header and entries (c) are read once per batch; only its M rows differ per query (each query
+// has its own table). The per-query lane constants are reloaded when the query changes.
 template <int CW, int NT, int TW, bool CONV>
 __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW>()) sinkhorn_fused_kernel(
     const int4* __restrict__ sdoc, const Entry* __restrict__ ent, int64_t pos0, int64_t pos1,
-    const float* __restrict__ Mx, int v_r, const float* __restrict__ rpad, float lambda, int iters,
-    float tol, int32_t* __restrict__ iters_doc, float* __restrict__ dist,
-    uint8_t* __restrict__ flags, int32_t* __restrict__ flagged_list,
-    int32_t* __restrict__ flagged_count) {
+    QuerySet qs, float lambda, int iters, float tol) {
   using S = Shape<CW, NT, TW>;
   constexpr int LD = S::LD, RW = S::RW, NW = S::NW, P = S::P;
   constexpr int NOWN = NT + (TW ? 1 : 0);        // own rows per lane after the row reduce
@@ -95,36 +96,50 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW>()) sinkhorn_f
   extern __shared__ __align__(16) float smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int a = lane >> 3, b = lane & 7;
-  // the staged M rows: two buffers per warp, the current document's (read again by the final
-  // step) and the next document's (filled by cp.async while the current one iterates)
+  // the staged M rows: two buffers per warp, the current item's (read again by the final step)
+  // and the next item's (filled by cp.async while the current one iterates)
   float* const buf0 = smem + 2 * wib * S::BUF;
-  int cur = 0;                                   // buffer of the current document
+  int cur = 1;                                   // buffer of the current item (flipped per item)
   const int64_t stride = (int64_t)gridDim.x * kWarps;
   const uint64_t keep = l2_evict_last_policy();         // the gathered M rows stay in L2
   const uint64_t stream_pol = l2_evict_first_policy();  // c is read once
   const int2* ent2 = reinterpret_cast<const int2*>(ent);
   const float alpha = lambda * kLog2e;          // exp(-lambda x) = 2^(-alpha x)
-  const float kv_s = (float)v_r * kUnder;
+  const int nq = qs.nq;
 
-  // own columns (after the column reduce) and their marginals r_i (zero beyond v_r)
+  // per-query constants of the current item: width, own columns (after the column reduce) and
+  // their marginals r_i (zero beyond v_r), real natural-order columns of the lane's group
+  int v_r = 0;
+  float kv_s = 0.f;
   float r_own[NCO];
-  bool oreal[NCO];
+  bool oreal[NCO], nreal[CW];
+  int64_t out0 = 0;               // the current query's distance row
+  auto set_query = [&](int q) {
+    const int g = qs.qmap ? __ldg(qs.qmap + q) : q;
+    out0 = (int64_t)g * qs.N;
+    v_r = qs.vr ? __ldg(qs.vr + g) : qs.v_r;
+    kv_s = (float)v_r * kUnder;
+    const float* rp = qs.rpad + (size_t)g * WMD_MAX_VR_DEV;
 #pragma unroll
-  for (int g = 0; g < NCO; ++g) {
-    const int oc = CW >= 3 ? (g < CQ ? 32 * g + 4 * b + a : 32 * CQ + CR * b + (g - CQ))
-                           : (CW == 2 ? 2 * b + (a >> 1) : b);
-    r_own[g] = __ldg(rpad + oc);
-    oreal[g] = oc < v_r;
-  }
-  bool nreal[CW];  // natural-order columns of this lane's group are real query rows
+    for (int g = 0; g < NCO; ++g) {
+      const int oc = CW >= 3 ? (g < CQ ? 32 * g + 4 * b + a : 32 * CQ + CR * b + (g - CQ))
+                             : (CW == 2 ? 2 * b + (a >> 1) : b);
+      r_own[g] = __ldg(rp + oc);
+      oreal[g] = oc < v_r;
+    }
 #pragma unroll
-  for (int c = 0; c < CW; ++c) nreal[c] = nat_col<CW>(c, b) < v_r;
+    for (int c = 0; c < CW; ++c) nreal[c] = nat_col<CW>(c, b) < v_r;
+  };
 
-  // ---- prefetch: stage 1 (document header), stage 2 (entries), stage 3 (cp.async of M rows)
+  // ---- prefetch: stage 1 (next document's header), stage 2 (its entries), stage 3 (cp.async of
+  // the next item's M rows)
   int64_t pos = pos0 + (int64_t)blockIdx.x * kWarps + wib;
-  int pj = -1, pb = 0, pn = 0;
+  int pj = -1, pb = 0, pn = 0;     // next document
   int pk[NW];
   float pc[NW];
+  int cj, cn;                      // current document
+  int ck[NW];
+  float cc[NW];
   auto stage1 = [&](int64_t p) {
     pj = -1; pn = 0; pb = 0;
     if (p < pos1) {  // {document id, first nonzero, length, -} (a load that stays guarded)
@@ -142,45 +157,53 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW>()) sinkhorn_f
       pc[w] = __int_as_float(x.y);   // 0 on rows past the document: v = 0 there
     }
   };
-  auto stage3 = [&]() {
+  auto stage3 = [&](const int (&ids)[NW], int nrows, int q) {
+    const float* tab = qs.Mx + (size_t)q * qs.mx_stride;
 #pragma unroll
     for (int w = 0; w < NW; ++w) {
       const int e = lane + 32 * w;
-      if (e < pn) {
+      if (e < nrows) {
         uint32_t k;  // opaque copy: keeps the address arithmetic (and its wait on the entry
-        asm volatile("mov.b32 %0, %1;" : "=r"(k) : "r"(pk[w]));  // load) at this point
-        const float* src = Mx + (size_t)k * P;
+        asm volatile("mov.b32 %0, %1;" : "=r"(k) : "r"(ids[w]));  // load) at this point
+        const float* src = tab + (size_t)k * P;
         const uint32_t dst = smem_u32(buf0 + (cur ^ 1) * S::BUF + e * P);
 #pragma unroll
-        for (int q = 0; q < P / 4; ++q) cp_async16(dst + 16 * q, src + 4 * q, keep);
+        for (int x = 0; x < P / 4; ++x) cp_async16(dst + 16 * x, src + 4 * x, keep);
       }
     }
     cp_async_commit();
   };
+  auto take_next_doc = [&]() {
+    cj = pj; cn = pn;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) { ck[w] = pk[w]; cc[w] = pc[w]; }
+  };
 
-  cur = 1;       // the first document's rows go to buffer 0 (cur ^ 1)
   stage1(pos);
   stage2();
-  stage3();
+  stage3(pk, pn, 0);
+  take_next_doc();
+  int q = 0;
 
-  for (; pos < pos1; pos += stride) {
-    cur ^= 1;      // this document's rows are in buffer cur; the next one's go to cur ^ 1
+  while (pos < pos1) {
+    cur ^= 1;      // this item's rows are in buffer cur; the next item's go to cur ^ 1
     const float* const buf = buf0 + cur * S::BUF;
-    const int j = pj, n = pn;
+    const int j = cj, n = cn;
+    set_query(q);
     // c of the lane's own rows: row 32T + lane (full tiles), tail row 32NT + TW a + (b >> TSH)
     float c_own[NOWN];
     bool v_ok[NOWN];
 #pragma unroll
     for (int T = 0; T < NT; ++T) {
-      c_own[T] = pc[T];
+      c_own[T] = cc[T];
       v_ok[T] = 32 * T + lane < n;
     }
     if constexpr (TW > 0) {
       const int tr = TW * a + (b >> S::TSH);
-      c_own[NT] = __shfl_sync(kFull, pc[NT], tr);
+      c_own[NT] = __shfl_sync(kFull, cc[NT], tr);
       v_ok[NT] = 32 * NT + tr < n;
     }
-    stage1(pos + stride);
+    if (q == 0) stage1(pos + stride);   // the next document's header
     cp_async_wait_all();
     __syncwarp();
 
@@ -240,7 +263,12 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW>()) sinkhorn_f
       for (int c = 0; c < CW; ++c) u[c] = nreal[c] ? (float)v_r * ex2_ftz(-alpha * mu[c]) : 0.f;
       to_slots<CW>(u, a);
     }
-    stage2();      // the next document's entries (its header load was issued above)
+    if (q == nq - 1) stage2();   // the next document's entries (its header load was issued above)
+    // the next item's rows: the same document for the next query, else the next document
+    auto stage3_next = [&]() {
+      if (q + 1 < nq) stage3(ck, n, q + 1);
+      else stage3(pk, pn, 0);
+    };
 
     // ---- iterations, then the final step
     float v_own[NOWN];
@@ -349,14 +377,14 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW>()) sinkhorn_f
         col_step();
         it = 1;
         row_step();
-        stage3();  // the next document's entries have landed: start its row copies
+        stage3_next();  // the next document's entries have landed: start its row copies
         while (it != iters && !(CONV && done)) {
           col_step();
           ++it;
           row_step();
         }
       } else {
-        stage3();
+        stage3_next();
       }
     };
     if (und) iterate(std::true_type{});
@@ -388,24 +416,30 @@ __global__ void __launch_bounds__(kThreads, min_blocks<CW, NT, TW>()) sinkhorn_f
     const bool flag = __any_sync(kFull, bad || !(umin >= FLT_MIN)) || umax_all > 0x7f7fffffu ||
                       !(fabsf(wsum) <= FLT_MAX);
     if (lane == 0) {
-      dist[j] = wsum;
-      if (iters_doc) iters_doc[j] = it;
+      const int64_t o = (int64_t)q * qs.N + j;
+      qs.dist[out0 + j] = wsum;
+      if (qs.iters_doc) qs.iters_doc[o] = it;
       uint8_t f = und ? kFlagUnderflow : 0;
       if (flag) {
         f |= kFlagFp32Range;
-        flagged_list[atomicAdd(flagged_count, 1)] = j;
+        qs.flagged_list[(int64_t)q * qs.N + atomicAdd(qs.flagged_count + q, 1)] = j;
       }
-      if (f) flags[j] |= f;
+      if (f) qs.flags[o] |= f;
+    }
+    if (q + 1 < nq) {
+      ++q;
+    } else {
+      q = 0;
+      pos += stride;
+      take_next_doc();
     }
   }
   cp_async_wait_all();  // nothing may be in flight when the warp exits
 }
 
 template <int CW, int NT, int TW, bool CONV>
-void launch_fused_range_t(const int4* sdoc, const Entry* ent, int64_t p0,
-                        int64_t p1, const float* Mx, int v_r, const float* rpad, float lambda,
-                        int iters, float tol, int32_t* itd, float* dist, uint8_t* flags, int32_t* fl,
-                        int32_t* fc, cudaStream_t st) {
+void launch_fused_range_t(const int4* sdoc, const Entry* ent, int64_t p0, int64_t p1, const QuerySet& qs,
+                          float lambda, int iters, float tol, cudaStream_t st) {
   if (p1 <= p0) return;
   constexpr size_t smem = sizeof(float) * Shape<CW, NT, TW>::BUF * kWarps * 2;  // two row buffers per warp
   static PerDevice cache;
@@ -418,18 +452,16 @@ void launch_fused_range_t(const int4* sdoc, const Entry* ent, int64_t p0,
   });
   const int64_t need = (p1 - p0 + kWarps - 1) / kWarps;
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, resident));
-  sinkhorn_fused_kernel<CW, NT, TW, CONV><<<grid, kThreads, smem, st>>>(sdoc, ent, p0, p1, Mx, v_r, rpad,
-                                                                   lambda, iters, tol, itd, dist, flags, fl, fc);
+  sinkhorn_fused_kernel<CW, NT, TW, CONV><<<grid, kThreads, smem, st>>>(sdoc, ent, p0, p1, qs, lambda, iters, tol);
 }
 
 template <int CW, int NT, int TW>
-void launch_fused_range(const int4* sdoc, const Entry* ent, int64_t p0, int64_t p1, const float* Mx, int v_r,
-                        const float* rpad, float lambda, int iters, float tol, int32_t* itd, float* dist,
-                        uint8_t* flags, int32_t* fl, int32_t* fc, cudaStream_t st) {
+void launch_fused_range(const int4* sdoc, const Entry* ent, int64_t p0, int64_t p1, const QuerySet& qs,
+                        float lambda, int iters, float tol, cudaStream_t st) {
   if (tol >= 0.f)
-    launch_fused_range_t<CW, NT, TW, true>(sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, tol, itd, dist, flags, fl, fc, st);
+    launch_fused_range_t<CW, NT, TW, true>(sdoc, ent, p0, p1, qs, lambda, iters, tol, st);
   else
-    launch_fused_range_t<CW, NT, TW, false>(sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, tol, itd, dist, flags, fl, fc, st);
+    launch_fused_range_t<CW, NT, TW, false>(sdoc, ent, p0, p1, qs, lambda, iters, tol, st);
 }
 
 // Length buckets (rows covered: 8, 16, 32, 40, 48, 64) over the length-sorted order.
@@ -440,12 +472,10 @@ constexpr int kNumBuckets = 6;
 constexpr bool fits(int cw, int ne) { return (ne / 4) * cw <= 96; }  // block registers per lane
 
 template <int CW>
-void dispatch_bucket(int bi, const int4* sdoc, const Entry* ent, int64_t p0,
-                     int64_t p1, const float* Mx, int v_r, const float* rpad, float lambda, int iters,
-                     float tol, int32_t* itd, float* dist, uint8_t* flags, int32_t* fl, int32_t* fc,
-                     cudaStream_t st) {
+void dispatch_bucket(int bi, const int4* sdoc, const Entry* ent, int64_t p0, int64_t p1, const QuerySet& qs,
+                     float lambda, int iters, float tol, cudaStream_t st) {
 #define F_(NT, TW) \
-  if constexpr (fits(CW, 32 * NT + 4 * TW)) launch_fused_range<CW, NT, TW>(sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, tol, itd, dist, flags, fl, fc, st)
+  if constexpr (fits(CW, 32 * NT + 4 * TW)) launch_fused_range<CW, NT, TW>(sdoc, ent, p0, p1, qs, lambda, iters, tol, st)
   switch (bi) {
     case 0: F_(0, 2); break;
     case 1: F_(0, 4); break;
@@ -480,13 +510,11 @@ int fused_ld(int v_r, int64_t max_doc_nnz, bool conv) {
 }
 
 void launch_sinkhorn_fused(const int4* sdoc, const Entry* ent, int64_t N,
-                           const int64_t* len_prefix, int64_t max_len, const float* Mx, int ld,
-                           int v_r, const float* rpad, float lambda, int iters, float tol,
-                           int32_t* iters_doc, float* dist, uint8_t* flags, int32_t* flagged_list,
-                           int32_t* flagged_count, cudaStream_t st0, StreamRing* ring) {
+                           const int64_t* len_prefix, int64_t max_len, int ld, const QuerySet& qs,
+                           float lambda, int iters, float tol, cudaStream_t st0, StreamRing* ring) {
   // len_prefix[L] = number of documents with fewer than L nonzeros: the length-sorted order
   // splits into buckets of at most 8 / 16 / 32 / 40 / 48 / 64 nonzeros (one-warp kernel, one
-  // launch each) and, past warp_max_rows(ld), 64 / 128 / ... / 320 (one-CTA kernel).
+  // launch each) and, past warp_max_rows(ld), 64 / 128 / ... / 320 (one-CTA kernel, one query).
   const int wmax = warp_max_rows(ld);
   int64_t p0 = 0;
   for (int bi = 0; bi < kNumBuckets && p0 < N && kBuckets[bi].ne <= wmax; ++bi) {
@@ -495,21 +523,21 @@ void launch_sinkhorn_fused(const int4* sdoc, const Entry* ent, int64_t N,
     if (p1 > p0) {
       const cudaStream_t st = ring ? ring->next(st0) : st0;
       switch (ld) {
-        case 8: dispatch_bucket<1>(bi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, tol, iters_doc, dist, flags, flagged_list, flagged_count, st); break;
-        case 16: dispatch_bucket<2>(bi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, tol, iters_doc, dist, flags, flagged_list, flagged_count, st); break;
-        case 32: dispatch_bucket<4>(bi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, tol, iters_doc, dist, flags, flagged_list, flagged_count, st); break;
-        case 24: dispatch_bucket<3>(bi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, tol, iters_doc, dist, flags, flagged_list, flagged_count, st); break;
-        case 40: dispatch_bucket<5>(bi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, tol, iters_doc, dist, flags, flagged_list, flagged_count, st); break;
-        case 48: dispatch_bucket<6>(bi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, tol, iters_doc, dist, flags, flagged_list, flagged_count, st); break;
-        case 64: dispatch_bucket<8>(bi, sdoc, ent, p0, p1, Mx, v_r, rpad, lambda, iters, tol, iters_doc, dist, flags, flagged_list, flagged_count, st); break;
+        case 8: dispatch_bucket<1>(bi, sdoc, ent, p0, p1, qs, lambda, iters, tol, st); break;
+        case 16: dispatch_bucket<2>(bi, sdoc, ent, p0, p1, qs, lambda, iters, tol, st); break;
+        case 24: dispatch_bucket<3>(bi, sdoc, ent, p0, p1, qs, lambda, iters, tol, st); break;
+        case 32: dispatch_bucket<4>(bi, sdoc, ent, p0, p1, qs, lambda, iters, tol, st); break;
+        case 40: dispatch_bucket<5>(bi, sdoc, ent, p0, p1, qs, lambda, iters, tol, st); break;
+        case 48: dispatch_bucket<6>(bi, sdoc, ent, p0, p1, qs, lambda, iters, tol, st); break;
+        case 64: dispatch_bucket<8>(bi, sdoc, ent, p0, p1, qs, lambda, iters, tol, st); break;
         default: break;
       }
     }
     p0 = std::max(p0, p1);
   }
-  if (p0 < N)
-    launch_sinkhorn_cta(sdoc, ent, p0, N, len_prefix, max_len, Mx, ld, v_r, rpad, lambda, iters, iters_doc,
-                        dist, flags, flagged_list, flagged_count, st0, ring);
+  if (p0 < N && qs.nq == 1)
+    launch_sinkhorn_cta(sdoc, ent, p0, N, len_prefix, max_len, qs.Mx, ld, qs.v_r, qs.rpad, lambda, iters,
+                        qs.iters_doc, qs.dist, qs.flags, qs.flagged_list, qs.flagged_count, st0, ring);
 }
 
 int fused_launch_count(const int64_t* len_prefix, int64_t max_len, int64_t N, int ld) {

@@ -156,6 +156,13 @@ struct wmd_handle {
   // batched queries (wmd_query_batch): device rows, pinned staging, host-output buffer
   DevBuf<int32_t> bsel;
   DevBuf<float> brpad, batch_dist;
+  // batched fused passes (NEXT-2 (ii)): widths and width-sorted order of the batch's queries,
+  // B side-by-side tables, batch-local flags / flagged lists / counts
+  DevBuf<int32_t> bvr, bqmap, bflagged, bcount;
+  DevBuf<float> Mxb[2];                            // tables of two passes: the next pass's builds
+  cudaEvent_t mxb_free[2] = {nullptr, nullptr};    // (build stream) overlap this pass's solve
+  cudaEvent_t up_ev = nullptr;                     // the batch's uploads are on the device
+  DevBuf<uint8_t> bflags;
   void* batch_stage = nullptr;
   size_t batch_stage_bytes = 0;
   cudaEvent_t batch_ev = nullptr;
@@ -183,6 +190,7 @@ struct wmd_handle {
   int64_t opt_path = WMD_PATH_AUTO, opt_timing = 0, opt_fallback = 1, opt_graph = 0;
   int64_t opt_build = WMD_BUILD_DIRECT;  // WMD_OPT_BUILD
   int64_t opt_layout_nnz = 0;  // WMD_OPT_LAYOUT_DOC_NNZ
+  int64_t opt_batch = 0;       // WMD_OPT_BATCH
   // stats
   wmd_stats st{};
   // per-phase timing (WMD_OPT_TIMING): events of queries in flight (a deque: push_back /
@@ -455,6 +463,10 @@ wmd_status wmd_create(const float* vocab_emb, int64_t V, int32_t d, int32_t devi
       h->counters.ensure(6) != cudaSuccess)
     return bail(WMD_ERR_OUT_OF_MEMORY);
   if (cudaEventCreateWithFlags(&h->batch_ev, cudaEventDisableTiming) != cudaSuccess) return bail(WMD_ERR_CUDA);
+  if (cudaEventCreateWithFlags(&h->up_ev, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->mxb_free[0], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->mxb_free[1], cudaEventDisableTiming) != cudaSuccess)
+    return bail(WMD_ERR_CUDA);
   if (cudaEventCreateWithFlags(&h->fork_ev, cudaEventDisableTiming) != cudaSuccess) return bail(WMD_ERR_CUDA);
   if (cudaStreamCreateWithFlags(&h->bstream, cudaStreamNonBlocking) != cudaSuccess) return bail(WMD_ERR_CUDA);
   if (cudaEventCreateWithFlags(&h->built_ev, cudaEventDisableTiming) != cudaSuccess ||
@@ -490,6 +502,12 @@ void wmd_destroy(wmd_handle* h) {
   if (h->batch_stage) cudaFreeHost(h->batch_stage);
   if (h->batch_ev) cudaEventDestroy(h->batch_ev);
   h->bsel.release(); h->brpad.release(); h->batch_dist.release();
+  h->bvr.release(); h->bqmap.release(); h->bflagged.release(); h->bcount.release();
+  h->Mxb[0].release(); h->Mxb[1].release();
+  h->bflags.release();
+  for (auto& e : h->mxb_free)
+    if (e) cudaEventDestroy(e);
+  if (h->up_ev) cudaEventDestroy(h->up_ev);
   for (int s = 0; s < 2; ++s) {
     if (h->stage[s]) cudaFreeHost(h->stage[s]);
     if (h->stage_ev[s]) cudaEventDestroy(h->stage_ev[s]);
@@ -532,6 +550,10 @@ wmd_status wmd_set_option(wmd_handle* h, int32_t option, int64_t value) {
     case WMD_OPT_BUILD:
       if (value != WMD_BUILD_TENSOR_CORE && value != WMD_BUILD_DIRECT) return fail(h, WMD_ERR_INVALID_ARGUMENT, "bad build kernel");
       h->opt_build = value;
+      return WMD_OK;
+    case WMD_OPT_BATCH:
+      if (value < 0 || value > 64) return fail(h, WMD_ERR_INVALID_ARGUMENT, "batch size outside [0, 64]");
+      h->opt_batch = value;
       return WMD_OK;
     case WMD_OPT_LAYOUT_DOC_NNZ:
       if (value < 0) return fail(h, WMD_ERR_INVALID_ARGUMENT, "negative layout document length");
@@ -692,9 +714,19 @@ wmd_status record_solve(wmd_handle* h, const float* d_r, int32_t v_r, float lamb
       CK(h, cudaEventRecord(h->fork_ev, st));
       for (int i = 0; i < ring.n; ++i) CK(h, cudaStreamWaitEvent(h->lanes[i], h->fork_ev, 0));
     }
-    wmd::launch_sinkhorn_fused(h->sdoc.p, h->ent.p, N, h->len_prefix.data(),
-                               h->max_doc_nnz, h->Mx.p, ld, v_r, d_r, lambda, iters, tol, h->iters_doc.p,
-                               dist, h->flags.p, h->flagged.p, h->counters.p, st, &ring);
+    wmd::QuerySet qs{};
+    qs.Mx = h->Mx.p;
+    qs.rpad = d_r;
+    qs.v_r = v_r;
+    qs.nq = 1;
+    qs.N = N;
+    qs.dist = dist;
+    qs.flags = h->flags.p;
+    qs.iters_doc = h->iters_doc.p;
+    qs.flagged_list = h->flagged.p;
+    qs.flagged_count = h->counters.p;
+    wmd::launch_sinkhorn_fused(h->sdoc.p, h->ent.p, N, h->len_prefix.data(), h->max_doc_nnz, ld, qs, lambda,
+                               iters, tol, st, &ring);
     DBG_PHASE(h, st, "fused Sinkhorn kernels");
     for (int i = 0; i < ring.n; ++i) {
       CK(h, cudaEventRecord(h->join_ev[i], h->lanes[i]));
@@ -917,6 +949,167 @@ wmd_status enqueue_query(wmd_handle* h, const int32_t* d_sel, const float* d_r, 
   return WMD_OK;
 }
 
+// NEXT-2 (ii): a wmd_query_batch call is solved B queries per fused pass when every query takes
+// the one-warp kernel for every document (no stopping tolerance, no graph mode). *bmax: queries
+// per pass, WMD_OPT_BATCH or, by default, as many tables as fit in half the L2 (the pass is
+// document-major, so the B tables are gathered concurrently), at most 16.
+bool batch_eligible(wmd_handle* h, const std::vector<int32_t>& nrow, float lambda, int32_t* bmax) {
+  const int32_t nq = (int32_t)nrow.size();
+  if (nq < 2 || h->opt_batch == 1 || h->opt_graph || h->tol >= 0.0 || h->opt_path == WMD_PATH_PER_ITER ||
+      lambda < wmd::kFusedMinLambda)
+    return false;
+  int32_t ldmax = 0;
+  for (int32_t q = 0; q < nq; ++q) {
+    const int32_t ld = wmd::fused_ld(nrow[q], layout_doc_nnz(h), false);
+    if (ld <= 0 || ld > 64 || layout_doc_nnz(h) > wmd::warp_max_rows(ld)) return false;
+    ldmax = std::max(ldmax, ld);
+  }
+  const double table = (double)h->V * (ldmax + 4) * 4;
+  int32_t b = h->opt_batch >= 2 ? (int32_t)h->opt_batch : (int32_t)std::min(16.0, std::floor(64e6 / table));
+  *bmax = std::max(1, std::min(b, nq));
+  return *bmax >= 2;
+}
+
+// The batched passes: queries sorted (stably) by table width, then for each run of B queries of
+// one width: a build per query into B side-by-side tables, one fused launch per length bucket
+// for all B (each document's entries read once), then each query's re-runs of flagged
+// documents (FP32 re-anchoring, FP64) as in a single query. Results equal single queries bit
+// for bit (the per-(document, query) arithmetic is the same). svr / smap: pinned staging for
+// the widths and the order (nq entries each).
+wmd_status enqueue_batched(wmd_handle* h, const std::vector<int32_t>& nrow, int32_t* svr, int32_t* smap,
+                           int32_t bmax, float lambda, int32_t iters, float* dist) {
+  const int32_t nq = (int32_t)nrow.size();
+  const int64_t N = h->N, V = h->V;
+  cudaStream_t st = h->stream;
+  std::vector<int32_t> ld(nq);
+  for (int32_t q = 0; q < nq; ++q) ld[q] = wmd::fused_ld(nrow[q], layout_doc_nnz(h), false);
+  std::vector<int32_t> order(nq);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return ld[x] < ld[y]; });
+  for (int32_t q = 0; q < nq; ++q) { svr[q] = nrow[q]; smap[q] = order[q]; }
+  CK(h, h->bvr.ensure(nq));
+  CK(h, h->bqmap.ensure(nq));
+  CK(h, cudaMemcpyAsync(h->bvr.p, svr, nq * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  CK(h, cudaMemcpyAsync(h->bqmap.p, smap, nq * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  int32_t ldmax = 0;
+  for (int32_t q = 0; q < nq; ++q) ldmax = std::max(ldmax, ld[q]);
+  const int64_t stride = V * (ldmax + 4) + 128;
+  CK(h, h->Mxb[0].ensure((size_t)bmax * stride));
+  CK(h, h->Mxb[1].ensure((size_t)bmax * stride));
+  // builds on the build stream, after the uploads; pass k's builds go to Mxb[k & 1] once pass
+  // k - 2 (the last user of that buffer) is done, so they overlap the solve of pass k - 1
+  CK(h, cudaEventRecord(h->up_ev, st));
+  CK(h, cudaStreamWaitEvent(h->bstream, h->up_ev, 0));
+  CK(h, h->bflags.ensure((size_t)bmax * N));
+  CK(h, h->bflagged.ensure((size_t)bmax * N));
+  CK(h, h->bcount.ensure(bmax));
+  wmd::launch_fill_i32(h->iters_doc.p, N, iters, st);   // fixed iterations for every document
+  int64_t launches = 1;
+  const int32_t last = nq - 1;                          // flags / counts kept for the introspection calls
+  int pass = 0;
+  for (int32_t c0 = 0; c0 < nq; ++pass) {
+    int32_t c1 = c0;
+    while (c1 < nq && c1 - c0 < bmax && ld[order[c1]] == ld[order[c0]]) ++c1;
+    const int32_t B = c1 - c0, w = ld[order[c0]];
+    float* const mxb = h->Mxb[pass & 1].p;
+    PhaseEvents* pe = new_phase_events(h);
+    if (pass >= 2) CK(h, cudaStreamWaitEvent(h->bstream, h->mxb_free[pass & 1], 0));
+    if (pe) CK(h, cudaEventRecord(pe->ev[0], h->bstream));
+    for (int32_t q = 0; q < B; ++q) {
+      const int32_t g = order[c0 + q];
+      wmd::launch_build_ktilde(h->E.p, 0, V, h->dp, h->bsel.p + (size_t)g * WMD_MAX_VR, nrow[g], w, lambda,
+                               nullptr, mxb + q * stride, h->opt_build == WMD_BUILD_TENSOR_CORE, h->bstream);
+    }
+    launches += B;
+    DBG_PHASE(h, h->bstream, "batched distance builds");
+    CK(h, cudaEventRecord(h->built_ev, h->bstream));
+    CK(h, cudaStreamWaitEvent(st, h->built_ev, 0));
+    // phase timing: the solve starts here (build_ms then includes any wait for the previous solve)
+    if (pe) CK(h, cudaEventRecord(pe->ev[1], st));
+    CK(h, cudaMemsetAsync(h->bflags.p, 0, (size_t)B * N, st));
+    CK(h, cudaMemsetAsync(h->bcount.p, 0, B * sizeof(int32_t), st));
+    wmd::QuerySet qs{};
+    qs.Mx = mxb;
+    qs.mx_stride = stride;
+    qs.rpad = h->brpad.p;
+    qs.qmap = h->bqmap.p + c0;
+    qs.vr = h->bvr.p;
+    qs.nq = B;
+    qs.N = N;
+    qs.dist = dist;
+    qs.flags = h->bflags.p;
+    qs.iters_doc = nullptr;
+    qs.flagged_list = h->bflagged.p;
+    qs.flagged_count = h->bcount.p;
+    const int nb = wmd::fused_launch_count(h->len_prefix.data(), h->max_doc_nnz, N, w);
+    wmd::StreamRing ring;
+    if (nb > 1) {
+      ring.s = h->lanes;
+      ring.n = std::min(nb, (int)wmd_handle::kLanes);
+      CK(h, cudaEventRecord(h->fork_ev, st));
+      for (int i = 0; i < ring.n; ++i) CK(h, cudaStreamWaitEvent(h->lanes[i], h->fork_ev, 0));
+    }
+    wmd::launch_sinkhorn_fused(h->sdoc.p, h->ent.p, N, h->len_prefix.data(), h->max_doc_nnz, w, qs, lambda, iters,
+                               -1.f, st, &ring);
+    DBG_PHASE(h, st, "batched fused Sinkhorn kernels");
+    for (int i = 0; i < ring.n; ++i) {
+      CK(h, cudaEventRecord(h->join_ev[i], h->lanes[i]));
+      CK(h, cudaStreamWaitEvent(st, h->join_ev[i], 0));
+    }
+    launches += nb;
+    h->st.iter_launches += nb;
+    if (pe) { CK(h, cudaEventRecord(pe->ev[2], st)); CK(h, cudaEventRecord(pe->ev[3], st)); }
+    for (int32_t q = 0; q < B && h->opt_fallback; ++q) {
+      const int32_t g = order[c0 + q];
+      const float* mxq = mxb + q * stride;
+      const float* rq = h->brpad.p + (size_t)g * WMD_MAX_VR;
+      float* dq = dist + (size_t)g * N;
+      uint8_t* fq = h->bflags.p + (size_t)q * N;
+      const int32_t* fl = h->bflagged.p + (size_t)q * N;
+      int32_t* fc = h->bcount.p + q;
+      if (wmd::cta_rerun_supported(w)) {
+        CK(h, cudaMemsetAsync(h->counters.p + 4, 0, sizeof(int32_t), st));
+        wmd::launch_cta_rerun(fl, fc, h->doc_ptr.p, h->ent.p, mxq, w, nrow[g], rq, lambda, iters, nullptr, dq, fq,
+                              h->flagged2.p, h->counters.p + 4, st);
+        ++launches;
+        fl = h->flagged2.p;
+        fc = h->counters.p + 4;
+      }
+      wmd::launch_fallback_fp64(mxq, w, rq, nrow[g], (double)lambda, iters, -1.f, nullptr, h->doc_ptr.p, h->ent.p,
+                                fl, fc, h->fb_scratch.p, h->max_doc_nnz, dq, fq, h->counters.p + 1,
+                                h->counters.p + 2, st);
+      ++launches;
+    }
+    DBG_PHASE(h, st, "batched re-runs");
+    CK(h, cudaEventRecord(h->mxb_free[pass & 1], st));
+    if (pe) {
+      CK(h, cudaEventRecord(pe->ev[4], st));
+      pe->complete = true;
+    }
+    // the last query's flags and flagged count (wmd_read_flags / wmd_sync report the last query)
+    for (int32_t q = 0; q < B; ++q)
+      if (order[c0 + q] == last) {
+        CK(h, cudaMemcpyAsync(h->flags.p, h->bflags.p + (size_t)q * N, N, cudaMemcpyDeviceToDevice, st));
+        CK(h, cudaMemcpyAsync(h->counters.p, h->bcount.p + q, sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+      }
+    c0 = c1;
+  }
+  CK(h, cudaGetLastError());
+  h->kt_valid = false;
+  h->u_valid = false;
+  h->path_used = WMD_PATH_FUSED;
+  h->v_r = nrow[last];
+  h->ld = ld[last];
+  h->last_sel = h->bsel.p + (size_t)last * WMD_MAX_VR;
+  h->last_r = h->brpad.p + (size_t)last * WMD_MAX_VR;
+  h->st.queries += nq;
+  h->st.kernel_launches += launches;
+  h->st.last_v_r = nrow[last];
+  h->st.last_ld = ld[last];
+  h->st.last_path = WMD_PATH_FUSED;
+  return WMD_OK;
+}
+
 wmd_status check_query_args(wmd_handle* h, const void* out_dist, float lambda, int32_t iters) {
   if (!h->has_targets) return fail(h, WMD_ERR_STATE, "query before wmd_set_targets");
   if (!out_dist || !(lambda > 0.f) || !std::isfinite(lambda) || iters < 0)
@@ -981,7 +1174,7 @@ wmd_status wmd_query_batch(wmd_handle* h, const int32_t* query_ids, const float*
   cudaStream_t st = h->stream;
   // validate and sort every query before any work is enqueued (all-or-nothing)
   CK(h, cudaEventSynchronize(h->batch_ev));  // the previous batch's upload has left the staging
-  const size_t need = (size_t)nq * WMD_MAX_VR * 8;
+  const size_t need = (size_t)nq * WMD_MAX_VR * 8 + (size_t)nq * 8;  // ids, weights, widths, order
   if (h->batch_stage_bytes < need) {
     if (h->batch_stage) cudaFreeHost(h->batch_stage);
     h->batch_stage = nullptr;
@@ -1011,10 +1204,24 @@ wmd_status wmd_query_batch(wmd_handle* h, const int32_t* query_ids, const float*
   CK(h, h->brpad.ensure((size_t)nq * WMD_MAX_VR));
   CK(h, cudaMemcpyAsync(h->bsel.p, ssel, (size_t)nq * WMD_MAX_VR * 4, cudaMemcpyHostToDevice, st));
   CK(h, cudaMemcpyAsync(h->brpad.p, sr, (size_t)nq * WMD_MAX_VR * 4, cudaMemcpyHostToDevice, st));
-  CK(h, cudaEventRecord(h->batch_ev, st));
   const bool dev_out = is_device_ptr(out_dist);
   if (!dev_out) CK(h, h->batch_dist.ensure((size_t)nq * h->N));
   float* dist = dev_out ? out_dist : h->batch_dist.p;
+  // NEXT-2 (ii): B queries per fused pass when every query takes the one-warp kernel
+  int32_t bmax = 0;
+  if (batch_eligible(h, nrow, lambda, &bmax)) {
+    int32_t* svr = (int32_t*)((char*)h->batch_stage + (size_t)nq * WMD_MAX_VR * 8);
+    int32_t* smap = svr + nq;
+    s = enqueue_batched(h, nrow, svr, smap, bmax, lambda, iters, dist);
+    CK(h, cudaEventRecord(h->batch_ev, st));
+    if (s != WMD_OK) return s;
+    if (!dev_out) {
+      CK(h, cudaMemcpyAsync(out_dist, dist, (size_t)nq * h->N * sizeof(float), cudaMemcpyDeviceToHost, st));
+      CK(h, cudaStreamSynchronize(st));
+    }
+    return WMD_OK;
+  }
+  CK(h, cudaEventRecord(h->batch_ev, st));
   // Build/solve overlap: when every query takes the fused path, query q's
   // table is built on the handle's build stream into one of two tables while query q-1 is
   // solved on the main stream (the build is latency-bound and leaves most of the GPU idle).

@@ -118,12 +118,34 @@ struct StreamRing {
   int k = 0;
   cudaStream_t next(cudaStream_t st) { return n ? s[k++ % n] : st; }
 };
+// The queries one fused launch solves (NEXT-2 (ii), "one tweet vs a day of tweets"):
+// nq queries against the same documents, each document's entries read once for all of them.
+// Query q (0 <= q < nq) has a caller index g = qmap ? qmap[q] : q and: table Mx + q * mx_stride,
+// weights rpad + g * WMD_MAX_VR (zero padded), width vr ? vr[g] : v_r, distances dist + g * N;
+// its flags (flags + q * N), iteration counts (iters_doc + q * N) and flagged documents
+// (flagged_list + q * N, count flagged_count[q]) are batch-local. nq = 1, qmap = vr = nullptr is
+// a single query (wmd_query).
+struct QuerySet {
+  const float* Mx;
+  int64_t mx_stride;
+  const float* rpad;
+  const int32_t* qmap;     // device, nq entries, or nullptr
+  const int32_t* vr;       // device, indexed by g, or nullptr (every query has width v_r)
+  int32_t v_r;
+  int32_t nq;
+  int64_t N;
+  float* dist;
+  uint8_t* flags;
+  int32_t* iters_doc;      // may be nullptr
+  int32_t* flagged_list;
+  int32_t* flagged_count;
+};
+
 // sdoc[p] = {document id, first nonzero, length, 0} of the p-th document in length order.
+// qs.nq > 1 needs every document within the one-warp kernel's rows (warp_max_rows(ld)).
 void launch_sinkhorn_fused(const int4* sdoc, const Entry* ent, int64_t N,
-                           const int64_t* len_prefix, int64_t max_len, const float* Mx, int ld,
-                           int v_r, const float* rpad, float lambda, int iters, float tol,
-                           int32_t* iters_doc, float* dist, uint8_t* flags, int32_t* flagged_list,
-                           int32_t* flagged_count, cudaStream_t st, StreamRing* ring = nullptr);
+                           const int64_t* len_prefix, int64_t max_len, int ld, const QuerySet& qs,
+                           float lambda, int iters, float tol, cudaStream_t st, StreamRing* ring = nullptr);
 int fused_launch_count(const int64_t* len_prefix, int64_t max_len, int64_t N, int ld);
 
 // --- NEXT-1, long documents: one CTA of ceil(n/32) warps per document (wmd_fused_cta.cu) -----

@@ -37,6 +37,7 @@ WMD_ERR_CUDA = 10
 WMD_PATH_AUTO, WMD_PATH_PER_ITER, WMD_PATH_FUSED = 0, 1, 2
 WMD_OPT_PATH, WMD_OPT_TIMING, WMD_OPT_FALLBACK, WMD_OPT_GRAPH, WMD_OPT_BUILD = 1, 2, 3, 4, 5
 WMD_OPT_LAYOUT_DOC_NNZ = 6
+WMD_OPT_BATCH = 7
 WMD_BUILD_TENSOR_CORE, WMD_BUILD_DIRECT = 0, 1
 
 EXPORTED = (

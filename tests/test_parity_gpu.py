@@ -664,6 +664,42 @@ def test_query_batch_equals_single_queries_and_oracle(W):
         assert_parity(single[i], o, f"batch query {i}")
 
 
+@pytest.mark.parametrize("batch", [0, 1, 2, 3, 7, 64])
+def test_query_batch_passes_equal_single_queries(W, batch):
+    """NEXT-2 (ii): B queries per fused pass (WMD_OPT_BATCH; 0 = automatic, 1 = one at a time),
+    each document's entries read once for the B queries, queries regrouped by table width
+    (v_r 15..40 -> widths 16/24/32/40) and written back in caller order: bit for bit the single
+    queries' distances, the last query's flags, and a warp-flagged document (re-run by the
+    one-CTA kernel) inside a batch."""
+    wl = synth.make_workload("many", n_queries=11, N=2500)
+    qs = list(wl.queries)
+    # a 50-64-word document block against a 40-word query: the one-warp kernel flags some of
+    # them (the FP32 re-anchoring re-run then runs inside the batch)
+    cp, ri, va = _docs_with_lengths(wl.cfg.V, [60, 64, 52, 58] * 20, seed=77)
+    rng = np.random.Generator(np.random.PCG64(5))
+    qs.append(synth.make_query(rng, wl.cfg.V, 40, 1.07, 0.6))
+    for corpus in ((wl.col_ptr, wl.row_idx, wl.val), (cp, ri, va)):
+        N = corpus[0].shape[0] - 1
+        h = W.wmd_create(wl.E)
+        try:
+            W.wmd_set_targets(h, *corpus)
+            single = np.empty((len(qs), N), np.float32)
+            for i, (q, w) in enumerate(qs):
+                W.wmd_query(h, q, w, 10.0, 15, single[i])
+            f_single = W.wmd_read_flags(h, N)
+            W.wmd_set_option(h, W.WMD_OPT_BATCH, batch)
+            out = np.empty((len(qs), N), np.float32)
+            W.wmd_query_batch(h, qs, 10.0, 15, out)
+            W.wmd_sync(h)
+            f_batch = W.wmd_read_flags(h, N)
+            sel, r = W.wmd_get_query_rows(h, qs[-1][0].shape[0])
+        finally:
+            W.wmd_destroy(h)
+        assert np.array_equal(out, single)
+        assert np.array_equal(f_batch, f_single)
+        assert np.array_equal(sel, qs[-1][0])
+
+
 def test_query_batch_validates_all_before_enqueueing(W):
     wl = synth.make_workload("tiny", n_queries=3)
     qs = list(wl.queries)
