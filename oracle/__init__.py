@@ -26,12 +26,17 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "wmd_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
+# tools/oracle_mutation_check.py points this at a deliberately broken build of the same source
+# to show the pins catch it; nothing else sets it
+_LIB = os.environ.get("WMD_ORACLE_LIB_OVERRIDE") or _LIB
 
 _lib = None
 
 
 def build(force: bool = False) -> str:
     """Compile the oracle (gcc -O2, no fast-math, no OpenMP/BLAS)."""
+    if os.environ.get("WMD_ORACLE_LIB_OVERRIDE"):
+        return _LIB
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-fno-fast-math",
                                "-ffp-contract=off", "-o", _LIB, _SRC, "-lm"])

@@ -213,6 +213,34 @@ def test_P2_column_marginal_exact_and_P3_row_marginal_converges():
     assert row < 1e-9 and st["iters_run"] < 100000
 
 
+def test_half_step_identities_at_every_iteration():
+    """The non-converged iterates, pinned at every t (Eq. 1; Alg. 1 l.3-6):
+    with u_t = 1/x_t and v_t = c / (K^T u_t) (the final u and v of a run of t updates), the
+    plan diag(u_t) K diag(v_{t-1}) has row sums r (u_t = r / (K v_{t-1}), the x-update) and
+    diag(u_t) K diag(v_t) has column sums c (the v-update), for t = 1..6; and t = 0 starts
+    from x_0 = 1/v_r. K = exp(-lambda M) from the oracle's M, which P11 pins
+    to scipy's cdist; a dropped 1/r, a wrong x_0 or a transposed K breaks one of these."""
+    rng = np.random.default_rng(31)
+    E, cp, ri, va = _rand_instance(rng, 50, 5, 9, 0.12, lo=2)
+    q, w = _rand_query(rng, 50, 6)
+    lam = 0.7
+    sel, r = oracle.select_nonzero(50, q, w)
+    K = np.exp(-lam * oracle.euclidean_rows(E, sel))          # v_r x V
+    states = []
+    for t in range(0, 7):
+        _, st = oracle.sinkhorn_wmd(E, cp, ri, va, q, w, lam, t, return_state=True)
+        states.append(st)
+    assert np.allclose(states[0]["u"], sel.shape[0])          # u_0 = 1 / x_0 = v_r
+    for t in range(1, 7):
+        u_t, v_prev, v_t = states[t]["u"], states[t - 1]["v"], states[t]["v"]
+        for j in range(cp.shape[0] - 1):
+            ks = ri[cp[j]:cp[j + 1]]
+            rows = u_t[j] * (K[:, ks] @ v_prev[cp[j]:cp[j + 1]])
+            np.testing.assert_allclose(rows, r, rtol=1e-12)
+            cols = v_t[cp[j]:cp[j + 1]] * (u_t[j] @ K[:, ks])
+            np.testing.assert_allclose(cols, va[cp[j]:cp[j + 1]].astype(np.float64), rtol=1e-12)
+
+
 # ---------------------------------------------------------------- 2x2 closed form at convergence
 
 def test_2x2_converged_closed_form():
