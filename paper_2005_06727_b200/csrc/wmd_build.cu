@@ -10,12 +10,13 @@
 //                                                   runs)
 // E is stored with rows padded to dp (a multiple of 32) floats of zeros, which add nothing.
 //
-// Mapping: a block owns 256 vocabulary words x 32 query rows (more rows: further passes) and
-// streams d in chunks of 32 through shared memory with cp.async, double buffered. Thread
-// micro-tile: 4 query rows x 8 words = 32 independent accumulators; per d-quad a thread issues
-// 12 LDS.128 (4 warp-broadcast query quads, 8 conflict-free word quads) for 256 FP32
-// instructions (FADD + FFMA per (i, k, t) triple). Bound: FP32 issue, 2 instructions per
-// triple (PAPER.md:260 counts 3 flops), E read once from HBM.
+// Mapping: a block owns 256 vocabulary words x 8 RB query rows per pass (RB <= 6 chosen per
+// query so that the passes cover v_r with at most 7 padded rows each) and streams d in chunks of
+// 32 through shared memory with cp.async, double buffered. Thread micro-tile: RB query rows x 8
+// words = 8 RB independent accumulators; per d-quad a thread issues RB + 8 LDS.128 (RB
+// warp-broadcast query quads, 8 conflict-free word quads) for 64 RB FP32 instructions (FADD +
+// FFMA per (i, k, t) triple). Bound: FP32 issue, 2 instructions per triple (PAPER.md:260 counts
+// 3 flops), E read once per pass from HBM.
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
@@ -27,12 +28,12 @@ namespace wmd {
 namespace {
 
 constexpr int BW = 256;        // vocabulary words per block
-constexpr int BI = 32;         // query rows per pass
 constexpr int BD = 32;         // d chunk
 constexpr int BP = BD + 4;     // smem pitch of a staged row (floats)
 constexpr int kThreads = 256;
-constexpr int kStageFloats = BI * BP + BW * BP;  // one pipeline stage: query rows + words
-constexpr int kMsPitch = BI + 1;
+constexpr int kMaxRB = 6;      // query rows per thread and pass (8 RB rows per pass)
+
+template <int RB> constexpr int stage_floats() { return 8 * RB * BP + BW * BP; }  // query rows + words
 
 __device__ __forceinline__ void cp16(float* dst, const float* src, bool valid) {
   const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
@@ -40,11 +41,17 @@ __device__ __forceinline__ void cp16(float* dst, const float* src, bool valid) {
                : "memory");
 }
 
+// RB: query rows per thread and pass; a pass covers BI = 8 RB query rows (the host picks the
+// smallest RB whose passes cover v_r: v_r = 15 -> one pass of 16, 30 -> 32, 40 -> 40,
+// 100 -> three of 40), so a pass wastes at most 7 padded rows.
+template <int RB>
 __global__ void __launch_bounds__(kThreads, 2) build_mx_kernel(
     const float* __restrict__ E, int64_t row0, int64_t V, int dp, const int32_t* __restrict__ sel,
     int v_r, int ld, float lambda, float* __restrict__ Kt, float* __restrict__ Mx) {
-  extern __shared__ __align__(16) float smem[];
-  float* stage[2] = {smem, smem + kStageFloats};
+  constexpr int BI = 8 * RB;
+  constexpr int STAGE = stage_floats<RB>();
+  constexpr int MSP = BI + 1;              // pitch of the M tile of a pass in shared memory
+  extern __shared__ __align__(16) float smem[];  // two pipeline stages of STAGE floats
   __shared__ float cmin[BW];
   const int tid = threadIdx.x, tw = tid & 31, ti = tid >> 5;
   const int64_t k0 = row0 + (int64_t)blockIdx.x * BW;  // rows [row0, V) of this launch
@@ -53,15 +60,15 @@ __global__ void __launch_bounds__(kThreads, 2) build_mx_kernel(
   for (int w = tid; w < BW; w += kThreads) cmin[w] = FLT_MAX;
 
   for (int i0 = 0; i0 < v_r; i0 += BI) {
-    // stage one d chunk: 32 query rows (one 16 B copy per thread) + 256 words (eight per thread)
+    // stage one d chunk: BI query rows + 256 words, one 16 B copy per (row, 4 floats)
     auto issue = [&](int c, float* buf) {
-      const int t4 = tid & 7;
-      {
-        const int r = tid >> 3;                       // 0..31
+      for (int x = tid; x < BI * 8; x += kThreads) {
+        const int r = x >> 3, t4 = x & 7;
         const bool ok = i0 + r < v_r;
         const int64_t row = ok ? sel[i0 + r] : 0;
         cp16(buf + r * BP + 4 * t4, E + row * dp + c * BD + 4 * t4, ok);
       }
+      const int t4 = tid & 7;
 #pragma unroll
       for (int q = 0; q < BW / 32; ++q) {
         const int w = (tid >> 3) + 32 * q;            // 0..255
@@ -70,31 +77,31 @@ __global__ void __launch_bounds__(kThreads, 2) build_mx_kernel(
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    float acc[4][8];
+    float acc[RB][8];
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
+    for (int r = 0; r < RB; ++r)
 #pragma unroll
       for (int s = 0; s < 8; ++s) acc[r][s] = 0.f;
-    issue(0, stage[0]);
+    issue(0, smem);
     for (int c = 0; c < nchunk; ++c) {
       if (c + 1 < nchunk) {
-        issue(c + 1, stage[(c + 1) & 1]);
+        issue(c + 1, smem + ((c + 1) & 1) * STAGE);
         asm volatile("cp.async.wait_group 1;" ::: "memory");
       } else {
         asm volatile("cp.async.wait_group 0;" ::: "memory");
       }
       __syncthreads();
-      const float* Qs = stage[c & 1];
+      const float* Qs = smem + (c & 1) * STAGE;
       const float* Es = Qs + BI * BP;
 #pragma unroll 2
       for (int t = 0; t < BD; t += 4) {
-        float4 q[4], e[8];
+        float4 q[RB], e[8];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) q[r] = *reinterpret_cast<const float4*>(Qs + (ti + 8 * r) * BP + t);
+        for (int r = 0; r < RB; ++r) q[r] = *reinterpret_cast<const float4*>(Qs + (ti + 8 * r) * BP + t);
 #pragma unroll
         for (int s = 0; s < 8; ++s) e[s] = *reinterpret_cast<const float4*>(Es + (tw + 32 * s) * BP + t);
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
+        for (int r = 0; r < RB; ++r)
 #pragma unroll
           for (int s = 0; s < 8; ++s) {
             float df;
@@ -107,26 +114,32 @@ __global__ void __launch_bounds__(kThreads, 2) build_mx_kernel(
       __syncthreads();  // the stage is refilled by the next iteration's issue
     }
     // epilogue of this pass: M tile through shared memory (the staging buffers are idle)
-    float* Ms = smem;  // [BW][kMsPitch]
+    float* Ms = smem;  // [BW][MSP]
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
+    for (int r = 0; r < RB; ++r)
 #pragma unroll
-      for (int s = 0; s < 8; ++s) Ms[(tw + 32 * s) * kMsPitch + ti + 8 * r] = sqrtf(acc[r][s]);
+      for (int s = 0; s < 8; ++s) Ms[(tw + 32 * s) * MSP + ti + 8 * r] = sqrtf(acc[r][s]);
     __syncthreads();
-    // warp per word: lane i owns query row i0 + i (coalesced row writes)
+    // warp per word: lane l owns query rows i0 + l and i0 + 32 + l (coalesced row writes)
     const int warp = tid >> 5, lane = tid & 31;
     const bool last = i0 + BI >= v_r;
     for (int w = warp; w < BW; w += kThreads / 32) {
       const int64_t k = k0 + w;
       if (k >= V) break;
-      const int i = i0 + lane;
-      const float m = Ms[w * kMsPitch + lane];
-      float mn = i < v_r ? m : FLT_MAX;
+      float mn = FLT_MAX;
+#pragma unroll
+      for (int h = 0; h < (BI + 31) / 32; ++h) {
+        const int x = 32 * h + lane;
+        if (x < BI && i0 + x < v_r) {
+          const float m = Ms[w * MSP + x];
+          mn = fminf(mn, m);
+          Mx[k * ldx + i0 + x] = m;
+        }
+      }
 #pragma unroll
       for (int off = 16; off; off >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, off));
       mn = fminf(mn, cmin[w]);
       __syncwarp();
-      if (i < v_r) Mx[k * ldx + i] = m;
       if (!last) {
         if (lane == 0) cmin[w] = mn;
         continue;
@@ -136,7 +149,7 @@ __global__ void __launch_bounds__(kThreads, 2) build_mx_kernel(
       if (Kt) {
         for (int x = lane; x < ld; x += 32) {
           float kt = 0.f;
-          if (x < v_r) kt = expf(-lambda * ((x >= i0 ? Ms[w * kMsPitch + x - i0] : Mx[k * ldx + x]) - mn));
+          if (x < v_r) kt = expf(-lambda * ((x >= i0 ? Ms[w * MSP + x - i0] : Mx[k * ldx + x]) - mn));
           Kt[k * ld + x] = kt;
         }
       }
@@ -453,12 +466,27 @@ void launch_build_ktilde(const float* E, int64_t row0, int64_t row1, int dp, con
                          int ld, float lambda, float* Kt, float* Mx, bool use_tc, cudaStream_t st) {
   if (row1 <= row0) return;
   if (!use_tc) {
-    constexpr size_t smem = sizeof(float) * 2 * kStageFloats;
-    static_assert(BW * kMsPitch <= 2 * kStageFloats, "M tile must fit in the staging buffers");
-    static PerDevice attr;
-    attr.get([&] { return (int)cudaFuncSetAttribute(build_mx_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
+    // fewest passes of at most 8 kMaxRB query rows, then the smallest rows-per-thread covering them
+    const int passes = (v_r + 8 * kMaxRB - 1) / (8 * kMaxRB);
+    const int rb = ((v_r + passes - 1) / passes + 7) / 8;
     const int64_t grid = (row1 - row0 + BW - 1) / BW;
-    build_mx_kernel<<<(unsigned)grid, kThreads, smem, st>>>(E, row0, row1, dp, sel, v_r, ld, lambda, Kt, Mx);
+#define SIMT_(RB)                                                                                        \
+  {                                                                                                      \
+    constexpr size_t smem = sizeof(float) * 2 * stage_floats<RB>();                                       \
+    static_assert(BW * (8 * RB + 1) <= 2 * stage_floats<RB>(), "M tile must fit in the staging buffers"); \
+    static PerDevice attr;                                                                               \
+    attr.get([&] { return (int)cudaFuncSetAttribute(build_mx_kernel<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); }); \
+    build_mx_kernel<RB><<<(unsigned)grid, kThreads, smem, st>>>(E, row0, row1, dp, sel, v_r, ld, lambda, Kt, Mx); \
+  }
+    switch (rb) {
+      case 1: SIMT_(1) break;
+      case 2: SIMT_(2) break;
+      case 3: SIMT_(3) break;
+      case 4: SIMT_(4) break;
+      case 5: SIMT_(5) break;
+      default: SIMT_(6) break;
+    }
+#undef SIMT_
     return;
   }
   const unsigned grid = (unsigned)((row1 - row0 + TC_M - 1) / TC_M);

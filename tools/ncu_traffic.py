@@ -17,12 +17,14 @@ UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e
 def main():
     rep, cfg, sub = sys.argv[1], sys.argv[2], sys.argv[3]
     out = sys.argv[4] if len(sys.argv) > 4 else os.path.join(
-        os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "r01_traffic.json")
+        os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "r02_traffic.json")
     txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     h, units = rows[0], rows[1]
     ik, ir, iw, it = (h.index(x) for x in ("Kernel Name", "dram__bytes_read.sum", "dram__bytes_write.sum",
                                           "gpu__time_duration.sum"))
+    ih = h.index("lts__t_sector_hit_rate.pct") if "lts__t_sector_hit_rate.pct" in h else None
+    hits = []
     launches, rd, wr, ms = [], 0.0, 0.0, 0.0
     for r in rows[2:]:
         if sub not in r[ik]:
@@ -33,9 +35,12 @@ def main():
         launches.append({"kernel": r[ik].split("(")[0], "dram_read_bytes": b_r, "dram_write_bytes": b_w,
                          "duration_ms_under_ncu": t})
         rd, wr, ms = rd + b_r, wr + b_w, ms + t
+        if ih is not None:
+            hits.append((float(r[ih]), t))
     data = json.load(open(out)) if os.path.exists(out) else {}
     data[cfg] = {"kernel_match": sub, "launches": launches, "dram_bytes_per_query": rd + wr,
-                 "dram_read_bytes": rd, "dram_write_bytes": wr, "source": os.path.basename(rep)}
+                 "dram_read_bytes": rd, "dram_write_bytes": wr, "source": os.path.basename(rep),
+                 "l2_hit_rate_pct": (sum(h * t for h, t in hits) / sum(t for _, t in hits)) if hits else None}
     with open(out, "w") as f:
         json.dump(data, f, indent=1)
     print(cfg, len(launches), "launches", f"{(rd + wr) / 1e6:.1f} MB")
