@@ -27,13 +27,14 @@
 namespace wmd {
 namespace {
 
-constexpr int BW = 256;        // vocabulary words per block
+constexpr int BW = 256;        // vocabulary words per block (tensor-core variant, SIMT default)
 constexpr int BD = 32;         // d chunk
 constexpr int BP = BD + 4;     // smem pitch of a staged row (floats)
 constexpr int kThreads = 256;
 constexpr int kMaxRB = 6;      // query rows per thread and pass (8 RB rows per pass)
 
-template <int RB> constexpr int stage_floats() { return 8 * RB * BP + BW * BP; }  // query rows + words
+// query rows + words of one pipeline stage (NWT words per thread: 32 NWT words per block)
+template <int RB, int NWT> constexpr int stage_floats() { return 8 * RB * BP + 32 * NWT * BP; }
 
 __device__ __forceinline__ void cp16(float* dst, const float* src, bool valid) {
   const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
@@ -44,23 +45,26 @@ __device__ __forceinline__ void cp16(float* dst, const float* src, bool valid) {
 // RB: query rows per thread and pass; a pass covers BI = 8 RB query rows (the host picks the
 // smallest RB whose passes cover v_r: v_r = 15 -> one pass of 16, 30 -> 32, 40 -> 40,
 // 100 -> three of 40), so a pass wastes at most 7 padded rows.
-template <int RB>
-__global__ void __launch_bounds__(kThreads, 2) build_mx_kernel(
+// NWT: words per thread (8: 256 words per block; 4: 128, for small vocabularies, where 256-word
+// blocks leave the last wave mostly empty).
+template <int RB, int NWT>
+__global__ void __launch_bounds__(kThreads, NWT == 4 ? 3 : 2) build_mx_kernel(
     const float* __restrict__ E, int64_t row0, int64_t V, int dp, const int32_t* __restrict__ sel,
     int v_r, int ld, float lambda, float* __restrict__ Kt, float* __restrict__ Mx) {
   constexpr int BI = 8 * RB;
-  constexpr int STAGE = stage_floats<RB>();
+  constexpr int BWW = 32 * NWT;            // words per block
+  constexpr int STAGE = stage_floats<RB, NWT>();
   constexpr int MSP = BI + 1;              // pitch of the M tile of a pass in shared memory
   extern __shared__ __align__(16) float smem[];  // two pipeline stages of STAGE floats
-  __shared__ float cmin[BW];
+  __shared__ float cmin[BWW];
   const int tid = threadIdx.x, tw = tid & 31, ti = tid >> 5;
-  const int64_t k0 = row0 + (int64_t)blockIdx.x * BW;  // rows [row0, V) of this launch
+  const int64_t k0 = row0 + (int64_t)blockIdx.x * BWW;  // rows [row0, V) of this launch
   const int nchunk = dp / BD;
   const int ldx = ld + 4;
-  for (int w = tid; w < BW; w += kThreads) cmin[w] = FLT_MAX;
+  for (int w = tid; w < BWW; w += kThreads) cmin[w] = FLT_MAX;
 
   for (int i0 = 0; i0 < v_r; i0 += BI) {
-    // stage one d chunk: BI query rows + 256 words, one 16 B copy per (row, 4 floats)
+    // stage one d chunk: BI query rows + BWW words, one 16 B copy per (row, 4 floats)
     auto issue = [&](int c, float* buf) {
       for (int x = tid; x < BI * 8; x += kThreads) {
         const int r = x >> 3, t4 = x & 7;
@@ -70,18 +74,18 @@ __global__ void __launch_bounds__(kThreads, 2) build_mx_kernel(
       }
       const int t4 = tid & 7;
 #pragma unroll
-      for (int q = 0; q < BW / 32; ++q) {
-        const int w = (tid >> 3) + 32 * q;            // 0..255
+      for (int q = 0; q < BWW / 32; ++q) {
+        const int w = (tid >> 3) + 32 * q;            // 0..BWW-1
         const bool ok = k0 + w < V;
         cp16(buf + BI * BP + w * BP + 4 * t4, E + (ok ? k0 + w : 0) * dp + c * BD + 4 * t4, ok);
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    float acc[RB][8];
+    float acc[RB][NWT];
 #pragma unroll
     for (int r = 0; r < RB; ++r)
 #pragma unroll
-      for (int s = 0; s < 8; ++s) acc[r][s] = 0.f;
+      for (int s = 0; s < NWT; ++s) acc[r][s] = 0.f;
     issue(0, smem);
     for (int c = 0; c < nchunk; ++c) {
       if (c + 1 < nchunk) {
@@ -95,15 +99,15 @@ __global__ void __launch_bounds__(kThreads, 2) build_mx_kernel(
       const float* Es = Qs + BI * BP;
 #pragma unroll 2
       for (int t = 0; t < BD; t += 4) {
-        float4 q[RB], e[8];
+        float4 q[RB], e[NWT];
 #pragma unroll
         for (int r = 0; r < RB; ++r) q[r] = *reinterpret_cast<const float4*>(Qs + (ti + 8 * r) * BP + t);
 #pragma unroll
-        for (int s = 0; s < 8; ++s) e[s] = *reinterpret_cast<const float4*>(Es + (tw + 32 * s) * BP + t);
+        for (int s = 0; s < NWT; ++s) e[s] = *reinterpret_cast<const float4*>(Es + (tw + 32 * s) * BP + t);
 #pragma unroll
         for (int r = 0; r < RB; ++r)
 #pragma unroll
-          for (int s = 0; s < 8; ++s) {
+          for (int s = 0; s < NWT; ++s) {
             float df;
             df = q[r].x - e[s].x; acc[r][s] = fmaf(df, df, acc[r][s]);
             df = q[r].y - e[s].y; acc[r][s] = fmaf(df, df, acc[r][s]);
@@ -114,16 +118,16 @@ __global__ void __launch_bounds__(kThreads, 2) build_mx_kernel(
       __syncthreads();  // the stage is refilled by the next iteration's issue
     }
     // epilogue of this pass: M tile through shared memory (the staging buffers are idle)
-    float* Ms = smem;  // [BW][MSP]
+    float* Ms = smem;  // [BWW][MSP]
 #pragma unroll
     for (int r = 0; r < RB; ++r)
 #pragma unroll
-      for (int s = 0; s < 8; ++s) Ms[(tw + 32 * s) * MSP + ti + 8 * r] = sqrtf(acc[r][s]);
+      for (int s = 0; s < NWT; ++s) Ms[(tw + 32 * s) * MSP + ti + 8 * r] = sqrtf(acc[r][s]);
     __syncthreads();
     // warp per word: lane l owns query rows i0 + l and i0 + 32 + l (coalesced row writes)
     const int warp = tid >> 5, lane = tid & 31;
     const bool last = i0 + BI >= v_r;
-    for (int w = warp; w < BW; w += kThreads / 32) {
+    for (int w = warp; w < BWW; w += kThreads / 32) {
       const int64_t k = k0 + w;
       if (k >= V) break;
       float mn = FLT_MAX;
@@ -469,15 +473,18 @@ void launch_build_ktilde(const float* E, int64_t row0, int64_t row1, int dp, con
     // fewest passes of at most 8 kMaxRB query rows, then the smallest rows-per-thread covering them
     const int passes = (v_r + 8 * kMaxRB - 1) / (8 * kMaxRB);
     const int rb = ((v_r + passes - 1) / passes + 7) / 8;
-    const int64_t grid = (row1 - row0 + BW - 1) / BW;
-#define SIMT_(RB)                                                                                        \
+    // 128-word blocks when 256-word blocks would fill fewer than ~4 waves of 2 blocks per SM
+    const bool small = (row1 - row0) < (int64_t)BW * device_sms() * 8;
+#define SIMT2_(RB, NWT)                                                                                  \
   {                                                                                                      \
-    constexpr size_t smem = sizeof(float) * 2 * stage_floats<RB>();                                       \
-    static_assert(BW * (8 * RB + 1) <= 2 * stage_floats<RB>(), "M tile must fit in the staging buffers"); \
+    constexpr size_t smem = sizeof(float) * 2 * stage_floats<RB, NWT>();                                  \
+    static_assert(32 * NWT * (8 * RB + 1) <= 2 * stage_floats<RB, NWT>(), "M tile must fit in the staging buffers"); \
     static PerDevice attr;                                                                               \
-    attr.get([&] { return (int)cudaFuncSetAttribute(build_mx_kernel<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); }); \
-    build_mx_kernel<RB><<<(unsigned)grid, kThreads, smem, st>>>(E, row0, row1, dp, sel, v_r, ld, lambda, Kt, Mx); \
+    attr.get([&] { return (int)cudaFuncSetAttribute(build_mx_kernel<RB, NWT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); }); \
+    const int64_t grid = (row1 - row0 + 32 * NWT - 1) / (32 * NWT);                                     \
+    build_mx_kernel<RB, NWT><<<(unsigned)grid, kThreads, smem, st>>>(E, row0, row1, dp, sel, v_r, ld, lambda, Kt, Mx); \
   }
+#define SIMT_(RB) if (small) SIMT2_(RB, 4) else SIMT2_(RB, 8)
     switch (rb) {
       case 1: SIMT_(1) break;
       case 2: SIMT_(2) break;
@@ -487,6 +494,7 @@ void launch_build_ktilde(const float* E, int64_t row0, int64_t row1, int dp, con
       default: SIMT_(6) break;
     }
 #undef SIMT_
+#undef SIMT2_
     return;
   }
   const unsigned grid = (unsigned)((row1 - row0 + TC_M - 1) / TC_M);
