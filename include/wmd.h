@@ -107,10 +107,18 @@ typedef enum {
  *  WMD_BUILD_TENSOR_CORE: M^2 = |e|^2 + |q|^2 - 2 e.q with e.q on the tcgen05 tensor cores in
  *    3xTF32, near pairs recomputed directly. Faster, but the expansion's absolute error
  *    ~eps (|e|^2 + |q|^2) reaches lambda*dM ~ 1e-2 on clustered embeddings of varied norm, where
- *    distances end up ~1e-4 off (R34); accurate on isotropic (N(0,1)-like) data. */
+ *    distances end up ~1e-4 off (R34); accurate on isotropic (N(0,1)-like) data.
+ *  WMD_BUILD_EXACT: the same expansion in exact integer arithmetic on the tcgen05 tensor cores
+ *    (kind::i8): at wmd_create E is rounded once to fixed point n = rint(E 2^F) with |n| <= 2^26
+ *    (F from max|E|: about one FP32 ulp of the largest coordinates) and split into byte limbs;
+ *    the limb products, their int64 combination and M^2 = (|n_k|^2 - n_k.n_q) + (|n_q|^2 - n_k.n_q)
+ *    are exact, so M_{i,sel_i} = 0 and there is no cancellation for any geometry. Needs
+ *    dp = d rounded up to 32 <= 1280 (wmd_set_option fails with WMD_ERR_INVALID_ARGUMENT
+ *    otherwise). Costs V * dp bytes of extra device memory per handle. */
 typedef enum {
   WMD_BUILD_TENSOR_CORE = 0,
-  WMD_BUILD_DIRECT = 1
+  WMD_BUILD_DIRECT = 1,
+  WMD_BUILD_EXACT = 2
 } wmd_build;
 
 typedef struct {

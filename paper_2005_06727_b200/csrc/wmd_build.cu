@@ -23,9 +23,14 @@
 #include <cstdint>
 
 #include "wmd_internal.h"
+#include "wmd_umma.cuh"
 
 namespace wmd {
 namespace {
+
+using umma::su32;
+using umma::mbar_wait;
+using umma::tmem_ld32;
 
 constexpr int BW = 256;        // vocabulary words per block (tensor-core variant, SIMT default)
 constexpr int BD = 32;         // d chunk
@@ -201,9 +206,6 @@ constexpr int TC_NS = WMD_TC_STAGES;  // raw-chunk ring stages
 constexpr int TC_LO = WMD_TC_LO;      // lo-part buffers = how many chunks back the MMA wait is
 constexpr float kNearFrac = 1.0f / 64.f;
 
-__device__ __forceinline__ uint32_t su32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
 // byte offset of element (r, k) (k < 32) in a K-major no-swizzle tile of R rows: core matrices
 // of 8 rows x 4 floats; SBO = 128 B between 8-row groups, LBO = R/8 * 128 B between K quads
 // Operand layouts (K-major). SWZ = 64 (default): SWIZZLE_64B with 16-float chunks (one 64-byte
@@ -220,48 +222,12 @@ __device__ __forceinline__ uint32_t km_off(int r, int k, int R) {
   else if constexpr (SWZ == 64) return (uint32_t)((r >> 3) * 512 + (r & 7) * 64 + ((((k >> 2) ^ (r >> 1)) & 3) << 4) + (k & 3) * 4);
   else return (uint32_t)((k >> 2) * (R / 8 * 128) + (r >> 3) * 128 + (r & 7) * 16 + (k & 3) * 4);
 }
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
-         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);  // version 1, no swizzle
-}
-// SWIZZLE_128B K-major: SBO = 1024 B between 8-row atoms, LBO unused (1), layout type 2
-__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
-  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
-         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
-}
-// SWIZZLE_64B K-major: SBO = 512 B between 8-row atoms, layout type 4
-__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
-  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(512 >> 4) << 32) |
-         ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
-}
 __device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n"
       ::"r"(tmem), "l"(da), "l"(db), "r"(idesc), "r"(acc));
 }
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
-                 "selp.b32 %0, 1, 0, P1;\n\t}\n" : "=r"(done) : "r"(bar), "r"(parity));
-  }
-}
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
-  uint32_t r[32];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int c = 0; c < 32; ++c) v[c] = __uint_as_float(r[c]);
-}
-
 template <int NP>
 __global__ void __launch_bounds__(128, NP <= 32 ? (WMD_TC_SWZ_BYTES == 64 ? 4 : 2) : (NP <= 64 && WMD_TC_SWZ_MAX >= 64 ? 2 : 1)) build_mx_tc_kernel(
     const float* __restrict__ E, int64_t row0, int64_t V, int dp, const int32_t* __restrict__ sel,
@@ -380,14 +346,14 @@ __global__ void __launch_bounds__(128, NP <= 32 ? (WMD_TC_SWZ_BYTES == 64 ? 4 : 
         for (int kk = 0; kk < TC_K; kk += 8) {
           uint64_t da, db;
           if constexpr (SWZ == 128) {
-            da = umma_desc_sw128(a + 4 * kk);
-            db = umma_desc_sw128(b + 4 * kk);
+            da = umma::desc_sw128(a + 4 * kk);
+            db = umma::desc_sw128(b + 4 * kk);
           } else if constexpr (SWZ == 64) {
-            da = umma_desc_sw64(a + 4 * kk);
-            db = umma_desc_sw64(b + 4 * kk);
+            da = umma::desc_sw64(a + 4 * kk);
+            db = umma::desc_sw64(b + 4 * kk);
           } else {
-            da = umma_desc(a + (kk >> 2) * (TC_M / 8 * 128), TC_M / 8 * 128, 128);
-            db = umma_desc(b + (kk >> 2) * (NP / 8 * 128), NP / 8 * 128, 128);
+            da = umma::desc(a + (kk >> 2) * (TC_M / 8 * 128), TC_M / 8 * 128, 128);
+            db = umma::desc(b + (kk >> 2) * (NP / 8 * 128), NP / 8 * 128, 128);
           }
           mma_tf32(tm, da, db, IDESC, (c | pass | kk) ? 1u : 0u);
         }

@@ -115,6 +115,7 @@ struct wmd_handle {
   cudaEvent_t built_ev = nullptr;
   // embeddings
   DevBuf<float> E;
+  wmd::ExactE ex;            // E in fixed-point limbs (exact tensor-core build)
   int64_t V = 0;
   int32_t d = 0, dp = 0;     // dp: padded row stride of E (multiple of 32)
   // targets
@@ -459,6 +460,9 @@ wmd_status wmd_create(const float* vocab_emb, int64_t V, int32_t d, int32_t devi
         cudaStreamSynchronize(h->stream) != cudaSuccess)
       return bail(WMD_ERR_CUDA);
   }
+  // fixed-point limb planes for the exact tensor-core build (unsupported shapes leave ex.ok false)
+  if (const int e = wmd::prepare_exact_e(h->E.p, V, dp, &h->ex, h->stream))
+    return bail(e == (int)cudaErrorMemoryAllocation ? WMD_ERR_OUT_OF_MEMORY : WMD_ERR_CUDA);
   if (h->sel.ensure(WMD_MAX_VR) != cudaSuccess || h->rpad.ensure(WMD_MAX_VR) != cudaSuccess ||
       h->counters.ensure(6) != cudaSuccess)
     return bail(WMD_ERR_OUT_OF_MEMORY);
@@ -512,6 +516,7 @@ void wmd_destroy(wmd_handle* h) {
     if (h->stage[s]) cudaFreeHost(h->stage[s]);
     if (h->stage_ev[s]) cudaEventDestroy(h->stage_ev[s]);
   }
+  wmd::free_exact_e(&h->ex);
   h->E.release(); h->doc_ptr.release(); h->order.release(); h->sdoc.release(); h->ent.release(); h->sel.release(); h->rpad.release();
   h->Kt.release(); h->Mx.release(); h->Mx2.release(); h->ua.release(); h->ub.release(); h->umask.release();
   h->dist_tmp.release(); h->flags.release(); h->flagged.release(); h->flagged2.release(); h->counters.release();
@@ -548,7 +553,10 @@ wmd_status wmd_set_option(wmd_handle* h, int32_t option, int64_t value) {
     case WMD_OPT_FALLBACK: h->opt_fallback = value != 0; return WMD_OK;
     case WMD_OPT_GRAPH: h->opt_graph = value != 0; return WMD_OK;
     case WMD_OPT_BUILD:
-      if (value != WMD_BUILD_TENSOR_CORE && value != WMD_BUILD_DIRECT) return fail(h, WMD_ERR_INVALID_ARGUMENT, "bad build kernel");
+      if (value != WMD_BUILD_TENSOR_CORE && value != WMD_BUILD_DIRECT && value != WMD_BUILD_EXACT)
+        return fail(h, WMD_ERR_INVALID_ARGUMENT, "bad build kernel");
+      if (value == WMD_BUILD_EXACT && !h->ex.ok)
+        return fail(h, WMD_ERR_INVALID_ARGUMENT, "exact build unavailable (dp=%d outside [32, 1280] or max|E| out of range)", h->dp);
       h->opt_build = value;
       return WMD_OK;
     case WMD_OPT_BATCH:
@@ -680,14 +688,23 @@ wmd_status prepare_query(wmd_handle* h, int32_t v_r, float lambda, int64_t table
   return WMD_OK;
 }
 
+// The distance build of the handle's WMD_OPT_BUILD kernel for rows [row0, row1).
+void build_rows(wmd_handle* h, const int32_t* d_sel, int32_t v_r, int32_t ld, float lambda, float* Kt, float* Mx,
+                int64_t row0, int64_t row1, cudaStream_t st) {
+  if (h->opt_build == WMD_BUILD_EXACT)
+    wmd::launch_build_exact(h->ex, row0, row1, d_sel, v_r, ld, lambda, Kt, Mx, st);
+  else
+    wmd::launch_build_ktilde(h->E.p, row0, row1, h->dp, d_sel, v_r, ld, lambda, Kt, Mx,
+                             h->opt_build == WMD_BUILD_TENSOR_CORE, st);
+}
+
 // a2 for vocabulary rows [row0, row1) (capturable stream work).
 wmd_status record_build(wmd_handle* h, const int32_t* d_sel, int32_t v_r, float lambda, int64_t row0,
                         int64_t row1, bool fused, int32_t ld, PhaseEvents* pe) {
   cudaStream_t st = h->stream;
   if (pe) CK(h, cudaEventRecord(pe->ev[0], st));
   // M (+ m), and K~ for the per-iteration path
-  wmd::launch_build_ktilde(h->E.p, row0, row1, h->dp, d_sel, v_r, ld, lambda, fused ? nullptr : h->Kt.p,
-                           h->Mx.p, h->opt_build == WMD_BUILD_TENSOR_CORE, st);
+  build_rows(h, d_sel, v_r, ld, lambda, fused ? nullptr : h->Kt.p, h->Mx.p, row0, row1, st);
   DBG_PHASE(h, st, "distance build");
   if (pe) CK(h, cudaEventRecord(pe->ev[1], st));
   CK(h, cudaGetLastError());
@@ -1017,8 +1034,8 @@ wmd_status enqueue_batched(wmd_handle* h, const std::vector<int32_t>& nrow, int3
     if (pe) CK(h, cudaEventRecord(pe->ev[0], h->bstream));
     for (int32_t q = 0; q < B; ++q) {
       const int32_t g = order[c0 + q];
-      wmd::launch_build_ktilde(h->E.p, 0, V, h->dp, h->bsel.p + (size_t)g * WMD_MAX_VR, nrow[g], w, lambda,
-                               nullptr, mxb + q * stride, h->opt_build == WMD_BUILD_TENSOR_CORE, h->bstream);
+      build_rows(h, h->bsel.p + (size_t)g * WMD_MAX_VR, nrow[g], w, lambda, nullptr, mxb + q * stride, 0, V,
+                 h->bstream);
     }
     launches += B;
     DBG_PHASE(h, h->bstream, "batched distance builds");

@@ -72,6 +72,29 @@ struct QueryDev {
 void launch_build_ktilde(const float* E, int64_t row0, int64_t row1, int dp, const int32_t* sel, int v_r,
                          int ld, float lambda, float* Kt, float* Mx, bool use_tc, cudaStream_t st);
 
+// Exact build (wmd_build_exact.cu): E in fixed point, n = rint(E 2^frac_bits), as four byte-limb
+// planes limbs[limb][dp/16][V][16 B] (chunk-major: the TMA boxes of 128 rows are contiguous) and
+// nn[k] = sum_t n_kt^2 (int64); tmap: the planes' 4-D TMA descriptor (a CUtensorMap).
+struct ExactE {
+  uint8_t* limbs = nullptr;
+  long long* nn = nullptr;
+  int64_t V = 0;
+  int dp = 0;
+  int frac_bits = 0;
+  float inv_scale = 1.f;  // 2^-frac_bits
+  bool ok = false;        // tables built (false: unsupported dp / range; the build is unavailable)
+  alignas(64) unsigned char tmap[128] = {};
+};
+bool exact_build_supported(int dp);
+int exact_frac_bits_limit(int dp);
+// (Re)builds *x from E (V x dp, device) on st; synchronises st once (max |E|). Returns a
+// cudaError_t value (0 also when the shape is unsupported: x->ok stays false).
+int prepare_exact_e(const float* E, int64_t V, int dp, ExactE* x, cudaStream_t st);
+void free_exact_e(ExactE* x);
+// Same contract as launch_build_ktilde (x.ok required).
+void launch_build_exact(const ExactE& x, int64_t row0, int64_t row1, const int32_t* sel, int v_r, int ld,
+                        float lambda, float* Kt, float* Mx, cudaStream_t st);
+
 // "While x changes" (NEXT-3): tol < 0 runs the fixed iteration count. Otherwise a
 // document stops after the first x-update with max_i |x_new/x - 1| <= tol (R31);
 // conv[j] marks it (per-iteration path), iters_doc[j] receives its number of x-updates.

@@ -38,7 +38,7 @@ WMD_PATH_AUTO, WMD_PATH_PER_ITER, WMD_PATH_FUSED = 0, 1, 2
 WMD_OPT_PATH, WMD_OPT_TIMING, WMD_OPT_FALLBACK, WMD_OPT_GRAPH, WMD_OPT_BUILD = 1, 2, 3, 4, 5
 WMD_OPT_LAYOUT_DOC_NNZ = 6
 WMD_OPT_BATCH = 7
-WMD_BUILD_TENSOR_CORE, WMD_BUILD_DIRECT = 0, 1
+WMD_BUILD_TENSOR_CORE, WMD_BUILD_DIRECT, WMD_BUILD_EXACT = 0, 1, 2
 
 EXPORTED = (
     "wmd_create", "wmd_set_stream", "wmd_set_option", "wmd_set_targets", "wmd_query",
