@@ -7,12 +7,16 @@
 // (B is the largest value for which every intermediate below fits in int64, given dp). The
 // rounding is the only approximation: |E_kt - n_kt 2^-F| <= 2^-(F+1), about one FP32 ulp of the
 // largest coordinates. Each n is split into four byte limbs, n = L0 + 2^8 L1 + 2^16 L2 + 2^24 L3
-// (L0..L2 unsigned, L3 = n >> 24 signed, |L3| <= 4), stored as four planes; nn_k = sum_t n_kt^2
-// exactly in int64.
+// (balanced base-256 digits L_a in [-128, 127], |L3| <= 4), stored as four planes;
+// nn_k = sum_t n_kt^2 exactly in int64.
 //
 // Per query row i (word sel_i) and vocabulary word k, the tensor cores compute the 16 limb
-// products  P_ab = sum_t L_a(n_k,t) L_b(n_sel_i,t)  (tcgen05.mma kind::i8, u8/s8 x u8/s8 -> s32)
-// accumulated by g = a + b into seven int32 TMEM accumulators A_g (|A_g| <= 4 dp 255^2 < 2^31),
+// products  P_ab = sum_t L_a(n_k,t) L_b(n_sel_i,t)  (tcgen05.mma kind::i8, s8 x s8 -> s32)
+// accumulated by g = a + b into seven int32 TMEM accumulators A_g (|A_g| <= 4 dp 128^2 < 2^31):
+// the B operand holds the four limbs of the 32 query rows side by side (N = 128, column
+// 32 b + i), and the MMA of vocabulary limb a writes TMEM columns from 32 a, so its column block
+// b lands on accumulator a + b: four N = 128 MMAs per K-step (the accumulators are zeroed by the
+// epilogue after it reads them),
 // and the epilogue forms, in int64,
 //     dot = sum_g A_g 2^(8g),   M_ik^2 2^(2F) = (nn_k - dot) + (nn_sel_i - dot)    (exact)
 //     M_ik = sqrt(float(M^2 2^(2F))) * 2^-F          (two roundings: M within ~1 ulp of the
@@ -21,6 +25,7 @@
 //
 // Block: 128 threads, 128 vocabulary rows (TMEM lanes, MMA M) x 32 query rows per pass (MMA N);
 // v_r > 32 runs ceil(v_r/32) passes over the same rows (the A tile is re-read, mostly from L2).
+// (16 MMAs of N = 32 per K-step measured tensor-pipe bound: 68 % busy at 2.9 TB/s.)
 // Operands (K-major, no swizzle, core matrices of 8 rows x 16 B): A = the vocabulary limbs,
 // one 3-D TMA box per 32-coordinate K-step (128 rows x 16 B x 2 chunks x 4 planes = 16 KB) into
 // a 4-stage mbarrier ring (expect-tx); B = the pass's 32 query rows, all K-steps resident in
@@ -49,18 +54,17 @@ constexpr int XM = 128;                 // vocabulary rows per block (MMA M, TME
 constexpr int XN = 32;                  // query rows per pass (MMA N)
 constexpr int XK = 32;                  // coordinates (= bytes per limb) per K-step (MMA K)
 constexpr int XL = 4;                   // limbs
-constexpr int XS = 4;                   // TMA ring stages
+constexpr int kMaxStages = 8;           // TMA ring stages (as many as shared memory allows)
+constexpr int XT = 192;                 // warps: TMA, MMA, 4 x epilogue
 constexpr int XA = XM * XK * XL;        // A bytes per stage (16 KB)
 constexpr int XB = XN * XK * XL;        // B bytes per K-step (4 KB)
-constexpr uint32_t XCOLS = 256;         // TMEM: 7 accumulators x 32 columns
-constexpr int kMaxExactDp = 1280;       // B resident in shared memory: 128 B per coordinate
+constexpr uint32_t XCOLS = 512;         // TMEM: two sets of 7 accumulators x 32 columns
+constexpr int kMaxExactDp = 1280;       // query limbs resident in shared memory: 128 B per coordinate
 
-// kind::i8 instruction descriptor: S32 accumulate, A/B signedness, N = 32, M = 128, K-major
-template <int SA, int SB>
-constexpr uint32_t idesc_i8() {
-  return (2u << 4) | ((uint32_t)SA << 7) | ((uint32_t)SB << 10) | ((uint32_t)(XN >> 3) << 17) |
-         ((uint32_t)(XM >> 4) << 24);
-}
+// kind::i8 instruction descriptor: S32 accumulate, signed A and B, N = 4 limbs x 32 query rows,
+// M = 128, both K-major
+constexpr uint32_t kIdescI8 = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)((XL * XN) >> 3) << 17) |
+                              ((uint32_t)(XM >> 4) << 24);
 
 __device__ __forceinline__ void mma_i8(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
   asm volatile(
@@ -74,147 +78,173 @@ __device__ __forceinline__ void cp16z(void* dst, const void* src, bool valid) {
                : "memory");
 }
 
-__global__ void __launch_bounds__(128, 2) build_mx_exact_kernel(
+// Persistent, warp-specialised: one block per SM, tiles blockIdx.x, + gridDim.x, ...
+//   warp 0 (one lane): TMA producer, K-step G of the block's job into ring stage G % stages
+//   warp 1 (one lane): MMA issuer, 16 MMAs per K-step into accumulator set U & 1 (of two)
+//   warps 2-5: epilogue of accumulator set U & 1 (TMEM lane quarter warp % 4), released to the
+//              MMA warp as soon as its tcgen05.ld are done
+// so the loads of the next tile stream while this tile's products finish and its epilogue runs.
+// The query limbs of every pass stay resident in shared memory for the whole kernel.
+__global__ void __launch_bounds__(XT, 1) build_mx_exact_kernel(
     const __grid_constant__ CUtensorMap tmap, const uint8_t* __restrict__ limbs,
     const long long* __restrict__ nn, int64_t V, int64_t row0, int64_t row1, int dp,
     const int32_t* __restrict__ sel, int v_r, int ld, float inv_scale, float lambda,
-    float* __restrict__ Kt, float* __restrict__ Mx) {
+    float* __restrict__ Kt, float* __restrict__ Mx, int stages) {
   extern __shared__ __align__(1024) uint8_t xs_raw[];
-  uint8_t* const ring = xs_raw + ((1024u - (su32(xs_raw) & 1023u)) & 1023u);  // [XS][XA]
-  uint8_t* const bq = ring + XS * XA;                                          // [dp / XK][XB]
+  uint8_t* const ring = xs_raw + ((1024u - (su32(xs_raw) & 1023u)) & 1023u);  // [stages][XA]
+  uint8_t* const bq = ring + stages * XA;                                      // [npass][nsteps][XB]
   __shared__ uint32_t tmem_base;
-  __shared__ __align__(8) uint64_t full[XS], empty[XS], accb;
-  __shared__ long long qn[XN];
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const int64_t k0 = row0 + (int64_t)blockIdx.x * XM;
-  const int64_t k = k0 + tid;
-  const bool kok = k < row1;
+  __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages], accf[2], acce[2];
+  __shared__ long long qn[4 * XN];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nsteps = dp / XK, nch = dp / 16;
   const int npass = (v_r + XN - 1) / XN;
-  const int total = npass * nsteps;
+  const int64_t ntiles = (row1 - row0 + XM - 1) / XM;
   const int ldx = ld + 4;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_base)), "n"(XCOLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  if (tid == 0) {
-    for (int i = 0; i < XS; ++i) {
+  if (tid == 32) {
+    for (int i = 0; i < stages; ++i) {
       umma::mbar_init(&full[i], 1);
       umma::mbar_init(&empty[i], 1);
     }
-    umma::mbar_init(&accb, 1);
+    for (int i = 0; i < 2; ++i) {
+      umma::mbar_init(&accf[i], 1);
+      umma::mbar_init(&acce[i], 4);   // one arrival per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
   }
+  // the query limbs of every pass: rows p*32 .. p*32 + 31 of sel (zeros past v_r), every K-step
+  const int nb = npass * nsteps * XL * 2 * XN;
+  for (int x = tid; x < nb; x += XT) {
+    const int r = x % XN;
+    int t = x / XN;
+    const int h = t & 1;
+    t >>= 1;
+    const int a = t % XL;
+    t /= XL;
+    const int s = t % nsteps, p = t / nsteps;
+    const int i = p * XN + r;
+    const bool ok = i < v_r;
+    const int64_t row = ok ? sel[i] : 0;
+    cp16z(bq + (p * nsteps + s) * XB + ((h * XL + a) * XN + r) * 16,   // N row 32 a + r
+          limbs + (((int64_t)a * nch + 2 * s + h) * V + row) * 16, ok);
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  for (int x = tid; x < npass * XN; x += XT) qn[x] = x < v_r ? nn[sel[x]] : 0;
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();  // tmem_base
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp >= 2) {  // both accumulator sets start at zero (the MMAs always accumulate)
+    for (int c = 0; c < 512; c += 32) umma::tmem_zero32(tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)c);
+    umma::tmem_wait_st();
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy writes -> tensor core
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tm = tmem_base;
 
-  // TMA producer (thread 0): K-step g of the whole job (pass g / nsteps) into stage g % XS
-  int issued = 0;
-  auto produce = [&](int upto) {
-    upto = upto < total ? upto : total;
-    while (issued < upto) {
-      const int st = issued % XS;
-      if (issued >= XS) umma::mbar_wait(su32(&empty[st]), ((issued / XS) - 1) & 1);
-      const int s = issued % nsteps;
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[st])), "r"(XA) : "memory");
-      asm volatile(
-          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
-          ::"r"(su32(ring + st * XA)), "l"(reinterpret_cast<uint64_t>(&tmap)), "r"((int)(2 * k0)), "r"(2 * s), "r"(0),
-          "r"(su32(&full[st]))
-          : "memory");
-      ++issued;
-    }
-  };
-  if (tid == 0) produce(XS);
-
-  const long long nnk = kok ? nn[k] : 0;
-  float mn = FLT_MAX;
-  for (int p = 0; p < npass; ++p) {
-    const int i0 = p * XN;
-    // the pass's query limbs: rows i0 .. i0 + 31 of sel (zeros past v_r), every K-step
-    const int nb = nsteps * XL * 2 * XN;
-    for (int x = tid; x < nb; x += 128) {
-      const int r = x % XN;
-      int t = x / XN;
-      const int h = t & 1;
-      t >>= 1;
-      const int a = t % XL, s = t / XL;
-      const bool ok = i0 + r < v_r;
-      const int64_t row = ok ? sel[i0 + r] : 0;
-      cp16z(bq + s * XB + ((a * 2 + h) * XN + r) * 16, limbs + (((int64_t)a * nch + 2 * s + h) * V + row) * 16, ok);
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-    if (tid < XN) qn[tid] = i0 + tid < v_r ? nn[sel[i0 + tid]] : 0;
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy writes -> tensor core
-    __syncthreads();
-    if (tid == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      for (int s = 0; s < nsteps; ++s) {
-        const int g = p * nsteps + s, st = g % XS;
-        umma::mbar_wait(su32(&full[st]), (g / XS) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t a0 = su32(ring + st * XA), b0 = su32(bq + s * XB);
-#pragma unroll
-        for (int a = 0; a < XL; ++a) {
-#pragma unroll
-          for (int b = 0; b < XL; ++b) {
-            const uint64_t da = umma::desc(a0 + a * 2 * XM * 16, XM * 16, 128);
-            const uint64_t db = umma::desc(b0 + b * 2 * XN * 16, XN * 16, 128);
-            const uint32_t id = a == XL - 1 ? (b == XL - 1 ? idesc_i8<1, 1>() : idesc_i8<1, 0>())
-                                            : (b == XL - 1 ? idesc_i8<0, 1>() : idesc_i8<0, 0>());
-            // (a == 0 || b == 3) is the first product of accumulator a + b at each step
-            mma_i8(tm + 32u * (uint32_t)(a + b), da, db, id, (s > 0 || !(a == 0 || b == XL - 1)) ? 1u : 0u);
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer
+      int G = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int c0 = (int)(2 * (row0 + t * XM));
+        for (int p = 0; p < npass; ++p) {
+          for (int s = 0; s < nsteps; ++s, ++G) {
+            const int st = G % stages;
+            if (G >= stages) umma::mbar_wait(su32(&empty[st]), ((G / stages) - 1) & 1);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[st])), "r"(XA) : "memory");
+            asm volatile(
+                "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+                ::"r"(su32(ring + st * XA)), "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(c0), "r"(2 * s), "r"(0),
+                "r"(su32(&full[st]))
+                : "memory");
           }
         }
-        umma::commit(&empty[st]);
-        produce(g + XS);  // refill: waits for step g - 1's MMAs while step g's run
       }
-      umma::commit(&accb);
     }
-    __syncwarp();
-    umma::mbar_wait(su32(&accb), p & 1);
-    __syncwarp();  // tcgen05.ld is warp-collective
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    // epilogue: thread tid = vocabulary row k = TMEM lane tid
-    long long dot[XN];
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      int G = 0, U = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        for (int p = 0; p < npass; ++p, ++U) {
+          const int buf = U & 1;
+          if (U >= 2) umma::mbar_wait(su32(&acce[buf]), ((U >> 1) - 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t acc = tm + 256u * (uint32_t)buf;
+          for (int s = 0; s < nsteps; ++s, ++G) {
+            const int st = G % stages;
+            umma::mbar_wait(su32(&full[st]), (G / stages) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const uint32_t a0 = su32(ring + st * XA), b0 = su32(bq + (p * nsteps + s) * XB);
+            const uint64_t db = umma::desc(b0, XL * XN * 16, 128);
 #pragma unroll
-    for (int c = 0; c < XN; ++c) dot[c] = 0;
-#pragma unroll
-    for (int g = 0; g < 2 * XL - 1; ++g) {
-      uint32_t v[32];
-      umma::tmem_ld32(tm + ((uint32_t)(warp * 32) << 16) + 32u * (uint32_t)g, v);
-#pragma unroll
-      for (int c = 0; c < XN; ++c) dot[c] += (long long)(int32_t)v[c] * (1LL << (8 * g));
-    }
-    if (kok) {
-      float* const out = Mx + k * ldx;
-#pragma unroll
-      for (int c4 = 0; c4 < XN; c4 += 4) {
-        float m4[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int c = c4 + u;
-          const long long m2 = (nnk - dot[c]) + (qn[c] - dot[c]);
-          const float m = __fsqrt_rn(__ll2float_rn(m2)) * inv_scale;
-          const bool real = i0 + c < v_r;
-          m4[u] = real ? m : 0.f;
-          if (real) mn = fminf(mn, m);
+            for (int a = 0; a < XL; ++a)  // vocabulary limb a x query limbs 0..3 -> accumulators a .. a + 3
+              mma_i8(acc + 32u * (uint32_t)a, umma::desc(a0 + a * 2 * XM * 16, XM * 16, 128), db, kIdescI8, 1u);
+            umma::commit(&empty[st]);   // the stage is free once these MMAs have read it
+          }
+          umma::commit(&accf[buf]);     // the pass's products are complete
         }
-        if (i0 + c4 < ld) *reinterpret_cast<float4*>(out + i0 + c4) = make_float4(m4[0], m4[1], m4[2], m4[3]);
       }
     }
-    asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();  // the accumulators and the query limbs are reused by the next pass
-  }
-  if (kok) {
-    float* const out = Mx + k * ldx;
-    for (int x = std::min(npass * XN, ld); x < ldx; ++x) out[x] = x == ld ? mn : 0.f;
-    if (Kt) {
-      for (int x = 0; x < ld; ++x) Kt[k * ld + x] = x < v_r ? expf(-lambda * (out[x] - mn)) : 0.f;
+  } else {  // epilogue: row r of the tile = TMEM lane r, lane quarter warp % 4
+    const int r = 32 * (warp & 3) + lane;
+    const uint32_t lanes = (uint32_t)(32 * (warp & 3)) << 16;
+    int U = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int64_t k = row0 + t * XM + r;
+      const bool kok = k < row1;
+      const long long nnk = kok ? nn[k] : 0;
+      float* const out = Mx + k * ldx;
+      float mn = FLT_MAX;
+      for (int p = 0; p < npass; ++p, ++U) {
+        const int buf = U & 1, i0 = p * XN;
+        umma::mbar_wait(su32(&accf[buf]), (U >> 1) & 1);
+        __syncwarp();  // tcgen05.ld is warp-collective
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        long long dot[XN];
+#pragma unroll
+        for (int c = 0; c < XN; ++c) dot[c] = 0;
+#pragma unroll
+        for (int g = 0; g < 2 * XL - 1; ++g) {
+          uint32_t v[32];
+          umma::tmem_ld32(tm + lanes + 256u * (uint32_t)buf + 32u * (uint32_t)g, v);
+#pragma unroll
+          for (int c = 0; c < XN; ++c) dot[c] += (long long)(int32_t)v[c] * (1LL << (8 * g));
+          umma::tmem_zero32(tm + lanes + 256u * (uint32_t)buf + 32u * (uint32_t)g);
+        }
+        umma::tmem_wait_st();
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&acce[buf])) : "memory");
+        if (kok) {
+#pragma unroll
+          for (int c4 = 0; c4 < XN; c4 += 4) {
+            float m4[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int c = c4 + u;
+              const long long m2 = (nnk - dot[c]) + (qn[i0 + c] - dot[c]);
+              const float m = __fsqrt_rn(__ll2float_rn(m2)) * inv_scale;
+              const bool real = i0 + c < v_r;
+              m4[u] = real ? m : 0.f;
+              if (real) mn = fminf(mn, m);
+            }
+            if (i0 + c4 < ld) *reinterpret_cast<float4*>(out + i0 + c4) = make_float4(m4[0], m4[1], m4[2], m4[3]);
+          }
+        }
+      }
+      if (kok) {
+        for (int x = std::min(npass * XN, ld); x < ldx; ++x) out[x] = x == ld ? mn : 0.f;
+        if (Kt) {
+          for (int x = 0; x < ld; ++x) Kt[k * ld + x] = x < v_r ? expf(-lambda * (out[x] - mn)) : 0.f;
+        }
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -250,8 +280,13 @@ __global__ void limbs_kernel(const float* __restrict__ E, int64_t V, int dp, int
       for (int u = 0; u < 4; ++u) {
         const int n = __float2int_rn(ldexpf(xs[u], F));
         acc += (long long)n * n;
+        int rest = n;
 #pragma unroll
-        for (int a = 0; a < XL; ++a) b[a] |= ((uint32_t)(n >> (8 * a)) & 0xffu) << (8 * u);
+        for (int a = 0; a < XL; ++a) {  // balanced digits: rest = L + 256 rest', L in [-128, 127]
+          const int L = ((rest + 128) & 255) - 128;
+          rest = (rest - L) >> 8;
+          b[a] |= ((uint32_t)L & 0xffu) << (8 * u);
+        }
       }
 #pragma unroll
       for (int a = 0; a < XL; ++a) w[a][q] = b[a];
@@ -334,20 +369,29 @@ int prepare_exact_e(const float* E, int64_t V, int dp, ExactE* x, cudaStream_t s
   return 0;
 }
 
-void launch_build_exact(const ExactE& x, int64_t row0, int64_t row1, const int32_t* sel, int v_r, int ld,
+bool launch_build_exact(const ExactE& x, int64_t row0, int64_t row1, const int32_t* sel, int v_r, int ld,
                         float lambda, float* Kt, float* Mx, cudaStream_t st) {
-  if (row1 <= row0) return;
-  // ring + resident query limbs; at least 80 KB so that at most two blocks (2 x 256 TMEM
-  // columns) share an SM
-  const size_t smem = std::max<size_t>((size_t)XS * XA + (size_t)(x.dp / XK) * XB + 1024, 80 * 1024);
-  static PerDevice attr;
+  static PerDevice attr, optin;
+  const int budget = optin.get([&] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return v;
+  }) - 2048;  // static shared memory (barriers, norms) and slack
+  const int npass = (v_r + XN - 1) / XN;
+  const int bbytes = npass * (x.dp / XK) * XB;
+  const int stages = std::min(kMaxStages, (budget - 1024 - bbytes) / XA);
+  if (stages < 2) return false;  // the query limbs do not fit: the caller runs another build
+  if (row1 <= row0) return true;
   attr.get([&] {
-    return (int)cudaFuncSetAttribute(build_mx_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(XS * XA + (kMaxExactDp / XK) * XB + 1024));
+    return (int)cudaFuncSetAttribute(build_mx_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, budget);
   });
-  const unsigned grid = (unsigned)((row1 - row0 + XM - 1) / XM);
-  build_mx_exact_kernel<<<grid, 128, smem, st>>>(*reinterpret_cast<const CUtensorMap*>(x.tmap), x.limbs, x.nn, x.V,
-                                                 row0, row1, x.dp, sel, v_r, ld, x.inv_scale, lambda, Kt, Mx);
+  const size_t smem = (size_t)stages * XA + bbytes + 1024;
+  const int64_t ntiles = (row1 - row0 + XM - 1) / XM;
+  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, device_sms());
+  build_mx_exact_kernel<<<grid, XT, smem, st>>>(*reinterpret_cast<const CUtensorMap*>(x.tmap), x.limbs, x.nn, x.V,
+                                                row0, row1, x.dp, sel, v_r, ld, x.inv_scale, lambda, Kt, Mx, stages);
+  return true;
 }
 
 }  // namespace wmd

@@ -691,11 +691,10 @@ wmd_status prepare_query(wmd_handle* h, int32_t v_r, float lambda, int64_t table
 // The distance build of the handle's WMD_OPT_BUILD kernel for rows [row0, row1).
 void build_rows(wmd_handle* h, const int32_t* d_sel, int32_t v_r, int32_t ld, float lambda, float* Kt, float* Mx,
                 int64_t row0, int64_t row1, cudaStream_t st) {
-  if (h->opt_build == WMD_BUILD_EXACT)
-    wmd::launch_build_exact(h->ex, row0, row1, d_sel, v_r, ld, lambda, Kt, Mx, st);
-  else
-    wmd::launch_build_ktilde(h->E.p, row0, row1, h->dp, d_sel, v_r, ld, lambda, Kt, Mx,
-                             h->opt_build == WMD_BUILD_TENSOR_CORE, st);
+  if (h->opt_build == WMD_BUILD_EXACT && wmd::launch_build_exact(h->ex, row0, row1, d_sel, v_r, ld, lambda, Kt, Mx, st))
+    return;
+  wmd::launch_build_ktilde(h->E.p, row0, row1, h->dp, d_sel, v_r, ld, lambda, Kt, Mx,
+                           h->opt_build == WMD_BUILD_TENSOR_CORE, st);
 }
 
 // a2 for vocabulary rows [row0, row1) (capturable stream work).

@@ -91,8 +91,9 @@ int exact_frac_bits_limit(int dp);
 // cudaError_t value (0 also when the shape is unsupported: x->ok stays false).
 int prepare_exact_e(const float* E, int64_t V, int dp, ExactE* x, cudaStream_t st);
 void free_exact_e(ExactE* x);
-// Same contract as launch_build_ktilde (x.ok required).
-void launch_build_exact(const ExactE& x, int64_t row0, int64_t row1, const int32_t* sel, int v_r, int ld,
+// Same contract as launch_build_ktilde (x.ok required). Returns false, launching nothing, when
+// the query's limbs do not fit in shared memory (dp * 128 B per 32 query rows).
+bool launch_build_exact(const ExactE& x, int64_t row0, int64_t row1, const int32_t* sel, int v_r, int ld,
                         float lambda, float* Kt, float* Mx, cudaStream_t st);
 
 // "While x changes" (NEXT-3): tol < 0 runs the fixed iteration count. Otherwise a
