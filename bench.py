@@ -34,6 +34,10 @@ L2_BYTES = 126 * 2 ** 20
 TRAFFIC_JSON = os.path.join(ROOT, "profiles", "r02_traffic.json")
 
 
+BUILD_NAMES = {0: "tensor-core 3xTF32 (tcgen05 kind::tf32)",
+               1: "direct difference (FP32 SIMT)",
+               2: "exact fixed point (tcgen05 kind::i8, TMA)"}
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -364,6 +368,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-roofbench", action="store_true", help="skip the in-run roofline microbenchmarks")
     ap.add_argument("--graph", action="store_true", help="replay each query as a CUDA graph (WMD_OPT_GRAPH)")
+    ap.add_argument("--build", default="default", choices=["default", "exact", "direct", "tf32x3"],
+                    help="distance build kernel (WMD_OPT_BUILD); default: the library's (exact where available)")
     ap.add_argument("--no-shard-build", action="store_true",
                     help="N > 1: every rank builds the whole distance table (default: vocabulary rows "
                          "split over the ranks + NCCL all-gather of the table)")
@@ -418,6 +424,9 @@ def main():
     eng = ShardedEngine(E, wl.col_ptr, wl.row_idx, wl.val, rank, world, local_rank, path=path,
                         timing=not args.graph, shard_build=not args.no_shard_build)
     h = eng.engine.h
+    if args.build != "default":
+        wmd.wmd_set_option(h, wmd.WMD_OPT_BUILD, {"exact": wmd.WMD_BUILD_EXACT, "direct": wmd.WMD_BUILD_DIRECT,
+                                                  "tf32x3": wmd.WMD_BUILD_TENSOR_CORE}[args.build])
     if args.graph:
         wmd.wmd_set_option(h, wmd.WMD_OPT_GRAPH, 1)
     stream = torch.cuda.current_stream()
@@ -518,8 +527,9 @@ def main():
             "data": "synthetic (seeded Zipf bag-of-words, N(0,1) embeddings; BASELINE.json config; "
                     "inputs pinned by synth/manifest.json)",
             "config": config_dict(cfg, wl, args, path=args.path, graph=bool(args.graph),
-                                  build=("tensor-core 3xTF32, vocabulary rows sharded + NCCL table all-gather"
-                                         if world > 1 and not args.no_shard_build else "tensor-core 3xTF32")),
+                                  build=BUILD_NAMES.get(int(st["last_build"]) if st else -1, "?") +
+                                  (", vocabulary rows sharded + NCCL table all-gather"
+                                   if world > 1 and not args.no_shard_build else "")),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(v_r * 8),
                     "d2h_bytes_per_step": int(wl.N * 4)},
             "gpu_launches": int(st["kernel_launches"]) if st else 0,
@@ -567,6 +577,18 @@ def roofline_fields(st, cfg, wl, eng, args, world, v_r, pk):
     # SURVEY.md §8(d) algorithmic bytes of the per-iteration formulation
     B_it = 8 * nnz_l + 4 * (nl + 1) + 8 * v_r * nl    # streamed: c, doc pointers, u read + write
     G_it = 4 * v_r * nnz_l                              # gathered: one K~ row slice per nonzero
+    # the distance build (a2): HBM-bound streaming of the embedding rows (the exact build's limb
+    # planes are 4 B per padded coordinate, like FP32 E) + the table writes
+    rows = -(-cfg.V // world) if (world > 1 and eng.shard_build) else cfg.V
+    dp = -(-cfg.d // 32) * 32
+    per_iter = st["last_path"] == wmd.WMD_PATH_PER_ITER
+    ldb = st["last_ld"]
+    b_bytes = rows * (4 * dp + 4 * (ldb + 4) + (4 * ldb if per_iter else 0))
+    t_b = st["build_ms"] / 1e3 / max(1, st["queries"])
+    build_roof = {"kernel": BUILD_NAMES.get(int(st["last_build"]), "?"), "bound": "hbm",
+                  "algorithmic_bytes": b_bytes, "ms": t_b * 1e3, "achieved": b_bytes / t_b / 1e9,
+                  "peak": hbm, "unit": "GB/s", "frac": b_bytes / t_b / 1e9 / hbm, "peak_source": peak_src,
+                  "share_of_step": st["build_ms"] / max(st["query_ms"], 1e-9)}
     if st["last_path"] == wmd.WMD_PATH_PER_ITER:
         n_launch = st["iter_launches"]
         t_launch = st["iter_ms"] / 1e3 / max(1, n_launch)
@@ -582,7 +604,7 @@ def roofline_fields(st, cfg, wl, eng, args, world, v_r, pk):
             "traffic": traffic, "traffic_source": traffic_src,
             "share_of_step": st["iter_ms"] / max(st["query_ms"], 1e-9),
         }
-        return {"roofline": roof}
+        return {"roofline": roof, "build_roofline": build_roof}
     # fused path: all t iterations + the final step per document in one pass (one launch per
     # length bucket): FP32 issue-bound; the roofline is over the step's whole fused phase
     t_phase = st["iter_ms"] / 1e3 / args.steps
@@ -629,7 +651,7 @@ def roofline_fields(st, cfg, wl, eng, args, world, v_r, pk):
                           "l2_hit_rate_pct": l2hit, "source": traffic_src},
         "hbm_read_measured_gbs": pk.get("hbm_read_gbs"),
     }
-    return {"roofline": roof, "memory_roofline": mem}
+    return {"roofline": roof, "memory_roofline": mem, "build_roofline": build_roof}
 
 
 if __name__ == "__main__":

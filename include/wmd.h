@@ -86,24 +86,32 @@ typedef enum {
                               tolerance, path, output pointer and buffers repeat (the query rows are
                               re-uploaded every call); per-phase timing is off in this mode.
                               Default 0 */
-  WMD_OPT_BUILD = 5,       /* distance build (a2), a wmd_build value; default WMD_BUILD_DIRECT */
+  WMD_OPT_BUILD = 5,       /* distance build (a2), a wmd_build value; default WMD_BUILD_EXACT where
+                              available (dp <= 1280), else WMD_BUILD_DIRECT */
   WMD_OPT_BATCH = 7,       /* wmd_query_batch, queries per fused pass (NEXT-2 (ii)): 0 = automatic
                               (as many tables as fit in half the L2, at most 16; default),
                               1 = one query at a time, 2..64 = that many. Applies when every query
                               takes the one-warp kernel for every document, no tolerance is set and
                               graph mode is off; results are bitwise those of single queries */
-  WMD_OPT_LAYOUT_DOC_NNZ = 6 /* >= 0: the path and table-width decision of every query assumes the
+  WMD_OPT_LAYOUT_DOC_NNZ = 6, /* >= 0: the path and table-width decision of every query assumes the
                               longest document has max(this, local longest) words. A document-
                               sharded run passes the GLOBAL longest document on every
                               rank, so all ranks pick the same path and row width (their tables
                               are then all-gatherable and their results bitwise equal to an
                               unsharded run). Default 0 (the local targets decide) */
+  WMD_OPT_LAYOUT_DOCS = 8  /* >= 0: the fused kernels' choice assumes max(this, local N) target
+                              documents: documents of <= 40 words run two per warp (half-warp
+                              kernel) at table widths 16 and 32 on corpora of >= 32768 documents,
+                              one per warp below. A document-sharded run passes the GLOBAL N on
+                              every rank (same kernels, bitwise equal to an unsharded run).
+                              Default 0 */
 } wmd_option;
 
 /* Distance build (a2) kernels, wmd_set_option(WMD_OPT_BUILD, ...). PAPER.md:259-268 (§6) compares
  * a dot-type and a GEMM-type distance kernel; both are here:
  *  WMD_BUILD_DIRECT: M_ik = sqrt(sum_t (E[sel_i,t] - E[k,t])^2) in FP32 SIMT (direct difference).
- *    Accurate for any embedding geometry (relative error of M ~1e-7); the default.
+ *    Accurate for any embedding geometry (relative error of M ~1e-7); the default where
+ *    WMD_BUILD_EXACT is unavailable.
  *  WMD_BUILD_TENSOR_CORE: M^2 = |e|^2 + |q|^2 - 2 e.q with e.q on the tcgen05 tensor cores in
  *    3xTF32, near pairs recomputed directly. Faster, but the expansion's absolute error
  *    ~eps (|e|^2 + |q|^2) reaches lambda*dM ~ 1e-2 on clustered embeddings of varied norm, where
@@ -114,7 +122,9 @@ typedef enum {
  *    the limb products, their int64 combination and M^2 = (|n_k|^2 - n_k.n_q) + (|n_q|^2 - n_k.n_q)
  *    are exact, so M_{i,sel_i} = 0 and there is no cancellation for any geometry. Needs
  *    dp = d rounded up to 32 <= 1280 (wmd_set_option fails with WMD_ERR_INVALID_ARGUMENT
- *    otherwise). Costs V * dp bytes of extra device memory per handle. */
+ *    otherwise); a query whose limbs do not fit in shared memory (dp * 128 B per 32 query rows,
+ *    e.g. dp = 1280 with v_r > 32) is built by WMD_BUILD_DIRECT (see wmd_stats.last_build).
+ *    Costs 4 * V * dp + 8 * V bytes of extra device memory per handle. The default. */
 typedef enum {
   WMD_BUILD_TENSOR_CORE = 0,
   WMD_BUILD_DIRECT = 1,
@@ -130,6 +140,7 @@ typedef struct {
   int32_t last_v_r;
   int32_t last_ld;           /* row width (floats) of the K~ / M tables: v_r rounded up to 8 (per-iteration path); on the fused path 8 CW with CW in {1, 2, 3, 4, 5, 6, 8} when every document fits the one-warp kernel, else in {4, 5, 6, 8, 10, 12, 13, 16} */
   int32_t last_path;         /* wmd_path actually used by the last query */
+  int32_t last_build;        /* wmd_build kernel that built the last query's distance table */
   int32_t timing_valid;      /* 1 if the *_ms fields below are populated (WMD_OPT_TIMING) */
   double build_ms;           /* distance + kernel build (step a2), summed over queries */
   double iter_ms;            /* Sinkhorn iterations (a4) */

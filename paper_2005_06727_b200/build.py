@@ -13,7 +13,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libwmd_b200.so")
-SOURCES = ["wmd_build.cu", "wmd_build_exact.cu", "wmd_kernels.cu", "wmd_fused.cu", "wmd_fused_cta.cu", "wmd_host.cpp"]
+SOURCES = ["wmd_build.cu", "wmd_build_exact.cu", "wmd_kernels.cu", "wmd_fused.cu", "wmd_fused_half.cu", "wmd_fused_cta.cu", "wmd_host.cpp"]
 HEADERS = ["wmd_internal.h", "wmd_umma.cuh", "wmd_device.cuh", "wmd_tile.cuh", os.path.join("..", "..", "include", "wmd.h")]
 
 NVCC_FLAGS = [

@@ -38,6 +38,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <cstdint>
+#include <cstdlib>
 #include <type_traits>
 
 #include "wmd_tile.cuh"
@@ -509,14 +510,28 @@ int fused_ld(int v_r, int64_t max_doc_nnz, bool conv) {
   return cta_ld(v_r);
 }
 
-void launch_sinkhorn_fused(const int4* sdoc, const Entry* ent, int64_t N,
+bool use_half(int ld, float tol, int64_t layout_docs) {
+  // WMD_FUSED_HALF: "0" never, "1" always (where the shape allows), unset: large corpora only
+  // (a few thousand documents leave most of the GPU idle at two documents per warp: Tweet's
+  // fused phase 0.036 ms one-warp vs 0.043 half-warp; Scaling 8.08 vs 7.36 ms)
+  const char* e = std::getenv("WMD_FUSED_HALF");
+  const bool shape = (ld == 16 || ld == 32) && tol < 0.f;
+  if (e && e[0] == '0') return false;
+  if (e && e[0] == '1') return shape;
+  return shape && layout_docs >= kHalfMinDocs;
+}
+
+void launch_sinkhorn_fused(const int4* sdoc, const Entry* ent, int64_t N, int64_t layout_docs,
                            const int64_t* len_prefix, int64_t max_len, int ld, const QuerySet& qs,
                            float lambda, int iters, float tol, cudaStream_t st0, StreamRing* ring) {
   // len_prefix[L] = number of documents with fewer than L nonzeros: the length-sorted order
   // splits into buckets of at most 8 / 16 / 32 / 40 / 48 / 64 nonzeros (one-warp kernel, one
   // launch each) and, past warp_max_rows(ld), 64 / 128 / ... / 320 (one-CTA kernel, one query).
   const int wmax = warp_max_rows(ld);
-  int64_t p0 = 0;
+  // documents of at most half_max_rows() nonzeros: two per warp (wmd_fused_half.cu)
+  int64_t p0 = use_half(ld, tol, layout_docs) ? launch_sinkhorn_half(sdoc, ent, N, len_prefix, max_len, ld, qs, lambda, iters,
+                                                        st0, ring, nullptr)
+                                 : 0;
   for (int bi = 0; bi < kNumBuckets && p0 < N && kBuckets[bi].ne <= wmax; ++bi) {
     const int NE = kBuckets[bi].ne;
     const int64_t p1 = NE >= max_len ? N : len_prefix[NE + 1];
@@ -540,10 +555,14 @@ void launch_sinkhorn_fused(const int4* sdoc, const Entry* ent, int64_t N,
                         qs.iters_doc, qs.dist, qs.flags, qs.flagged_list, qs.flagged_count, st0, ring);
 }
 
-int fused_launch_count(const int64_t* len_prefix, int64_t max_len, int64_t N, int ld) {
+int fused_launch_count(const int64_t* len_prefix, int64_t max_len, int64_t N, int64_t layout_docs, int ld,
+                       float tol) {
   const int wmax = warp_max_rows(ld);
-  int64_t p0 = 0;
   int cnt = 0;
+  const int64_t p0h = use_half(ld, tol, layout_docs) ? launch_sinkhorn_half(nullptr, nullptr, N, len_prefix, max_len, ld,
+                                                               QuerySet{}, 0.f, 0, nullptr, nullptr, &cnt)
+                                        : 0;
+  int64_t p0 = p0h;
   for (int bi = 0; bi < kNumBuckets && p0 < N && kBuckets[bi].ne <= wmax; ++bi) {
     const int64_t p1 = kBuckets[bi].ne >= max_len ? N : len_prefix[kBuckets[bi].ne + 1];
     cnt += p1 > p0;

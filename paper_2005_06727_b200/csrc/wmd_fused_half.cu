@@ -1,0 +1,508 @@
+// wmd_fused_half.cu — NEXT-1 for short documents: the one-warp fused kernel's
+// algorithm (wmd_fused.cu: all Sinkhorn iterations and the final step of a document in one
+// launch, doc-local two-sided rescale, power-of-two gauge, FP32 range certificate)
+// with HALF a warp per document: each 16-lane half-warp solves its own (document, query) item.
+//
+// Why: the one-warp kernel is bound by its warp shuffles (one SHFL per SM-cycle against ~3.5
+// FFMA, profiles/r01_issue_bench.jsonl; L1/TEX pipe 60-71 % busy, r02_full_scaling_fused_
+// summary.txt). A reduce-scatter + all-gather of S register slots over P lanes costs
+// 2 S (P - 1) / P shuffles, so per iteration a lane of the one-warp layout (8 b-lanes x 4 a-lanes,
+// RW x CW = 8 x 4 tile) issues 20 shuffles for 64 FFMA; here (4 b-lanes x 4 a-lanes per
+// document, RW x CW = 8 x 8 tile) a lane issues 24 shuffles for 128 FFMA, and every shuffle
+// instruction serves two documents: 12 shuffle issues per document-iteration instead of 20.
+//
+// Mapping: lane = 16 h + 4 a + b (h: the half-warp's item, a: row group, b: column group).
+// Row slots: full 16-row tiles T, slot 4T + t holds row 16T + 4a + (t ^ b); a tail tile (TW = 2)
+// slot 4NT + t holds row 16NT + 2a + (t ^ (b >> 1)). Column slots: quads g, slot 4g + t holds
+// column 16g + 4b + (t ^ a) (CW = 4Q columns per lane, LD = 4 CW in {16, 32}).
+//
+// Final step without M: the staging buffer is reused for the next item as soon as the block is
+// built (one buffer per half-warp, so four blocks fit per SM), so the final step recovers the
+// distance from the block: with Kh_ei = 2^(-alpha (D_ei - mu_i)) and M_ie = D_ei + m_e,
+//     sum_i Kh_ei uh_i M_ie = sum_i Kh_ei uh_i (mu_i - log2(Kh_ei) / alpha) + m_e s_e
+// (s_e = sum_i Kh_ei uh_i), and vh_e s_e = c_e after the last row step, so
+//     WMD_j = sum_e vh_e sum_i Kh_ei uh_i (mu_i - log2(Kh_ei) / alpha) + sum_e c_e m_e.
+// Every term is non-negative (no cancellation); log2 of an ex2 result returns its argument to
+// ~2^-22 relative, so M is recovered to ~3e-7 relative for lambda >= kFusedMinLambda (R35, R37).
+// Flushed entries (Kh = 0) contribute 0.
+#include <algorithm>
+#include <cfloat>
+#include <cstdint>
+#include <type_traits>
+
+#include "wmd_tile.cuh"
+
+namespace wmd {
+namespace {
+
+using namespace dev;
+using namespace tile;
+
+constexpr int kWarps = 4;
+constexpr int kThreads = 32 * kWarps;
+constexpr float kUnder = 0x1p-110f;        // 2^-126 / 2^-16
+constexpr float kLog2e = 1.4426950408889634f;
+
+template <int CW, int NT, int TW>
+struct HShape {
+  static_assert(CW % 4 == 0 && (TW == 0 || TW == 2), "quads only; tail of 2 rows per row group");
+  static constexpr int LD = 4 * CW;
+  static constexpr int Q = CW / 4;
+  static constexpr int RW = 4 * NT + TW;         // row slots per lane
+  static constexpr int NE = 16 * NT + 4 * TW;    // document rows covered
+  static constexpr int NW = (NE + 15) / 16;      // entry slots per lane
+  static constexpr int NOWN = NT + (TW ? 1 : 0); // own rows per lane after the row reduce
+  static constexpr int P = LD + 4;               // row pitch (floats) of Mx and the staging buffer
+  static constexpr int BUF = NE * P;
+  static constexpr int REGS = RW * CW;
+};
+
+template <int CW, int NT, int TW>
+constexpr int hmin_blocks() {
+  using S = HShape<CW, NT, TW>;
+#ifndef WMD_HALF_REGS
+#define WMD_HALF_REGS 24
+#endif
+  constexpr int regs = ((S::REGS + 3 * S::RW + 3 * CW + WMD_HALF_REGS) + 7) / 8 * 8;
+  constexpr int b = 65536 / (kThreads * regs);
+  return b < 1 ? 1 : (b > 8 ? 8 : b);
+}
+
+template <int NT, int TW>
+__device__ __forceinline__ int hrow_of(int s, int a, int b) {
+  if (s < 4 * NT) return 16 * (s >> 2) + 4 * a + ((s & 3) ^ b);
+  return 16 * NT + 2 * a + ((s - 4 * NT) ^ (b >> 1));
+}
+// natural-order column of slot c (the order hload_cols delivers) and slot-order column
+__device__ __forceinline__ int hnat_col(int c, int b) { return 16 * (c >> 2) + 4 * b + (c & 3); }
+
+template <int CW>
+__device__ __forceinline__ void hload_cols(const float* row, int b, float (&x)[CW]) {
+#pragma unroll
+  for (int g = 0; g < CW / 4; ++g) {
+    const float4 t = *reinterpret_cast<const float4*>(row + 16 * g + 4 * b);
+    x[4 * g] = t.x; x[4 * g + 1] = t.y; x[4 * g + 2] = t.z; x[4 * g + 3] = t.w;
+  }
+}
+
+// reduce-scatter of the row partials over the 4 b-lanes (xor 2, 1): p[4T] = row 16T + 4a + b,
+// p[4NT] = tail row 16NT + 2a + (b >> 1)
+template <int NT, int TW>
+__device__ __forceinline__ void hreduce_rows(float* p) {
+#pragma unroll
+  for (int T = 0; T < NT; ++T) {
+    float* q = p + 4 * T;
+    q[0] += shx(q[2], 2); q[1] += shx(q[3], 2);
+    q[0] += shx(q[1], 1);
+  }
+  if constexpr (TW == 2) {
+    float* q = p + 4 * NT;
+    q[0] += shx(q[1], 2);
+    q[0] += shx(q[0], 1);
+  }
+}
+
+// reduce-scatter of the column partials over the 4 a-lanes (xor 8, 4): q[4g] = column 16g + 4b + a
+template <int CW>
+__device__ __forceinline__ void hreduce_cols(float* q) {
+#pragma unroll
+  for (int g = 0; g < CW / 4; ++g) {
+    float* y = q + 4 * g;
+    y[0] += shx(y[2], 8); y[1] += shx(y[3], 8);
+    y[0] += shx(y[1], 4);
+  }
+}
+
+// max over the lanes of each half-warp (two warp reductions, one per half)
+__device__ __forceinline__ uint32_t half_max(uint32_t x, int h) {
+  const uint32_t m0 = __reduce_max_sync(kFull, h ? 0u : x);
+  const uint32_t m1 = __reduce_max_sync(kFull, h ? x : 0u);
+  return h ? m1 : m0;
+}
+__device__ __forceinline__ bool half_any(bool x, int h) {
+  return ((__ballot_sync(kFull, x) >> (16 * h)) & 0xffffu) != 0u;
+}
+
+template <int CW, int NT, int TW>
+__global__ void __launch_bounds__(kThreads, hmin_blocks<CW, NT, TW>()) sinkhorn_half_kernel(
+    const int4* __restrict__ sdoc, const Entry* __restrict__ ent, int64_t pos0, int64_t pos1,
+    QuerySet qs, float lambda, int iters) {
+  using S = HShape<CW, NT, TW>;
+  constexpr int LD = S::LD, RW = S::RW, NW = S::NW, P = S::P, Q = S::Q, NOWN = S::NOWN;
+  extern __shared__ __align__(16) float smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int h = lane >> 4, l16 = lane & 15;
+  const int a = l16 >> 2, b = l16 & 3;
+  float* const buf = smem + (2 * wib + h) * S::BUF;   // this half-warp's staging buffer
+  const int64_t stride = (int64_t)gridDim.x * kWarps * 2;
+  const uint64_t keep = l2_evict_last_policy();
+  const uint64_t stream_pol = l2_evict_first_policy();
+  const int2* ent2 = reinterpret_cast<const int2*>(ent);
+  const float alpha = lambda * kLog2e;
+  const float inv_alpha = 1.f / alpha;
+  const int nq = qs.nq;
+
+  int v_r = 0;
+  float kv_s = 0.f;
+  float r_own[Q];
+  bool oreal[Q], nreal[CW];
+  int64_t out0 = 0;
+  auto set_query = [&](int q) {
+    const int g = qs.qmap ? __ldg(qs.qmap + q) : q;
+    out0 = (int64_t)g * qs.N;
+    v_r = qs.vr ? __ldg(qs.vr + g) : qs.v_r;
+    kv_s = (float)v_r * kUnder;
+    const float* rp = qs.rpad + (size_t)g * WMD_MAX_VR_DEV;
+#pragma unroll
+    for (int gq = 0; gq < Q; ++gq) {
+      const int oc = 16 * gq + 4 * b + a;
+      r_own[gq] = __ldg(rp + oc);
+      oreal[gq] = oc < v_r;
+    }
+#pragma unroll
+    for (int c = 0; c < CW; ++c) nreal[c] = hnat_col(c, b) < v_r;
+  };
+
+  int64_t pos = pos0 + ((int64_t)blockIdx.x * kWarps + wib) * 2 + h;
+  int pj = -1, pb = 0, pn = 0;
+  int pk[NW];
+  float pc[NW];
+  int cj, cn;
+  int ck[NW];
+  float cc[NW];
+  auto stage1 = [&](int64_t p) {
+    pj = -1; pn = 0; pb = 0;
+    if (p < pos1) {
+      const int4 x = ldg_guarded(sdoc + p);
+      pj = x.x; pb = x.y; pn = x.z;
+    }
+  };
+  auto stage2 = [&]() {
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const int e = l16 + 16 * w;
+      int2 x = make_int2(0, 0);
+      if (e < pn) x = ldg_guarded_stream(ent2 + pb + e, stream_pol);
+      pk[w] = x.x;
+      pc[w] = __int_as_float(x.y);
+    }
+  };
+  auto stage3 = [&](const int (&ids)[NW], int nrows, int q) {
+    const float* tab = qs.Mx + (size_t)q * qs.mx_stride;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const int e = l16 + 16 * w;
+      if (e < nrows) {
+        uint32_t k;
+        asm volatile("mov.b32 %0, %1;" : "=r"(k) : "r"(ids[w]));
+        const float* src = tab + (size_t)k * P;
+        const uint32_t dst = smem_u32(buf + e * P);
+#pragma unroll
+        for (int x = 0; x < P / 4; ++x) cp_async16(dst + 16 * x, src + 4 * x, keep);
+      }
+    }
+    cp_async_commit();
+  };
+  auto take_next_doc = [&]() {
+    cj = pj; cn = pn;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) { ck[w] = pk[w]; cc[w] = pc[w]; }
+  };
+
+  stage1(pos);
+  stage2();
+  stage3(pk, pn, 0);
+  take_next_doc();
+  int q = 0;
+
+  while (__any_sync(kFull, pos < pos1)) {   // a half-warp past the end runs an empty item
+    const int j = cj, n = cn;
+    set_query(q);
+    // c and m of the lane's own rows: row 16T + l16 (full tiles), tail row 16NT + 2a + (b >> 1)
+    float c_own[NOWN], m_own[NOWN];
+    bool v_ok[NOWN];
+#pragma unroll
+    for (int T = 0; T < NT; ++T) {
+      c_own[T] = cc[T];
+      v_ok[T] = 16 * T + l16 < n;
+    }
+    if constexpr (TW > 0) {
+      const int tr = 2 * a + (b >> 1);
+      c_own[NT] = __shfl_sync(kFull, cc[NT], 16 * h + tr);
+      v_ok[NT] = 16 * NT + tr < n;
+    }
+    if (q == 0) stage1(pos + stride);
+    cp_async_wait_all();
+    __syncwarp();
+
+    // ---- block tile: D = M - m, mu = column minima over the document, Kh = 2^(-alpha (D - mu))
+    float K[RW][CW];
+    float u[CW], mu_s[CW];
+    bool und_mine;
+    {
+#pragma unroll
+      for (int T = 0; T < NOWN; ++T) {
+        const int e = T < NT ? 16 * T + l16 : 16 * NT + 2 * a + (b >> 1);
+        m_own[T] = v_ok[T] ? buf[e * P + LD] : 0.f;
+      }
+      float mu[CW];
+#pragma unroll
+      for (int c = 0; c < CW; ++c) mu[c] = INFINITY;
+      bool rok[RW];
+#pragma unroll
+      for (int s = 0; s < RW; ++s) {
+        const int e = hrow_of<NT, TW>(s, a, b);
+        rok[s] = e < n;
+        const float* row = buf + (rok[s] ? e : 0) * P;
+        float x[CW];
+        hload_cols<CW>(row, b, x);
+        const float bias = rok[s] ? -row[LD] : INFINITY;
+#pragma unroll
+        for (int c = 0; c < CW; ++c) {
+          K[s][c] = x[c] + bias;
+          mu[c] = fminf(mu[c], K[s][c]);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < CW; ++c) {  // column minima over the 4 a-lanes
+        mu[c] = fminf(mu[c], shx(mu[c], 4));
+        mu[c] = fminf(mu[c], shx(mu[c], 8));
+      }
+      float amu[CW], kmin[CW];
+#pragma unroll
+      for (int c = 0; c < CW; ++c) {
+        amu[c] = alpha * mu[c];
+        kmin[c] = 1.f;
+      }
+#pragma unroll
+      for (int s = 0; s < RW; ++s) {
+#pragma unroll
+        for (int c = 0; c < CW; ++c) {
+          K[s][c] = rok[s] ? ex2_ftz(fmaf(-alpha, K[s][c], amu[c])) : 1.f;
+          kmin[c] = fminf(kmin[c], K[s][c]);
+        }
+        to_slots<CW>(K[s], a);
+      }
+      bool flushed = false;
+#pragma unroll
+      for (int c = 0; c < CW; ++c) flushed |= nreal[c] && kmin[c] < FLT_MIN;
+      und_mine = half_any(flushed, h);
+#pragma unroll
+      for (int c = 0; c < CW; ++c) {
+        u[c] = nreal[c] ? (float)v_r * ex2_ftz(-alpha * mu[c]) : 0.f;
+        mu_s[c] = nreal[c] ? mu[c] : 0.f;   // padded columns: uh = 0 there
+      }
+      to_slots<CW>(u, a);
+      to_slots<CW>(mu_s, a);
+    }
+    __syncwarp();   // every lane of the half is done with the staged rows: the buffer is free
+    const bool und = __any_sync(kFull, und_mine);
+    if (q == nq - 1) stage2();
+    auto stage3_next = [&]() {
+      if (q + 1 < nq) stage3(ck, n, q + 1);
+      else stage3(pk, pn, 0);
+    };
+
+    // ---- iterations
+    float v_own[NOWN];
+    bool bad = false;
+    float umin = FLT_MAX;
+    uint32_t umax_all = 0u;
+    int it = 0;
+    auto iterate = [&](auto und_tag) {
+      constexpr bool UND = decltype(und_tag)::value;
+      float umax_k = (float)v_r * kv_s;
+      uint32_t vmax_b = 0u;
+      auto row_step = [&]() {
+        float p[RW];
+#pragma unroll
+        for (int s = 0; s < RW; ++s) {
+          float acc = K[s][0] * u[0];
+#pragma unroll
+          for (int c = 1; c < CW; ++c) acc = fmaf(K[s][c], u[c], acc);
+          p[s] = acc;
+        }
+        hreduce_rows<NT, TW>(p);
+        vmax_b = 0u;
+#pragma unroll
+        for (int o = 0; o < NOWN; ++o) {
+          const float sv = p[4 * o];
+          v_own[o] = c_own[o] * rcp_fast(sv);
+          if constexpr (UND) {
+            bad |= und_mine && v_ok[o] && umax_k > sv;
+            vmax_b = max(vmax_b, __float_as_uint(v_own[o]));
+          }
+        }
+      };
+      auto col_step = [&]() {
+        float vcap = 0.f;
+        if constexpr (UND) vcap = (float)n * __uint_as_float(half_max(vmax_b, h)) * kUnder;
+        float vs[RW];
+#pragma unroll
+        for (int T = 0; T < NT; ++T) {
+          vs[4 * T] = v_own[T];
+#pragma unroll
+          for (int t = 1; t < 4; ++t) vs[4 * T + t] = shx(v_own[T], t);
+        }
+        if constexpr (TW > 0) {
+          vs[4 * NT] = v_own[NT];
+          vs[4 * NT + 1] = shx(v_own[NT], 2);
+        }
+        float qv[CW];
+#pragma unroll
+        for (int c = 0; c < CW; ++c) {
+          float q0 = K[0][c] * vs[0];
+#pragma unroll
+          for (int s = 1; s < RW; ++s) q0 = fmaf(K[s][c], vs[s], q0);
+          qv[c] = q0;
+        }
+        hreduce_cols<CW>(qv);
+        uint32_t umax_b = 0u;
+        float uo[Q];
+#pragma unroll
+        for (int g = 0; g < Q; ++g) {
+          const float acc = qv[4 * g];
+          uo[g] = r_own[g] * rcp_fast(acc);
+          if constexpr (UND) bad |= und_mine && vcap > acc;
+          umax_b = max(umax_b, __float_as_uint(uo[g]));
+        }
+        umax_b = half_max(umax_b, h);
+        umax_all = max(umax_all, umax_b);
+        const float sc = __uint_as_float((254u - min(umax_b >> 23, 253u)) << 23);
+        if constexpr (UND) umax_k = 2.f * kv_s;
+#pragma unroll
+        for (int g = 0; g < Q; ++g) {
+          uo[g] *= sc;
+          umin = fminf(umin, oreal[g] ? uo[g] : 1.f);
+        }
+#pragma unroll
+        for (int g = 0; g < Q; ++g) {
+          u[4 * g] = uo[g];
+#pragma unroll
+          for (int c = 1; c < 4; ++c) u[4 * g + c] = shx(uo[g], 4 * c);
+        }
+      };
+      row_step();
+      if (iters > 0) {
+        col_step();
+        it = 1;
+        row_step();
+        stage3_next();   // the next item's entries have landed: start its row copies
+        while (it != iters) {
+          col_step();
+          ++it;
+          row_step();
+        }
+      } else {
+        stage3_next();
+      }
+    };
+    if (und) iterate(std::true_type{});
+    else iterate(std::false_type{});
+
+    // ---- final step, M recovered from the block (header comment)
+    float p[RW];
+#pragma unroll
+    for (int s = 0; s < RW; ++s) {
+      float acc = 0.f;
+#pragma unroll
+      for (int c = 0; c < CW; ++c) {
+        const float k = K[s][c];
+        const float dm = k > 0.f ? fmaf(-inv_alpha, lg2_approx(k), mu_s[c]) : 0.f;
+        acc = fmaf(k * u[c], dm, acc);
+      }
+      p[s] = acc;
+    }
+    hreduce_rows<NT, TW>(p);
+    float wsum = 0.f;
+#pragma unroll
+    for (int T = 0; T < NT; ++T)
+      if (v_ok[T]) wsum += fmaf(v_own[T], p[4 * T], c_own[T] * m_own[T]);
+    if constexpr (TW > 0) {  // each tail row is held by lanes b and b ^ 1: count it once
+      if (v_ok[NT] && (b & 1) == 0) wsum += fmaf(v_own[NT], p[4 * NT], c_own[NT] * m_own[NT]);
+    }
+#pragma unroll
+    for (int off = 8; off; off >>= 1) wsum += shx(wsum, off);
+    const bool flag = half_any(bad || !(umin >= FLT_MIN), h) || umax_all > 0x7f7fffffu || !(fabsf(wsum) <= FLT_MAX);
+    if (l16 == 0 && j >= 0) {
+      const int64_t o = (int64_t)q * qs.N + j;
+      qs.dist[out0 + j] = wsum;
+      if (qs.iters_doc) qs.iters_doc[o] = it;
+      uint8_t f = und_mine ? kFlagUnderflow : 0;
+      if (flag) {
+        f |= kFlagFp32Range;
+        qs.flagged_list[(int64_t)q * qs.N + atomicAdd(qs.flagged_count + q, 1)] = j;
+      }
+      if (f) qs.flags[o] |= f;
+    }
+    if (q + 1 < nq) {
+      ++q;
+    } else {
+      q = 0;
+      pos += stride;
+      take_next_doc();
+    }
+  }
+  cp_async_wait_all();
+}
+
+template <int CW, int NT, int TW>
+void launch_half_range(const int4* sdoc, const Entry* ent, int64_t p0, int64_t p1, const QuerySet& qs,
+                       float lambda, int iters, cudaStream_t st) {
+  if (p1 <= p0) return;
+  constexpr size_t smem = sizeof(float) * HShape<CW, NT, TW>::BUF * kWarps * 2;  // one buffer per half-warp
+  static PerDevice cache;
+  const int resident = cache.get([&] {
+    cudaFuncSetAttribute(sinkhorn_half_kernel<CW, NT, TW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(sinkhorn_half_kernel<CW, NT, TW>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sinkhorn_half_kernel<CW, NT, TW>, kThreads, smem);
+    return std::max(1, per_sm) * device_sms();
+  });
+  const int64_t need = (p1 - p0 + 2 * kWarps - 1) / (2 * kWarps);
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, resident));
+  sinkhorn_half_kernel<CW, NT, TW><<<grid, kThreads, smem, st>>>(sdoc, ent, p0, p1, qs, lambda, iters);
+}
+
+// Length buckets (rows covered: 8, 16, 24, 32, 40)
+struct HBucket { int ne, nt, tw; };
+constexpr HBucket kHBuckets[] = {{8, 0, 2}, {16, 1, 0}, {24, 1, 2}, {32, 2, 0}, {40, 2, 2}};
+constexpr int kNumHBuckets = 5;
+
+template <int CW>
+void dispatch_half(int bi, const int4* sdoc, const Entry* ent, int64_t p0, int64_t p1, const QuerySet& qs,
+                   float lambda, int iters, cudaStream_t st) {
+  switch (bi) {
+    case 0: launch_half_range<CW, 0, 2>(sdoc, ent, p0, p1, qs, lambda, iters, st); break;
+    case 1: launch_half_range<CW, 1, 0>(sdoc, ent, p0, p1, qs, lambda, iters, st); break;
+    case 2: launch_half_range<CW, 1, 2>(sdoc, ent, p0, p1, qs, lambda, iters, st); break;
+    case 3: launch_half_range<CW, 2, 0>(sdoc, ent, p0, p1, qs, lambda, iters, st); break;
+    default: launch_half_range<CW, 2, 2>(sdoc, ent, p0, p1, qs, lambda, iters, st); break;
+  }
+}
+
+}  // namespace
+
+int half_max_rows() { return kHBuckets[kNumHBuckets - 1].ne; }
+
+int64_t launch_sinkhorn_half(const int4* sdoc, const Entry* ent, int64_t N, const int64_t* len_prefix,
+                             int64_t max_len, int ld, const QuerySet& qs, float lambda, int iters,
+                             cudaStream_t st0, StreamRing* ring, int* launches) {
+  int64_t p0 = 0;
+  for (int bi = 0; bi < kNumHBuckets && p0 < N; ++bi) {
+    const int NE = kHBuckets[bi].ne;
+    const int64_t p1 = NE >= max_len ? N : len_prefix[NE + 1];
+    if (p1 > p0) {
+      if (launches) ++*launches;
+      if (sdoc) {
+        const cudaStream_t st = ring ? ring->next(st0) : st0;
+        if (ld == 16) dispatch_half<4>(bi, sdoc, ent, p0, p1, qs, lambda, iters, st);
+        else dispatch_half<8>(bi, sdoc, ent, p0, p1, qs, lambda, iters, st);
+      }
+    }
+    p0 = std::max(p0, p1);
+  }
+  return p0;
+}
+
+}  // namespace wmd

@@ -189,8 +189,10 @@ struct wmd_handle {
   int64_t targets_gen = 0;   // bumped by every wmd_set_targets (buffers may move)
   // options
   int64_t opt_path = WMD_PATH_AUTO, opt_timing = 0, opt_fallback = 1, opt_graph = 0;
-  int64_t opt_build = WMD_BUILD_DIRECT;  // WMD_OPT_BUILD
+  int64_t opt_build = WMD_BUILD_DIRECT;  // WMD_OPT_BUILD (WMD_BUILD_EXACT once ex is built)
+  int32_t build_used = WMD_BUILD_DIRECT; // kernel of the last build_rows
   int64_t opt_layout_nnz = 0;  // WMD_OPT_LAYOUT_DOC_NNZ
+  int64_t opt_layout_docs = 0; // WMD_OPT_LAYOUT_DOCS
   int64_t opt_batch = 0;       // WMD_OPT_BATCH
   // stats
   wmd_stats st{};
@@ -463,6 +465,7 @@ wmd_status wmd_create(const float* vocab_emb, int64_t V, int32_t d, int32_t devi
   // fixed-point limb planes for the exact tensor-core build (unsupported shapes leave ex.ok false)
   if (const int e = wmd::prepare_exact_e(h->E.p, V, dp, &h->ex, h->stream))
     return bail(e == (int)cudaErrorMemoryAllocation ? WMD_ERR_OUT_OF_MEMORY : WMD_ERR_CUDA);
+  if (h->ex.ok) h->opt_build = WMD_BUILD_EXACT;
   if (h->sel.ensure(WMD_MAX_VR) != cudaSuccess || h->rpad.ensure(WMD_MAX_VR) != cudaSuccess ||
       h->counters.ensure(6) != cudaSuccess)
     return bail(WMD_ERR_OUT_OF_MEMORY);
@@ -563,6 +566,10 @@ wmd_status wmd_set_option(wmd_handle* h, int32_t option, int64_t value) {
       if (value < 0 || value > 64) return fail(h, WMD_ERR_INVALID_ARGUMENT, "batch size outside [0, 64]");
       h->opt_batch = value;
       return WMD_OK;
+    case WMD_OPT_LAYOUT_DOCS:
+      if (value < 0) return fail(h, WMD_ERR_INVALID_ARGUMENT, "negative layout document count");
+      h->opt_layout_docs = value;
+      return WMD_OK;
     case WMD_OPT_LAYOUT_DOC_NNZ:
       if (value < 0) return fail(h, WMD_ERR_INVALID_ARGUMENT, "negative layout document length");
       h->opt_layout_nnz = value;
@@ -660,6 +667,7 @@ namespace {
 // WMD_OPT_LAYOUT_DOC_NNZ (every rank of a sharded run passes the global maximum, so all ranks
 // choose the same path and row width and their tables can be all-gathered).
 int64_t layout_doc_nnz(const wmd_handle* h) { return std::max(h->max_doc_nnz, h->opt_layout_nnz); }
+int64_t layout_docs(const wmd_handle* h) { return std::max(h->N, h->opt_layout_docs); }
 
 // Path decision and buffer allocation for one query (never inside a graph capture). The tables
 // get max(V, table_rows) rows (a sharded build all-gathers equal row slices, which may pad).
@@ -691,8 +699,11 @@ wmd_status prepare_query(wmd_handle* h, int32_t v_r, float lambda, int64_t table
 // The distance build of the handle's WMD_OPT_BUILD kernel for rows [row0, row1).
 void build_rows(wmd_handle* h, const int32_t* d_sel, int32_t v_r, int32_t ld, float lambda, float* Kt, float* Mx,
                 int64_t row0, int64_t row1, cudaStream_t st) {
-  if (h->opt_build == WMD_BUILD_EXACT && wmd::launch_build_exact(h->ex, row0, row1, d_sel, v_r, ld, lambda, Kt, Mx, st))
+  if (h->opt_build == WMD_BUILD_EXACT && wmd::launch_build_exact(h->ex, row0, row1, d_sel, v_r, ld, lambda, Kt, Mx, st)) {
+    h->build_used = WMD_BUILD_EXACT;
     return;
+  }
+  h->build_used = h->opt_build == WMD_BUILD_TENSOR_CORE ? WMD_BUILD_TENSOR_CORE : WMD_BUILD_DIRECT;
   wmd::launch_build_ktilde(h->E.p, row0, row1, h->dp, d_sel, v_r, ld, lambda, Kt, Mx,
                            h->opt_build == WMD_BUILD_TENSOR_CORE, st);
 }
@@ -722,7 +733,7 @@ wmd_status record_solve(wmd_handle* h, const float* d_r, int32_t v_r, float lamb
   if (fused) {
     // the length buckets run on the handle's lanes (forked from and joined to `st`), so one
     // bucket's tail overlaps the next one's start
-    const int nb = wmd::fused_launch_count(h->len_prefix.data(), h->max_doc_nnz, N, ld);
+    const int nb = wmd::fused_launch_count(h->len_prefix.data(), h->max_doc_nnz, N, layout_docs(h), ld, tol);
     wmd::StreamRing ring;
     if (nb > 1) {
       ring.s = h->lanes;
@@ -741,14 +752,14 @@ wmd_status record_solve(wmd_handle* h, const float* d_r, int32_t v_r, float lamb
     qs.iters_doc = h->iters_doc.p;
     qs.flagged_list = h->flagged.p;
     qs.flagged_count = h->counters.p;
-    wmd::launch_sinkhorn_fused(h->sdoc.p, h->ent.p, N, h->len_prefix.data(), h->max_doc_nnz, ld, qs, lambda,
+    wmd::launch_sinkhorn_fused(h->sdoc.p, h->ent.p, N, layout_docs(h), h->len_prefix.data(), h->max_doc_nnz, ld, qs, lambda,
                                iters, tol, st, &ring);
     DBG_PHASE(h, st, "fused Sinkhorn kernels");
     for (int i = 0; i < ring.n; ++i) {
       CK(h, cudaEventRecord(h->join_ev[i], h->lanes[i]));
       CK(h, cudaStreamWaitEvent(st, h->join_ev[i], 0));
     }
-    launches += wmd::fused_launch_count(h->len_prefix.data(), h->max_doc_nnz, N, ld);
+    launches += wmd::fused_launch_count(h->len_prefix.data(), h->max_doc_nnz, N, layout_docs(h), ld, tol);
     if (pe) { CK(h, cudaEventRecord(pe->ev[2], st)); CK(h, cudaEventRecord(pe->ev[3], st)); }
   } else {
     // a4: iters fused SDDMM_SpMM launches, u ping-pong
@@ -859,7 +870,8 @@ void note_query(wmd_handle* h, const int32_t* d_sel, const float* d_r, int32_t v
   h->u_valid = !fused && iters > 0;
   h->u_last = (!fused && iters > 0) ? ((iters - 1) & 1 ? h->ub.p : h->ua.p) : nullptr;
   h->path_used = fused ? WMD_PATH_FUSED : WMD_PATH_PER_ITER;
-  h->st.iter_launches += fused ? wmd::fused_launch_count(h->len_prefix.data(), h->max_doc_nnz, h->N, ld) : iters;
+  h->st.iter_launches += fused ? wmd::fused_launch_count(h->len_prefix.data(), h->max_doc_nnz, h->N, layout_docs(h), ld,
+                                                          h->tol >= 0.0 ? (float)h->tol : -1.f) : iters;
   h->v_r = v_r;
   h->ld = ld;
   h->last_sel = d_sel;
@@ -869,6 +881,7 @@ void note_query(wmd_handle* h, const int32_t* d_sel, const float* d_r, int32_t v
   h->st.last_v_r = v_r;
   h->st.last_ld = ld;
   h->st.last_path = h->path_used;
+  h->st.last_build = h->build_used;
 }
 
 // Enqueue one validated query whose sorted rows sel (device, v_r ids) and r (device, zero padded
@@ -1057,7 +1070,7 @@ wmd_status enqueue_batched(wmd_handle* h, const std::vector<int32_t>& nrow, int3
     qs.iters_doc = nullptr;
     qs.flagged_list = h->bflagged.p;
     qs.flagged_count = h->bcount.p;
-    const int nb = wmd::fused_launch_count(h->len_prefix.data(), h->max_doc_nnz, N, w);
+    const int nb = wmd::fused_launch_count(h->len_prefix.data(), h->max_doc_nnz, N, layout_docs(h), w, -1.f);
     wmd::StreamRing ring;
     if (nb > 1) {
       ring.s = h->lanes;
@@ -1065,7 +1078,7 @@ wmd_status enqueue_batched(wmd_handle* h, const std::vector<int32_t>& nrow, int3
       CK(h, cudaEventRecord(h->fork_ev, st));
       for (int i = 0; i < ring.n; ++i) CK(h, cudaStreamWaitEvent(h->lanes[i], h->fork_ev, 0));
     }
-    wmd::launch_sinkhorn_fused(h->sdoc.p, h->ent.p, N, h->len_prefix.data(), h->max_doc_nnz, w, qs, lambda, iters,
+    wmd::launch_sinkhorn_fused(h->sdoc.p, h->ent.p, N, layout_docs(h), h->len_prefix.data(), h->max_doc_nnz, w, qs, lambda, iters,
                                -1.f, st, &ring);
     DBG_PHASE(h, st, "batched fused Sinkhorn kernels");
     for (int i = 0; i < ring.n; ++i) {
@@ -1123,6 +1136,7 @@ wmd_status enqueue_batched(wmd_handle* h, const std::vector<int32_t>& nrow, int3
   h->st.last_v_r = nrow[last];
   h->st.last_ld = ld[last];
   h->st.last_path = WMD_PATH_FUSED;
+  h->st.last_build = h->build_used;
   return WMD_OK;
 }
 

@@ -167,10 +167,23 @@ struct QuerySet {
 
 // sdoc[p] = {document id, first nonzero, length, 0} of the p-th document in length order.
 // qs.nq > 1 needs every document within the one-warp kernel's rows (warp_max_rows(ld)).
-void launch_sinkhorn_fused(const int4* sdoc, const Entry* ent, int64_t N,
+void launch_sinkhorn_fused(const int4* sdoc, const Entry* ent, int64_t N, int64_t layout_docs,
                            const int64_t* len_prefix, int64_t max_len, int ld, const QuerySet& qs,
                            float lambda, int iters, float tol, cudaStream_t st, StreamRing* ring = nullptr);
-int fused_launch_count(const int64_t* len_prefix, int64_t max_len, int64_t N, int ld);
+int fused_launch_count(const int64_t* len_prefix, int64_t max_len, int64_t N, int64_t layout_docs, int ld, float tol);
+// Short documents, two per warp (wmd_fused_half.cu): ld in {16, 32}, fixed iteration count
+// (tol < 0), corpora of at least kHalfMinDocs documents (layout_docs: max(local N,
+// WMD_OPT_LAYOUT_DOCS)); WMD_FUSED_HALF=0 / 1 in the environment disables it / lifts the
+// corpus-size condition.
+constexpr int64_t kHalfMinDocs = 32768;
+bool use_half(int ld, float tol, int64_t layout_docs);
+int half_max_rows();
+// Launches the half-warp buckets over the length-sorted documents from position 0 while they fit
+// (<= half_max_rows() nonzeros); returns the first position not covered. sdoc == nullptr: only
+// counts the launches (into *launches).
+int64_t launch_sinkhorn_half(const int4* sdoc, const Entry* ent, int64_t N, const int64_t* len_prefix,
+                             int64_t max_len, int ld, const QuerySet& qs, float lambda, int iters,
+                             cudaStream_t st0, StreamRing* ring, int* launches);
 
 // --- NEXT-1, long documents: one CTA of ceil(n/32) warps per document (wmd_fused_cta.cu) -----
 int cta_max_rows();  // longest document the one-CTA kernel takes

@@ -119,6 +119,7 @@ class ShardedEngine:
         # hold the global col_ptr), so the ranks agree on the layout whatever their shard holds
         self.global_max_doc_nnz = global_max_doc_nnz(col_ptr)
         self.engine.set_option(wmd.WMD_OPT_LAYOUT_DOC_NNZ, self.global_max_doc_nnz)
+        self.engine.set_option(wmd.WMD_OPT_LAYOUT_DOCS, self.N)   # same fused kernels on every rank
         if self.n_local > 0:
             self.engine.set_targets(cp, ri, va)
         elif self.shard_build:  # no documents, but this rank still builds and gathers its rows

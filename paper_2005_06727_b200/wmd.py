@@ -37,6 +37,7 @@ WMD_ERR_CUDA = 10
 WMD_PATH_AUTO, WMD_PATH_PER_ITER, WMD_PATH_FUSED = 0, 1, 2
 WMD_OPT_PATH, WMD_OPT_TIMING, WMD_OPT_FALLBACK, WMD_OPT_GRAPH, WMD_OPT_BUILD = 1, 2, 3, 4, 5
 WMD_OPT_LAYOUT_DOC_NNZ = 6
+WMD_OPT_LAYOUT_DOCS = 8
 WMD_OPT_BATCH = 7
 WMD_BUILD_TENSOR_CORE, WMD_BUILD_DIRECT, WMD_BUILD_EXACT = 0, 1, 2
 
@@ -55,7 +56,7 @@ class wmd_stats(ctypes.Structure):
         ("queries", ctypes.c_int64), ("iter_launches", ctypes.c_int64),
         ("kernel_launches", ctypes.c_int64), ("fallback_docs", ctypes.c_int64),
         ("flagged_docs", ctypes.c_int64), ("last_v_r", ctypes.c_int32), ("last_ld", ctypes.c_int32),
-        ("last_path", ctypes.c_int32), ("timing_valid", ctypes.c_int32),
+        ("last_path", ctypes.c_int32), ("last_build", ctypes.c_int32), ("timing_valid", ctypes.c_int32),
         ("build_ms", ctypes.c_double), ("iter_ms", ctypes.c_double), ("final_ms", ctypes.c_double),
         ("fallback_ms", ctypes.c_double), ("query_ms", ctypes.c_double),
     ]

@@ -303,16 +303,18 @@ def test_structured_embeddings(W, kind, path):
     """Clustered embeddings with varied norms (synth.make_clustered_embeddings): distances from
     ~0 to several times sqrt(2d), so exp(-lambda M) spans far beyond FP32's exponent range within
     a document and the certificate / re-anchoring / FP64 re-run decide the result. The plain
-    FP64 oracle stays finite on these inputs (asserted). Default build (WMD_BUILD_DIRECT); the
-    tensor-core GEMM-form build's error on the same inputs is recorded, not asserted (DESIGN.md
-    R34: its |e|^2 + |q|^2 - 2e.q cancellation reaches ~1e-4 of the distance here)."""
+    FP64 oracle stays finite on these inputs (asserted). Default build (WMD_BUILD_EXACT) and the
+    direct-difference build are asserted; the 3xTF32 GEMM-form build's error on the same inputs
+    is recorded, not asserted (R34: its |e|^2 + |q|^2 - 2e.q cancellation reaches ~1e-4
+    of the distance here)."""
     E, cp, ri, va, (q, w), lam, iters = _clustered_case(kind)
     o = oracle_fanout(E, cp, ri, va, q, w, lam, iters)
     assert np.all(np.isfinite(o)), "instance outside the plain FP64 oracle's range"
     g, flags, st = gpu_run(W, E, cp, ri, va, q, w, lam, iters, path=path)
     name = f"edge/clustered_{kind}/{'auto' if path == 0 else 'per_iter'}"
     s = check(name, g, o, flags, {"N": int(cp.shape[0] - 1), "v_r": int(q.shape[0]), "ld": int(st["last_ld"]),
-                                  "path_used": int(st["last_path"]), "build": "direct"})
+                                  "path_used": int(st["last_path"]), "build": "exact"})
+    assert st["last_build"] == W.WMD_BUILD_EXACT
     # the instance must actually exercise the FP32 range machinery: in most documents the
     # doc-local block Kh = exp(-lambda (D - mu)) has entries below FLT_MIN = 2^-126 (a property
     # of the inputs, from the oracle's FP64 M)
@@ -324,6 +326,8 @@ def test_structured_embeddings(W, kind, path):
         D = M[:, ri[cp[j]:cp[j + 1]]] - m[ri[cp[j]:cp[j + 1]]]
         spans.append(lam * (D - D.min(1, keepdims=True)).max())
     assert np.mean(np.array(spans) > 126 * np.log(2)) > 0.5
+    gd, fd, std = gpu_run(W, E, cp, ri, va, q, w, lam, iters, path=path, build=W.WMD_BUILD_DIRECT)
+    check(name + "/direct_build", gd, o, fd, {"build": "direct"})
     gt, ft, _ = gpu_run(W, E, cp, ri, va, q, w, lam, iters, path=path, build=W.WMD_BUILD_TENSOR_CORE)
     st_tc, _ = parity_stats(gt, o, ft)
     record(name + "/tensor_core_build", dict(st_tc, build="tensor_core", asserted=False))

@@ -146,8 +146,8 @@ def test_query_compaction_bit_exact(W):
 
 @pytest.mark.parametrize("v_r", [1, 7, 30, 33, 64, 65, 100, 128])
 def test_build_tensor_core_equals_simt_and_oracle(W, v_r):
-    """a2 on the tensor cores (3xTF32 GEMM form, default) against the SIMT direct-difference
-    build and the FP64 oracle's M: every query width class (N = 32/64/96/128 MMA tiles), a
+    """a2 on the tensor cores (3xTF32 GEMM form; exact fixed point, the default) against the SIMT
+    direct-difference build and the FP64 oracle's M: every query width class (N = 32/64/96/128 MMA tiles), a
     vocabulary that is not a multiple of the 128-row tile, exact zeros at the query words."""
     wl = synth.make_workload("tiny")
     V = 1000 + 77
@@ -157,7 +157,7 @@ def test_build_tensor_core_equals_simt_and_oracle(W, v_r):
     w = np.full(v_r, 1.0 / v_r, np.float32)
     cp, ri, va = synth.csc_from_lists([{int(k): 1.0} for k in (0, 5, V - 1)], V)
     out = {}
-    for build in (0, 1):
+    for build in (0, 1, 2):
         h = W.wmd_create(E)
         try:
             W.wmd_set_option(h, W.WMD_OPT_BUILD, build)
@@ -169,7 +169,7 @@ def test_build_tensor_core_equals_simt_and_oracle(W, v_r):
         finally:
             W.wmd_destroy(h)
     M = oracle.euclidean_rows(E, q).T                      # (V, v_r) FP64
-    for build in (0, 1):
+    for build in (0, 1, 2):
         kt, km, cm = out[build]
         np.testing.assert_allclose(km[:, :v_r], M, rtol=2e-6, atol=2e-5)
         assert np.all(km[q, np.arange(v_r)] == 0.0)
