@@ -503,6 +503,10 @@ int fused_ld(int v_r, int64_t max_doc_nnz, bool conv) {
   int ld = 0;
   for (int cw : {1, 2, 3, 4, 5, 6, 8})
     if (8 * cw >= v_r) { ld = 8 * cw; break; }
+  if (const char* e = std::getenv("WMD_LD_OVERRIDE")) {   // measurement knob: a wider table
+    const int w = std::atoi(e);
+    if (w >= ld && w <= 64 && w % 8 == 0 && !conv) ld = w;
+  }
   if (ld && max_doc_nnz <= warp_max_rows(ld)) return ld;
   // longer documents (or v_r > 64): one CTA per document (wmd_fused_cta.cu; fixed iteration
   // count), whose table width the one-warp kernel then shares for the shorter documents
