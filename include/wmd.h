@@ -101,7 +101,7 @@ typedef enum {
                               unsharded run). Default 0 (the local targets decide) */
   WMD_OPT_LAYOUT_DOCS = 8  /* >= 0: the fused kernels' choice assumes max(this, local N) target
                               documents: documents of <= 40 words run two per warp (half-warp
-                              kernel) at table widths 16 and 32 on corpora of >= 32768 documents,
+                              kernel) at table widths 16-40 on corpora of >= 32768 documents,
                               one per warp below. A document-sharded run passes the GLOBAL N on
                               every rank (same kernels, bitwise equal to an unsharded run).
                               Default 0 */

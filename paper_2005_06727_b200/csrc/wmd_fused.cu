@@ -519,7 +519,7 @@ bool use_half(int ld, float tol, int64_t layout_docs) {
   // (a few thousand documents leave most of the GPU idle at two documents per warp: Tweet's
   // fused phase 0.036 ms one-warp vs 0.043 half-warp; Scaling 8.08 vs 7.36 ms)
   const char* e = std::getenv("WMD_FUSED_HALF");
-  const bool shape = (ld == 16 || ld == 32) && tol < 0.f;
+  const bool shape = (ld == 16 || ld == 24 || ld == 32 || ld == 40) && tol < 0.f;
   if (e && e[0] == '0') return false;
   if (e && e[0] == '1') return shape;
   return shape && layout_docs >= kHalfMinDocs;

@@ -13,8 +13,9 @@
 //
 // Mapping: lane = 16 h + 4 a + b (h: the half-warp's item, a: row group, b: column group).
 // Row slots: full 16-row tiles T, slot 4T + t holds row 16T + 4a + (t ^ b); a tail tile (TW = 2)
-// slot 4NT + t holds row 16NT + 2a + (t ^ (b >> 1)). Column slots: quads g, slot 4g + t holds
-// column 16g + 4b + (t ^ a) (CW = 4Q columns per lane, LD = 4 CW in {16, 32}).
+// slot 4NT + t holds row 16NT + 2a + (t ^ (b >> 1)). Column slots: CW = 4Q + R per lane,
+// LD = 4 CW in {16, 24, 32, 40}: quads g, slot 4g + t holds column 16g + 4b + (t ^ a), then R = 0
+// or 2 plain columns 16Q + Rb + r (the same in the four a-lanes, reduced by a butterfly).
 //
 // Final step without M: the staging buffer is reused for the next item as soon as the block is
 // built (one buffer per half-warp, so four blocks fit per SM), so the final step recovers the
@@ -45,9 +46,11 @@ constexpr float kLog2e = 1.4426950408889634f;
 
 template <int CW, int NT, int TW>
 struct HShape {
-  static_assert(CW % 4 == 0 && (TW == 0 || TW == 2), "quads only; tail of 2 rows per row group");
+  static_assert((CW % 4 == 0 || CW % 4 == 2) && (TW == 0 || TW == 2), "quads + 0 or 2 plain columns; 2-row tail");
   static constexpr int LD = 4 * CW;
-  static constexpr int Q = CW / 4;
+  static constexpr int Q = CW / 4;               // column quads per lane
+  static constexpr int R = CW % 4;               // plain columns per lane
+  static constexpr int NCO = Q + R;              // own columns per lane after the column reduce
   static constexpr int RW = 4 * NT + TW;         // row slots per lane
   static constexpr int NE = 16 * NT + 4 * TW;    // document rows covered
   static constexpr int NW = (NE + 15) / 16;      // entry slots per lane
@@ -73,15 +76,24 @@ __device__ __forceinline__ int hrow_of(int s, int a, int b) {
   if (s < 4 * NT) return 16 * (s >> 2) + 4 * a + ((s & 3) ^ b);
   return 16 * NT + 2 * a + ((s - 4 * NT) ^ (b >> 1));
 }
-// natural-order column of slot c (the order hload_cols delivers) and slot-order column
-__device__ __forceinline__ int hnat_col(int c, int b) { return 16 * (c >> 2) + 4 * b + (c & 3); }
+// natural-order column of slot c (the order hload_cols delivers)
+template <int CW>
+__device__ __forceinline__ int hnat_col(int c, int b) {
+  constexpr int Q = CW / 4, R = CW % 4;
+  return c < 4 * Q ? 16 * (c >> 2) + 4 * b + (c & 3) : 16 * Q + R * b + (c - 4 * Q);
+}
 
 template <int CW>
 __device__ __forceinline__ void hload_cols(const float* row, int b, float (&x)[CW]) {
+  constexpr int Q = CW / 4, R = CW % 4;
 #pragma unroll
-  for (int g = 0; g < CW / 4; ++g) {
+  for (int g = 0; g < Q; ++g) {
     const float4 t = *reinterpret_cast<const float4*>(row + 16 * g + 4 * b);
     x[4 * g] = t.x; x[4 * g + 1] = t.y; x[4 * g + 2] = t.z; x[4 * g + 3] = t.w;
+  }
+  if constexpr (R == 2) {
+    const float2 t = *reinterpret_cast<const float2*>(row + 16 * Q + 2 * b);
+    x[4 * Q] = t.x; x[4 * Q + 1] = t.y;
   }
 }
 
@@ -102,14 +114,21 @@ __device__ __forceinline__ void hreduce_rows(float* p) {
   }
 }
 
-// reduce-scatter of the column partials over the 4 a-lanes (xor 8, 4): q[4g] = column 16g + 4b + a
+// reduce-scatter of the column partials over the 4 a-lanes (xor 8, 4): q[4g] = column 16g + 4b + a;
+// plain columns by a butterfly (every a-lane gets the sum)
 template <int CW>
 __device__ __forceinline__ void hreduce_cols(float* q) {
+  constexpr int Q = CW / 4, R = CW % 4;
 #pragma unroll
-  for (int g = 0; g < CW / 4; ++g) {
+  for (int g = 0; g < Q; ++g) {
     float* y = q + 4 * g;
     y[0] += shx(y[2], 8); y[1] += shx(y[3], 8);
     y[0] += shx(y[1], 4);
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    q[4 * Q + r] += shx(q[4 * Q + r], 8);
+    q[4 * Q + r] += shx(q[4 * Q + r], 4);
   }
 }
 
@@ -128,7 +147,7 @@ __global__ void __launch_bounds__(kThreads, hmin_blocks<CW, NT, TW>()) sinkhorn_
     const int4* __restrict__ sdoc, const Entry* __restrict__ ent, int64_t pos0, int64_t pos1,
     QuerySet qs, float lambda, int iters) {
   using S = HShape<CW, NT, TW>;
-  constexpr int LD = S::LD, RW = S::RW, NW = S::NW, P = S::P, Q = S::Q, NOWN = S::NOWN;
+  constexpr int LD = S::LD, RW = S::RW, NW = S::NW, P = S::P, Q = S::Q, R = S::R, NCO = S::NCO, NOWN = S::NOWN;
   extern __shared__ __align__(16) float smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int h = lane >> 4, l16 = lane & 15;
@@ -144,8 +163,8 @@ __global__ void __launch_bounds__(kThreads, hmin_blocks<CW, NT, TW>()) sinkhorn_
 
   int v_r = 0;
   float kv_s = 0.f;
-  float r_own[Q];
-  bool oreal[Q], nreal[CW];
+  float r_own[NCO];
+  bool oreal[NCO], nreal[CW];
   int64_t out0 = 0;
   auto set_query = [&](int q) {
     const int g = qs.qmap ? __ldg(qs.qmap + q) : q;
@@ -154,13 +173,13 @@ __global__ void __launch_bounds__(kThreads, hmin_blocks<CW, NT, TW>()) sinkhorn_
     kv_s = (float)v_r * kUnder;
     const float* rp = qs.rpad + (size_t)g * WMD_MAX_VR_DEV;
 #pragma unroll
-    for (int gq = 0; gq < Q; ++gq) {
-      const int oc = 16 * gq + 4 * b + a;
+    for (int gq = 0; gq < NCO; ++gq) {
+      const int oc = gq < Q ? 16 * gq + 4 * b + a : 16 * Q + R * b + (gq - Q);
       r_own[gq] = __ldg(rp + oc);
       oreal[gq] = oc < v_r;
     }
 #pragma unroll
-    for (int c = 0; c < CW; ++c) nreal[c] = hnat_col(c, b) < v_r;
+    for (int c = 0; c < CW; ++c) nreal[c] = hnat_col<CW>(c, b) < v_r;
   };
 
   int64_t pos = pos0 + ((int64_t)blockIdx.x * kWarps + wib) * 2 + h;
@@ -358,10 +377,10 @@ __global__ void __launch_bounds__(kThreads, hmin_blocks<CW, NT, TW>()) sinkhorn_
         }
         hreduce_cols<CW>(qv);
         uint32_t umax_b = 0u;
-        float uo[Q];
+        float uo[NCO];
 #pragma unroll
-        for (int g = 0; g < Q; ++g) {
-          const float acc = qv[4 * g];
+        for (int g = 0; g < NCO; ++g) {
+          const float acc = qv[g < Q ? 4 * g : 4 * Q + (g - Q)];
           uo[g] = r_own[g] * rcp_fast(acc);
           if constexpr (UND) bad |= und_mine && vcap > acc;
           umax_b = max(umax_b, __float_as_uint(uo[g]));
@@ -371,7 +390,7 @@ __global__ void __launch_bounds__(kThreads, hmin_blocks<CW, NT, TW>()) sinkhorn_
         const float sc = __uint_as_float((254u - min(umax_b >> 23, 253u)) << 23);
         if constexpr (UND) umax_k = 2.f * kv_s;
 #pragma unroll
-        for (int g = 0; g < Q; ++g) {
+        for (int g = 0; g < NCO; ++g) {
           uo[g] *= sc;
           umin = fminf(umin, oreal[g] ? uo[g] : 1.f);
         }
@@ -381,6 +400,8 @@ __global__ void __launch_bounds__(kThreads, hmin_blocks<CW, NT, TW>()) sinkhorn_
 #pragma unroll
           for (int c = 1; c < 4; ++c) u[4 * g + c] = shx(uo[g], 4 * c);
         }
+#pragma unroll
+        for (int r = 0; r < R; ++r) u[4 * Q + r] = uo[Q + r];
       };
       row_step();
       if (iters > 0) {
@@ -496,8 +517,12 @@ int64_t launch_sinkhorn_half(const int4* sdoc, const Entry* ent, int64_t N, cons
       if (launches) ++*launches;
       if (sdoc) {
         const cudaStream_t st = ring ? ring->next(st0) : st0;
-        if (ld == 16) dispatch_half<4>(bi, sdoc, ent, p0, p1, qs, lambda, iters, st);
-        else dispatch_half<8>(bi, sdoc, ent, p0, p1, qs, lambda, iters, st);
+        switch (ld) {
+          case 16: dispatch_half<4>(bi, sdoc, ent, p0, p1, qs, lambda, iters, st); break;
+          case 24: dispatch_half<6>(bi, sdoc, ent, p0, p1, qs, lambda, iters, st); break;
+          case 32: dispatch_half<8>(bi, sdoc, ent, p0, p1, qs, lambda, iters, st); break;
+          default: dispatch_half<10>(bi, sdoc, ent, p0, p1, qs, lambda, iters, st); break;
+        }
       }
     }
     p0 = std::max(p0, p1);

@@ -171,7 +171,7 @@ void launch_sinkhorn_fused(const int4* sdoc, const Entry* ent, int64_t N, int64_
                            const int64_t* len_prefix, int64_t max_len, int ld, const QuerySet& qs,
                            float lambda, int iters, float tol, cudaStream_t st, StreamRing* ring = nullptr);
 int fused_launch_count(const int64_t* len_prefix, int64_t max_len, int64_t N, int64_t layout_docs, int ld, float tol);
-// Short documents, two per warp (wmd_fused_half.cu): ld in {16, 32}, fixed iteration count
+// Short documents, two per warp (wmd_fused_half.cu): ld in {16, 24, 32, 40}, fixed iteration count
 // (tol < 0), corpora of at least kHalfMinDocs documents (layout_docs: max(local N,
 // WMD_OPT_LAYOUT_DOCS)); WMD_FUSED_HALF=0 / 1 in the environment disables it / lifts the
 // corpus-size condition.

@@ -77,11 +77,11 @@ def _docs(V, lens, seed):
     return synth.csc_from_lists(docs, V)
 
 
-@pytest.mark.parametrize("v_r", [3, 9, 16, 17, 30, 32])
+@pytest.mark.parametrize("v_r", [3, 9, 16, 17, 22, 30, 32, 33, 40])
 @pytest.mark.parametrize("lam,iters", [(10.0, 15), (1e-3, 5), (0.05, 2), (25.0, 1), (10.0, 0)])
 def test_half_kernel_shapes(W, v_r, lam, iters):
     """Every half-warp bucket (8/16/24/32/40 rows, lengths 1-40 incl. bucket edges), an odd number
-    of documents per bucket (an empty half-warp item), table widths 16 and 32, lambda down to the
+    of documents per bucket (an empty half-warp item), table widths 16, 24, 32, 40, lambda down to the
     fused path's minimum, 0-15 iterations."""
     wl = synth.make_workload("tiny")
     V = wl.cfg.V
