@@ -149,3 +149,25 @@ def test_exact_build_end_to_end_against_oracle(W, name):
     cp, ri, va = synth.subset_docs(wl.col_ptr, wl.row_idx, wl.val, docs)
     o = oracle.sinkhorn_wmd(wl.E, cp, ri, va, q, w, cfg.lam, cfg.iters)
     np.testing.assert_allclose(g[docs], o, rtol=1e-4, atol=1e-6)
+
+
+@pytest.mark.parametrize("V", [1, 2, 77, 128, 129])
+def test_exact_build_tiny_vocabularies(W, V):
+    """Vocabularies smaller than one 128-row tile, exactly one tile, one row past it (the TMA box
+    past V reads zeros; rows past V are not written)."""
+    E = synth.make_workload("tiny").E[:V].copy()
+    q = np.arange(min(V, 5), dtype=np.int32)
+    w = np.full(q.shape[0], 1.0 / q.shape[0], np.float32)
+    cp, ri, va = synth.csc_from_lists([{0: 1.0}, {V - 1: 1.0}], V)
+    h = W.wmd_create(E)
+    try:
+        W.wmd_set_option(h, W.WMD_OPT_PATH, W.WMD_PATH_PER_ITER)
+        W.wmd_set_targets(h, cp, ri, va)
+        W.wmd_query(h, q, w, 10.0, 3, np.empty(2, np.float32))
+        st = W.wmd_get_stats(h)
+        assert st["last_build"] == W.WMD_BUILD_EXACT
+        _, km, cm = W.wmd_read_kernel(h, 0, V, st["last_ld"])
+    finally:
+        W.wmd_destroy(h)
+    Mq, _ = _fixed_point_M(E, q)
+    assert np.array_equal(km[:, :q.shape[0]], Mq) and np.array_equal(cm, Mq.min(axis=1))
