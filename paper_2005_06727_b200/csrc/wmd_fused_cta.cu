@@ -523,8 +523,8 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W, TW>()) sinkhorn_
         const float ub = uc * (-ia * betal[col_of<CW>(c, a, b)]);
 #pragma unroll
         for (int s = 0; s < RW; ++s) {
-          const float k = K[s][c];
-          const float kl = k > 0.f ? k * lg2_approx(k) : 0.f;
+          const float k = K[s][c];   // 0 or normal (ex2.approx.ftz): k log2 k = 0 for k = 0
+          const float kl = k * lg2_ftz(fmaxf(k, FLT_MIN));
           p[s] = fmaf(k, ub, fmaf(kl * ia, uc, p[s]));
         }
       }

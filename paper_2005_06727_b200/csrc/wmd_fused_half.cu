@@ -41,6 +41,10 @@ using namespace tile;
 
 constexpr int kWarps = 4;
 constexpr int kThreads = 32 * kWarps;
+#ifndef WMD_HALF_TWO_BUF   // 1: two staging buffers per half-warp, the final step reads M back
+#define WMD_HALF_TWO_BUF 0
+#endif
+constexpr int kBufs = WMD_HALF_TWO_BUF ? 2 : 1;
 constexpr float kUnder = 0x1p-110f;        // 2^-126 / 2^-16
 constexpr float kLog2e = 1.4426950408889634f;
 
@@ -152,7 +156,8 @@ __global__ void __launch_bounds__(kThreads, hmin_blocks<CW, NT, TW>()) sinkhorn_
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int h = lane >> 4, l16 = lane & 15;
   const int a = l16 >> 2, b = l16 & 3;
-  float* const buf = smem + (2 * wib + h) * S::BUF;   // this half-warp's staging buffer
+  float* const buf0 = smem + (2 * wib + h) * kBufs * S::BUF;   // this half-warp's staging buffer(s)
+  int cur = 0;                                                  // the current item's buffer
   const int64_t stride = (int64_t)gridDim.x * kWarps * 2;
   const uint64_t keep = l2_evict_last_policy();
   const uint64_t stream_pol = l2_evict_first_policy();
@@ -215,7 +220,7 @@ __global__ void __launch_bounds__(kThreads, hmin_blocks<CW, NT, TW>()) sinkhorn_
         uint32_t k;
         asm volatile("mov.b32 %0, %1;" : "=r"(k) : "r"(ids[w]));
         const float* src = tab + (size_t)k * P;
-        const uint32_t dst = smem_u32(buf + e * P);
+        const uint32_t dst = smem_u32(buf0 + (kBufs == 2 ? (cur ^ 1) : 0) * S::BUF + e * P);
 #pragma unroll
         for (int x = 0; x < P / 4; ++x) cp_async16(dst + 16 * x, src + 4 * x, keep);
       }
@@ -228,6 +233,7 @@ __global__ void __launch_bounds__(kThreads, hmin_blocks<CW, NT, TW>()) sinkhorn_
     for (int w = 0; w < NW; ++w) { ck[w] = pk[w]; cc[w] = pc[w]; }
   };
 
+  cur = kBufs == 2 ? 1 : 0;   // the first item's rows go to buffer cur ^ 1, flipped below
   stage1(pos);
   stage2();
   stage3(pk, pn, 0);
@@ -236,6 +242,8 @@ __global__ void __launch_bounds__(kThreads, hmin_blocks<CW, NT, TW>()) sinkhorn_
 
   while (__any_sync(kFull, pos < pos1)) {   // a half-warp past the end runs an empty item
     const int j = cj, n = cn;
+    if constexpr (kBufs == 2) cur ^= 1;
+    const float* const buf = buf0 + cur * S::BUF;
     set_query(q);
     // c and m of the lane's own rows: row 16T + l16 (full tiles), tail row 16NT + 2a + (b >> 1)
     float c_own[NOWN], m_own[NOWN];
@@ -423,24 +431,40 @@ __global__ void __launch_bounds__(kThreads, hmin_blocks<CW, NT, TW>()) sinkhorn_
 
     // ---- final step, M recovered from the block (header comment)
     float p[RW];
+    if constexpr (kBufs == 2) {   // M read back from the item's staged rows (exact)
 #pragma unroll
-    for (int s = 0; s < RW; ++s) {
-      float acc = 0.f;
+      for (int s = 0; s < RW; ++s) {
+        const int e = hrow_of<NT, TW>(s, a, b);
+        float x[CW];
+        hload_cols<CW>(buf + (e < n ? e : 0) * P, b, x);
+        to_slots<CW>(x, a);
+        float acc = 0.f;
 #pragma unroll
-      for (int c = 0; c < CW; ++c) {
-        const float k = K[s][c];
-        const float dm = k > 0.f ? fmaf(-inv_alpha, lg2_approx(k), mu_s[c]) : 0.f;
-        acc = fmaf(k * u[c], dm, acc);
+        for (int c = 0; c < CW; ++c) acc = fmaf(K[s][c] * u[c], x[c], acc);
+        p[s] = acc;
       }
-      p[s] = acc;
+    } else {                      // M recovered from the block (R37)
+#pragma unroll
+      for (int s = 0; s < RW; ++s) {
+        float acc = 0.f;
+#pragma unroll
+        for (int c = 0; c < CW; ++c) {
+          // Kh is 0 or normal (ex2.approx.ftz); a flushed entry gets a finite dm and k u = 0
+          const float k = K[s][c];
+          const float dm = fmaf(-inv_alpha, lg2_ftz(fmaxf(k, FLT_MIN)), mu_s[c]);
+          acc = fmaf(k * u[c], dm, acc);
+        }
+        p[s] = acc;
+      }
     }
     hreduce_rows<NT, TW>(p);
     float wsum = 0.f;
+    const float cm_w = kBufs == 2 ? 0.f : 1.f;   // the sum_e c_e m_e term of the recovered form
 #pragma unroll
     for (int T = 0; T < NT; ++T)
-      if (v_ok[T]) wsum += fmaf(v_own[T], p[4 * T], c_own[T] * m_own[T]);
+      if (v_ok[T]) wsum += fmaf(v_own[T], p[4 * T], cm_w * c_own[T] * m_own[T]);
     if constexpr (TW > 0) {  // each tail row is held by lanes b and b ^ 1: count it once
-      if (v_ok[NT] && (b & 1) == 0) wsum += fmaf(v_own[NT], p[4 * NT], c_own[NT] * m_own[NT]);
+      if (v_ok[NT] && (b & 1) == 0) wsum += fmaf(v_own[NT], p[4 * NT], cm_w * c_own[NT] * m_own[NT]);
     }
 #pragma unroll
     for (int off = 8; off; off >>= 1) wsum += shx(wsum, off);
@@ -471,7 +495,7 @@ template <int CW, int NT, int TW>
 void launch_half_range(const int4* sdoc, const Entry* ent, int64_t p0, int64_t p1, const QuerySet& qs,
                        float lambda, int iters, cudaStream_t st) {
   if (p1 <= p0) return;
-  constexpr size_t smem = sizeof(float) * HShape<CW, NT, TW>::BUF * kWarps * 2;  // one buffer per half-warp
+  constexpr size_t smem = sizeof(float) * HShape<CW, NT, TW>::BUF * kWarps * 2 * kBufs;  // per half-warp
   static PerDevice cache;
   const int resident = cache.get([&] {
     cudaFuncSetAttribute(sinkhorn_half_kernel<CW, NT, TW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
