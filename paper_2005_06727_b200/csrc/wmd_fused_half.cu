@@ -335,12 +335,13 @@ __global__ void __launch_bounds__(kThreads, hmin_blocks<CW, NT, TW>()) sinkhorn_
     bool bad = false;
     float umin = FLT_MAX;
     uint32_t umax_all = 0u;
+    float vlo = FLT_MAX, vhi = 0.f;   // range of the real v over all row steps (UND blocks)
     int it = 0;
     auto iterate = [&](auto und_tag) {
       constexpr bool UND = decltype(und_tag)::value;
-      float umax_k = (float)v_r * kv_s;
-      uint32_t vmax_b = 0u;
-      auto row_step = [&]() {
+      // FIRST: the first row step, the only one that checks s_e directly (uh0 is not gauged)
+      auto row_step = [&](auto first_tag) {
+        constexpr bool FIRST = decltype(first_tag)::value;
         float p[RW];
 #pragma unroll
         for (int s = 0; s < RW; ++s) {
@@ -350,20 +351,18 @@ __global__ void __launch_bounds__(kThreads, hmin_blocks<CW, NT, TW>()) sinkhorn_
           p[s] = acc;
         }
         hreduce_rows<NT, TW>(p);
-        vmax_b = 0u;
 #pragma unroll
         for (int o = 0; o < NOWN; ++o) {
           const float sv = p[4 * o];
           v_own[o] = c_own[o] * rcp_fast(sv);
           if constexpr (UND) {
-            bad |= und_mine && v_ok[o] && umax_k > sv;
-            vmax_b = max(vmax_b, __float_as_uint(v_own[o]));
+            if constexpr (FIRST) bad |= und_mine && v_ok[o] && (float)v_r * kv_s > sv;
+            vlo = fminf(vlo, v_ok[o] ? v_own[o] : FLT_MAX);
+            vhi = fmaxf(vhi, v_own[o]);
           }
         }
       };
       auto col_step = [&]() {
-        float vcap = 0.f;
-        if constexpr (UND) vcap = (float)n * __uint_as_float(half_max(vmax_b, h)) * kUnder;
         float vs[RW];
 #pragma unroll
         for (int T = 0; T < NT; ++T) {
@@ -390,13 +389,11 @@ __global__ void __launch_bounds__(kThreads, hmin_blocks<CW, NT, TW>()) sinkhorn_
         for (int g = 0; g < NCO; ++g) {
           const float acc = qv[g < Q ? 4 * g : 4 * Q + (g - Q)];
           uo[g] = r_own[g] * rcp_fast(acc);
-          if constexpr (UND) bad |= und_mine && vcap > acc;
           umax_b = max(umax_b, __float_as_uint(uo[g]));
         }
         umax_b = half_max(umax_b, h);
         umax_all = max(umax_all, umax_b);
         const float sc = __uint_as_float((254u - min(umax_b >> 23, 253u)) << 23);
-        if constexpr (UND) umax_k = 2.f * kv_s;
 #pragma unroll
         for (int g = 0; g < NCO; ++g) {
           uo[g] *= sc;
@@ -411,16 +408,16 @@ __global__ void __launch_bounds__(kThreads, hmin_blocks<CW, NT, TW>()) sinkhorn_
 #pragma unroll
         for (int r = 0; r < R; ++r) u[4 * Q + r] = uo[Q + r];
       };
-      row_step();
+      row_step(std::true_type{});
       if (iters > 0) {
         col_step();
         it = 1;
-        row_step();
+        row_step(std::false_type{});
         stage3_next();   // the next item's entries have landed: start its row copies
         while (it != iters) {
           col_step();
           ++it;
-          row_step();
+          row_step(std::false_type{});
         }
       } else {
         stage3_next();
@@ -468,6 +465,14 @@ __global__ void __launch_bounds__(kThreads, hmin_blocks<CW, NT, TW>()) sinkhorn_
     }
 #pragma unroll
     for (int off = 8; off; off >>= 1) wsum += shx(wsum, off);
+    // range form of the certificate (blocks with flushed entries; R38): every real row
+    // and column of Kh holds a 1, so s_e >= min_i uh_i and acc_i >= min_e vh_e; after each gauge
+    // max uh is in [1, 2). Sufficient for every iteration t >= 1: min uh >= 2 v_r 2^-110, and for
+    // every t: min vh >= n 2^-110 max vh (min / max over all t; t = 0 checked directly above).
+    if (__any_sync(kFull, und_mine)) {
+      const float vcap = (float)n * kUnder * __uint_as_float(half_max(__float_as_uint(vhi), h));
+      bad |= und_mine && (umin < 2.f * kv_s || vlo < vcap);
+    }
     const bool flag = half_any(bad || !(umin >= FLT_MIN), h) || umax_all > 0x7f7fffffu || !(fabsf(wsum) <= FLT_MAX);
     if (l16 == 0 && j >= 0) {
       const int64_t o = (int64_t)q * qs.N + j;
