@@ -13,7 +13,7 @@
 //
 // Mapping: lane = 16 h + 4 a + b (h: the half-warp's item, a: row group, b: column group).
 // Row slots: full 16-row tiles T, slot 4T + t holds row 16T + 4a + (t ^ b); a tail tile (TW = 2)
-// slot 4NT + t holds row 16NT + 2a + (t ^ (b >> 1)). Column slots: CW = 4Q + R per lane,
+// slot 4NT + t holds row 16NT + 2a + (t ^ (b >> 1)); (TW = 1) slot 4NT holds row 16NT + a. Column slots: CW = 4Q + R per lane,
 // LD = 4 CW in {16, 24, 32, 40}: quads g, slot 4g + t holds column 16g + 4b + (t ^ a), then R = 0
 // or 2 plain columns 16Q + Rb + r (the same in the four a-lanes, reduced by a butterfly).
 //
@@ -50,7 +50,7 @@ constexpr float kLog2e = 1.4426950408889634f;
 
 template <int CW, int NT, int TW>
 struct HShape {
-  static_assert((CW % 4 == 0 || CW % 4 == 2) && (TW == 0 || TW == 2), "quads + 0 or 2 plain columns; 2-row tail");
+  static_assert((CW % 4 == 0 || CW % 4 == 2) && TW >= 0 && TW <= 2, "quads + 0 or 2 plain columns; 0-2-row tail");
   static constexpr int LD = 4 * CW;
   static constexpr int Q = CW / 4;               // column quads per lane
   static constexpr int R = CW % 4;               // plain columns per lane
@@ -78,6 +78,7 @@ constexpr int hmin_blocks() {
 template <int NT, int TW>
 __device__ __forceinline__ int hrow_of(int s, int a, int b) {
   if (s < 4 * NT) return 16 * (s >> 2) + 4 * a + ((s & 3) ^ b);
+  if constexpr (TW == 1) return 16 * NT + a;   // one tail row per row group, in all four b-lanes
   return 16 * NT + 2 * a + ((s - 4 * NT) ^ (b >> 1));
 }
 // natural-order column of slot c (the order hload_cols delivers)
@@ -114,6 +115,10 @@ __device__ __forceinline__ void hreduce_rows(float* p) {
   if constexpr (TW == 2) {
     float* q = p + 4 * NT;
     q[0] += shx(q[1], 2);
+    q[0] += shx(q[0], 1);
+  } else if constexpr (TW == 1) {   // butterfly: every b-lane gets row 16NT + a
+    float* q = p + 4 * NT;
+    q[0] += shx(q[0], 2);
     q[0] += shx(q[0], 1);
   }
 }
@@ -254,7 +259,7 @@ __global__ void __launch_bounds__(kThreads, hmin_blocks<CW, NT, TW>()) sinkhorn_
       v_ok[T] = 16 * T + l16 < n;
     }
     if constexpr (TW > 0) {
-      const int tr = 2 * a + (b >> 1);
+      const int tr = TW == 1 ? a : 2 * a + (b >> 1);
       c_own[NT] = __shfl_sync(kFull, cc[NT], 16 * h + tr);
       v_ok[NT] = 16 * NT + tr < n;
     }
@@ -269,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, hmin_blocks<CW, NT, TW>()) sinkhorn_
     {
 #pragma unroll
       for (int T = 0; T < NOWN; ++T) {
-        const int e = T < NT ? 16 * T + l16 : 16 * NT + 2 * a + (b >> 1);
+        const int e = T < NT ? 16 * T + l16 : 16 * NT + (TW == 1 ? a : 2 * a + (b >> 1));
         m_own[T] = v_ok[T] ? buf[e * P + LD] : 0.f;
       }
       float mu[CW];
@@ -372,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, hmin_blocks<CW, NT, TW>()) sinkhorn_
         }
         if constexpr (TW > 0) {
           vs[4 * NT] = v_own[NT];
-          vs[4 * NT + 1] = shx(v_own[NT], 2);
+          if constexpr (TW == 2) vs[4 * NT + 1] = shx(v_own[NT], 2);
         }
         float qv[CW];
 #pragma unroll
@@ -460,8 +465,8 @@ __global__ void __launch_bounds__(kThreads, hmin_blocks<CW, NT, TW>()) sinkhorn_
 #pragma unroll
     for (int T = 0; T < NT; ++T)
       if (v_ok[T]) wsum += fmaf(v_own[T], p[4 * T], cm_w * c_own[T] * m_own[T]);
-    if constexpr (TW > 0) {  // each tail row is held by lanes b and b ^ 1: count it once
-      if (v_ok[NT] && (b & 1) == 0) wsum += fmaf(v_own[NT], p[4 * NT], cm_w * c_own[NT] * m_own[NT]);
+    if constexpr (TW > 0) {  // each tail row is held by 2 (TW = 2) or 4 (TW = 1) lanes: count it once
+      if (v_ok[NT] && (b & (TW == 1 ? 3 : 1)) == 0) wsum += fmaf(v_own[NT], p[4 * NT], cm_w * c_own[NT] * m_own[NT]);
     }
 #pragma unroll
     for (int off = 8; off; off >>= 1) wsum += shx(wsum, off);
@@ -514,10 +519,10 @@ void launch_half_range(const int4* sdoc, const Entry* ent, int64_t p0, int64_t p
   sinkhorn_half_kernel<CW, NT, TW><<<grid, kThreads, smem, st>>>(sdoc, ent, p0, p1, qs, lambda, iters);
 }
 
-// Length buckets (rows covered: 8, 16, 24, 32, 40)
+// Length buckets (rows covered: 8, 16, 20, 24, 32, 36, 40)
 struct HBucket { int ne, nt, tw; };
-constexpr HBucket kHBuckets[] = {{8, 0, 2}, {16, 1, 0}, {24, 1, 2}, {32, 2, 0}, {40, 2, 2}};
-constexpr int kNumHBuckets = 5;
+constexpr HBucket kHBuckets[] = {{8, 0, 2}, {16, 1, 0}, {20, 1, 1}, {24, 1, 2}, {32, 2, 0}, {36, 2, 1}, {40, 2, 2}};
+constexpr int kNumHBuckets = 7;
 
 template <int CW>
 void dispatch_half(int bi, const int4* sdoc, const Entry* ent, int64_t p0, int64_t p1, const QuerySet& qs,
@@ -525,8 +530,10 @@ void dispatch_half(int bi, const int4* sdoc, const Entry* ent, int64_t p0, int64
   switch (bi) {
     case 0: launch_half_range<CW, 0, 2>(sdoc, ent, p0, p1, qs, lambda, iters, st); break;
     case 1: launch_half_range<CW, 1, 0>(sdoc, ent, p0, p1, qs, lambda, iters, st); break;
-    case 2: launch_half_range<CW, 1, 2>(sdoc, ent, p0, p1, qs, lambda, iters, st); break;
-    case 3: launch_half_range<CW, 2, 0>(sdoc, ent, p0, p1, qs, lambda, iters, st); break;
+    case 2: launch_half_range<CW, 1, 1>(sdoc, ent, p0, p1, qs, lambda, iters, st); break;
+    case 3: launch_half_range<CW, 1, 2>(sdoc, ent, p0, p1, qs, lambda, iters, st); break;
+    case 4: launch_half_range<CW, 2, 0>(sdoc, ent, p0, p1, qs, lambda, iters, st); break;
+    case 5: launch_half_range<CW, 2, 1>(sdoc, ent, p0, p1, qs, lambda, iters, st); break;
     default: launch_half_range<CW, 2, 2>(sdoc, ent, p0, p1, qs, lambda, iters, st); break;
   }
 }

@@ -80,12 +80,12 @@ def _docs(V, lens, seed):
 @pytest.mark.parametrize("v_r", [3, 9, 16, 17, 22, 30, 32, 33, 40])
 @pytest.mark.parametrize("lam,iters", [(10.0, 15), (1e-3, 5), (0.05, 2), (25.0, 1), (10.0, 0)])
 def test_half_kernel_shapes(W, v_r, lam, iters):
-    """Every half-warp bucket (8/16/24/32/40 rows, lengths 1-40 incl. bucket edges), an odd number
+    """Every half-warp bucket (8/16/20/24/32/36/40 rows, lengths 1-40 incl. bucket edges), an odd number
     of documents per bucket (an empty half-warp item), table widths 16, 24, 32, 40, lambda down to the
     fused path's minimum, 0-15 iterations."""
     wl = synth.make_workload("tiny")
     V = wl.cfg.V
-    lens = list(range(1, 41)) + [8, 9, 16, 17, 24, 25, 32, 33, 40, 1, 2]
+    lens = list(range(1, 41)) + [8, 9, 16, 17, 20, 21, 24, 25, 32, 33, 36, 37, 40, 1, 2]
     cp, ri, va = _docs(V, lens, 7 * v_r + iters)
     rng = np.random.default_rng(v_r)
     q = np.sort(rng.choice(V, v_r, replace=False)).astype(np.int32)
