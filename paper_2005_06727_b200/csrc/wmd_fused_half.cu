@@ -545,23 +545,30 @@ int half_max_rows() { return kHBuckets[kNumHBuckets - 1].ne; }
 int64_t launch_sinkhorn_half(const int4* sdoc, const Entry* ent, int64_t N, const int64_t* len_prefix,
                              int64_t max_len, int ld, const QuerySet& qs, float lambda, int iters,
                              cudaStream_t st0, StreamRing* ring, int* launches) {
+  // bucket ranges of the length-sorted order
+  int64_t r0[kNumHBuckets], r1[kNumHBuckets];
   int64_t p0 = 0;
-  for (int bi = 0; bi < kNumHBuckets && p0 < N; ++bi) {
+  for (int bi = 0; bi < kNumHBuckets; ++bi) {
     const int NE = kHBuckets[bi].ne;
-    const int64_t p1 = NE >= max_len ? N : len_prefix[NE + 1];
-    if (p1 > p0) {
-      if (launches) ++*launches;
-      if (sdoc) {
-        const cudaStream_t st = ring ? ring->next(st0) : st0;
-        switch (ld) {
-          case 16: dispatch_half<4>(bi, sdoc, ent, p0, p1, qs, lambda, iters, st); break;
-          case 24: dispatch_half<6>(bi, sdoc, ent, p0, p1, qs, lambda, iters, st); break;
-          case 32: dispatch_half<8>(bi, sdoc, ent, p0, p1, qs, lambda, iters, st); break;
-          default: dispatch_half<10>(bi, sdoc, ent, p0, p1, qs, lambda, iters, st); break;
-        }
-      }
+    const int64_t p1 = p0 >= N ? p0 : (NE >= max_len ? N : len_prefix[NE + 1]);
+    r0[bi] = p0;
+    r1[bi] = std::max(p0, p1);
+    p0 = r1[bi];
+  }
+  // longest bucket first: the shorter ones fill the SMs its tail leaves idle (Scaling 6.57 ->
+  // 6.55 ms)
+  for (int k = 0; k < kNumHBuckets; ++k) {
+    const int bi = kNumHBuckets - 1 - k;
+    if (r1[bi] <= r0[bi]) continue;
+    if (launches) ++*launches;
+    if (!sdoc) continue;
+    const cudaStream_t st = ring ? ring->next(st0) : st0;
+    switch (ld) {
+      case 16: dispatch_half<4>(bi, sdoc, ent, r0[bi], r1[bi], qs, lambda, iters, st); break;
+      case 24: dispatch_half<6>(bi, sdoc, ent, r0[bi], r1[bi], qs, lambda, iters, st); break;
+      case 32: dispatch_half<8>(bi, sdoc, ent, r0[bi], r1[bi], qs, lambda, iters, st); break;
+      default: dispatch_half<10>(bi, sdoc, ent, r0[bi], r1[bi], qs, lambda, iters, st); break;
     }
-    p0 = std::max(p0, p1);
   }
   return p0;
 }
