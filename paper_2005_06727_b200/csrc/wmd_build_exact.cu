@@ -347,15 +347,15 @@ int prepare_exact_e(const float* E, int64_t V, int dp, ExactE* x, cudaStream_t s
   // TMA map of the planes in 8-byte elements: dims (innermost first) 2 V (the 16-byte row
   // pieces of one chunk, contiguous), dp/16 chunks, 4 planes; a box of 256 x 2 x 4 elements is
   // 128 rows x 2 chunks x 4 planes, each (plane, chunk) a contiguous 2 KB run
-  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-  if (!encode) {
+  static const PFN_cuTensorMapEncodeTiled_v12000 encode = [] {   // thread-safe one-time lookup
     cudaDriverEntryPointQueryResult q;
     void* fn = nullptr;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess || !fn)
-      return (int)cudaErrorNotSupported;
-    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-  }
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  if (!encode) return (int)cudaErrorNotSupported;
   static_assert(sizeof(CUtensorMap) <= sizeof(x->tmap), "tensor map storage");
   const cuuint64_t dims[3] = {(cuuint64_t)V * 2, (cuuint64_t)(dp / 16), (cuuint64_t)XL};
   const cuuint64_t strides[2] = {(cuuint64_t)V * 16, (cuuint64_t)V * dp};
