@@ -355,7 +355,10 @@ int prepare_exact_e(const float* E, int64_t V, int dp, ExactE* x, cudaStream_t s
       fn = nullptr;
     return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }();
-  if (!encode) return (int)cudaErrorNotSupported;
+  if (!encode) {   // no tensor-map encoder in this driver: the exact build is unavailable
+    free_exact_e(x);
+    return 0;
+  }
   static_assert(sizeof(CUtensorMap) <= sizeof(x->tmap), "tensor map storage");
   const cuuint64_t dims[3] = {(cuuint64_t)V * 2, (cuuint64_t)(dp / 16), (cuuint64_t)XL};
   const cuuint64_t strides[2] = {(cuuint64_t)V * 16, (cuuint64_t)V * dp};
@@ -364,7 +367,10 @@ int prepare_exact_e(const float* E, int64_t V, int dp, ExactE* x, cudaStream_t s
   const CUresult r = encode(reinterpret_cast<CUtensorMap*>(x->tmap), CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, x->limbs, dims,
                             strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return (int)cudaErrorInvalidValue;
+  if (r != CUDA_SUCCESS) {   // shape the TMA unit does not take: unavailable, not an error
+    free_exact_e(x);
+    return 0;
+  }
   x->ok = true;
   return 0;
 }
