@@ -1,23 +1,23 @@
 #!/bin/bash
 # Round-2 (second pass) ncu captures, run ON the GPU box from the repo root (gpurun), after the
 # exact tensor-core build and the half-warp fused kernel: full-set captures of one Scaling query's
-# fused launches (half-warp kernel, 4 length buckets) and distance build, of one Long query's
+# fused launches (half-warp kernel, 6 length buckets) and distance build, of one Long query's
 # one-CTA launches, summarised on the box into gpurun_out/prof/ (the .ncu-rep files stay in /tmp:
 # they exceed gpurun's copy-back cap), plus the launch list of a whole bench run. Each capture runs
 # after its command exited 0 alone.
 set -u
 mkdir -p gpurun_out/prof
-R=/tmp/ncu_r02b; mkdir -p $R
+R=/tmp/ncu_r02b; rm -rf $R; mkdir -p $R   # a reused box keeps /tmp: never summarise an old report
 B="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-roofbench"
 $B > gpurun_out/prof/plain_scaling.log 2>&1 || exit 3
-ncu --set full --import-source on --clock-control none -k regex:"sinkhorn_half" --launch-skip 4 --launch-count 4 \
+ncu -f --set full --import-source on --clock-control none -k regex:"sinkhorn_half" --launch-skip 6 --launch-count 6 \
     -o $R/scaling_half $B > gpurun_out/prof/ncu_scaling_half.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:"build_mx" --launch-skip 1 --launch-count 1 \
+ncu -f --set full --import-source on --clock-control none -k regex:"build_mx" --launch-skip 1 --launch-count 1 \
     -o $R/scaling_build $B > gpurun_out/prof/ncu_scaling_build.log 2>&1
 $B --config long > gpurun_out/prof/plain_long.log 2>&1 || exit 4
-ncu --set full --import-source on --clock-control none -k regex:"sinkhorn_cta" --launch-skip 5 --launch-count 5 \
+ncu -f --set full --import-source on --clock-control none -k regex:"sinkhorn_cta" --launch-skip 5 --launch-count 5 \
     -o $R/long_cta $B --config long > gpurun_out/prof/ncu_long_cta.log 2>&1
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/prof/launches_scaling.csv \
+ncu -f --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/prof/launches_scaling.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-roofbench > gpurun_out/prof/ncu_launches.log 2>&1
 for r in scaling_half scaling_build long_cta; do
   [ -f $R/$r.ncu-rep ] || continue
