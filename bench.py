@@ -614,8 +614,18 @@ def roofline_fields(st, cfg, wl, eng, args, world, v_r, pk):
     peak_tf = sms * 128 * 2 * mhz * 1e6 / 1e12
     ld = st["last_ld"]
     warp_max = 0 if ld > 64 else (48 if ld == 64 else 64)   # one-warp kernel's longest document
-    kname = ("sinkhorn_cta" if cfg.doc_lo > warp_max else
-             ("sinkhorn_fused + sinkhorn_cta" if cfg.doc_hi > warp_max else "sinkhorn_fused"))
+    # documents <= 40 words run two per warp (sinkhorn_half) at widths 16-40 on corpora of
+    # >= 32768 documents (WMD_OPT_LAYOUT_DOCS: the global count at N > 1); DESIGN.md §5
+    half = (ld in (16, 24, 32, 40) and wl.N >= 32768 and os.environ.get("WMD_FUSED_HALF") != "0") or \
+        (os.environ.get("WMD_FUSED_HALF") == "1" and ld in (16, 24, 32, 40))
+    parts = []
+    if half and cfg.doc_lo <= 40:
+        parts.append("sinkhorn_half")
+    if cfg.doc_lo <= warp_max and (cfg.doc_hi > 40 or not half):
+        parts.append("sinkhorn_fused")
+    if cfg.doc_hi > warp_max:
+        parts.append("sinkhorn_cta")
+    kname = " + ".join(parts)
     roof = {
         "kernel": kname, "bound": "alu",
         "achieved": flops / t_phase / 1e12, "peak": peak_tf, "unit": "TFLOP/s",
