@@ -347,13 +347,22 @@ __global__ void __launch_bounds__(kThreads, hmin_blocks<CW, NT, TW>()) sinkhorn_
       // FIRST: the first row step, the only one that checks s_e directly (uh0 is not gauged)
       auto row_step = [&](auto first_tag) {
         constexpr bool FIRST = decltype(first_tag)::value;
+        // rows in pairs (s, s + 1), one FFMA2 per column with uh broadcast
         float p[RW];
 #pragma unroll
-        for (int s = 0; s < RW; ++s) {
-          float acc = K[s][0] * u[0];
+        for (int s = 0; s + 1 < RW; s += 2) {
+          float a0, a1;
+          fmul2(a0, a1, K[s][0], K[s + 1][0], u[0], u[0]);
 #pragma unroll
-          for (int c = 1; c < CW; ++c) acc = fmaf(K[s][c], u[c], acc);
-          p[s] = acc;
+          for (int c = 1; c < CW; ++c) ffma2(a0, a1, K[s][c], K[s + 1][c], u[c], u[c], a0, a1);
+          p[s] = a0;
+          p[s + 1] = a1;
+        }
+        if constexpr (RW & 1) {
+          float acc = K[RW - 1][0] * u[0];
+#pragma unroll
+          for (int c = 1; c < CW; ++c) acc = fmaf(K[RW - 1][c], u[c], acc);
+          p[RW - 1] = acc;
         }
         hreduce_rows<NT, TW>(p);
 #pragma unroll
@@ -379,12 +388,23 @@ __global__ void __launch_bounds__(kThreads, hmin_blocks<CW, NT, TW>()) sinkhorn_
           vs[4 * NT] = v_own[NT];
           if constexpr (TW == 2) vs[4 * NT + 1] = shx(v_own[NT], 2);
         }
+        // the same row pairs: even- and odd-row partial sums of each column in one FFMA2, added
+        uint64_t vp[RW / 2];
+#pragma unroll
+        for (int s = 0; s + 1 < RW; s += 2) vp[s / 2] = pack2(vs[s], vs[s + 1]);
         float qv[CW];
 #pragma unroll
         for (int c = 0; c < CW; ++c) {
-          float q0 = K[0][c] * vs[0];
+          // (the chain starts at a pair of shuffled v values: one that holds v_own is copied
+          // first by ptxas)
+          constexpr int NP = RW / 2, P0 = NP > 1 ? 1 : 0;
+          float e0, e1;
+          fmul2p(e0, e1, K[2 * P0][c], K[2 * P0 + 1][c], vp[P0]);
 #pragma unroll
-          for (int s = 1; s < RW; ++s) q0 = fmaf(K[s][c], vs[s], q0);
+          for (int pp = 0; pp < NP; ++pp)
+            if (pp != P0) ffma2p(e0, e1, K[2 * pp][c], K[2 * pp + 1][c], vp[pp], e0, e1);
+          float q0 = e0 + e1;
+          if constexpr (RW & 1) q0 = fmaf(K[RW - 1][c], vs[RW - 1], q0);
           qv[c] = q0;
         }
         hreduce_cols<CW>(qv);
@@ -446,17 +466,31 @@ __global__ void __launch_bounds__(kThreads, hmin_blocks<CW, NT, TW>()) sinkhorn_
         p[s] = acc;
       }
     } else {                      // M recovered from the block (R37)
+      // Kh is 0 or normal (ex2.approx.ftz); a flushed entry gets a finite dm and k u = 0
 #pragma unroll
-      for (int s = 0; s < RW; ++s) {
+      for (int s = 0; s + 1 < RW; s += 2) {
+        float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+        for (int c = 0; c < CW; ++c) {
+          const float k0 = K[s][c], k1 = K[s + 1][c];
+          float d0, d1, w0, w1;
+          ffma2(d0, d1, lg2_ftz(fmaxf(k0, FLT_MIN)), lg2_ftz(fmaxf(k1, FLT_MIN)), -inv_alpha, -inv_alpha,
+                mu_s[c], mu_s[c]);
+          fmul2(w0, w1, k0, k1, u[c], u[c]);
+          ffma2(a0, a1, w0, w1, d0, d1, a0, a1);
+        }
+        p[s] = a0;
+        p[s + 1] = a1;
+      }
+      if constexpr (RW & 1) {
         float acc = 0.f;
 #pragma unroll
         for (int c = 0; c < CW; ++c) {
-          // Kh is 0 or normal (ex2.approx.ftz); a flushed entry gets a finite dm and k u = 0
-          const float k = K[s][c];
+          const float k = K[RW - 1][c];
           const float dm = fmaf(-inv_alpha, lg2_ftz(fmaxf(k, FLT_MIN)), mu_s[c]);
           acc = fmaf(k * u[c], dm, acc);
         }
-        p[s] = acc;
+        p[RW - 1] = acc;
       }
     }
     hreduce_rows<NT, TW>(p);

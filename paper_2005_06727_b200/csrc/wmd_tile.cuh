@@ -41,6 +41,57 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ float shx(float v, int m) { return __shfl_xor_sync(kFull, v, m); }
 
+// Packed FP32 FMA on two lanes: (d0, d1) = (a0 b0 + c0, a1 b1 + c1), one fma.rn.f32x2 (SASS
+// FFMA2, sm_100a): the same 128 FMA/clk/SM as scalar FFMA in half the issue slots, IEEE
+// round-to-nearest per lane (profiles/r02_ffma2.jsonl). With b0 == b1 ptxas uses the scalar
+// (broadcast) operand form; the pair (a0, a1) is one 64-bit register pair, so the fused kernels
+// use each block entry in the same pairing (two adjacent document rows) in every step.
+__device__ __forceinline__ void ffma2(float& d0, float& d1, float a0, float a1, float b0, float b1, float c0,
+                                      float c1) {
+  asm("{.reg .b64 A, B, C, D;\n\t"
+      "mov.b64 A, {%2, %3};\n\t"
+      "mov.b64 B, {%4, %5};\n\t"
+      "mov.b64 C, {%6, %7};\n\t"
+      "fma.rn.f32x2 D, A, B, C;\n\t"
+      "mov.b64 {%0, %1}, D;}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
+}
+// A (b0, b1) operand packed once and reused by several ffma2p / fmul2p (ptxas otherwise copies
+// the pair before each use)
+__device__ __forceinline__ uint64_t pack2(float x, float y) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
+  return r;
+}
+__device__ __forceinline__ void ffma2p(float& d0, float& d1, float a0, float a1, uint64_t b, float c0, float c1) {
+  asm("{.reg .b64 A, C, D;\n\t"
+      "mov.b64 A, {%2, %3};\n\t"
+      "mov.b64 C, {%5, %6};\n\t"
+      "fma.rn.f32x2 D, A, %4, C;\n\t"
+      "mov.b64 {%0, %1}, D;}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "l"(b), "f"(c0), "f"(c1));
+}
+__device__ __forceinline__ void fmul2p(float& d0, float& d1, float a0, float a1, uint64_t b) {
+  asm("{.reg .b64 A, D;\n\t"
+      "mov.b64 A, {%2, %3};\n\t"
+      "mul.rn.f32x2 D, A, %4;\n\t"
+      "mov.b64 {%0, %1}, D;}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "l"(b));
+}
+// (d0, d1) = (a0 b0, a1 b1): one mul.rn.f32x2 (FMUL2)
+__device__ __forceinline__ void fmul2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+  asm("{.reg .b64 A, B, D;\n\t"
+      "mov.b64 A, {%2, %3};\n\t"
+      "mov.b64 B, {%4, %5};\n\t"
+      "mul.rn.f32x2 D, A, B;\n\t"
+      "mov.b64 {%0, %1}, D;}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+
 // Row index (within the document) of row slot s of lane (a, b).
 template <int NT, int TW>
 __device__ __forceinline__ int row_of(int s, int a, int b) {
