@@ -144,10 +144,10 @@ int main() {
     int iters = 4096, grid = nsm * 16, blk = 256;
     float ms = time_ms([&] { fma_only<<<grid, blk>>>(out, iters); });
     double ops = (double)grid * blk * iters * 64;
-    printf("{\"test\":\"fma\",\"Gfma_per_s\":%.1f,\"per_sm_per_clk_at_1965\":%.1f}\n", ops / ms / 1e6, ops / ms / 1e3 / nsm / 1.965e9);
+    printf("{\"test\":\"fma\",\"Gfma_per_s\":%.1f,\"per_sm_per_clk_at_1965\":%.1f}\n", ops / ms / 1e6, ops / ms * 1e3 / nsm / 1.965e9);
     ms = time_ms([&] { shfl_only<<<grid, blk>>>(out, iters); });
     ops = (double)grid * blk * iters * 32;
-    printf("{\"test\":\"shfl\",\"Gshfl_lanes_per_s\":%.1f,\"lanes_per_sm_per_clk_at_1965\":%.1f}\n", ops / ms / 1e6, ops / ms / 1e3 / nsm / 1.965e9);
+    printf("{\"test\":\"shfl\",\"Gshfl_lanes_per_s\":%.1f,\"lanes_per_sm_per_clk_at_1965\":%.1f}\n", ops / ms / 1e6, ops / ms * 1e3 / nsm / 1.965e9);
   }
   return 0;
 }

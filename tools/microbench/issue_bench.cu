@@ -134,7 +134,9 @@ K_BEGIN(k_mufu)
   for (int i = 0; i < 8; ++i) a[i] = lane * 0.1f + i + 1.f;
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) { float y; asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(a[i])); a[i] = y; }
+    // volatile, and not an involution (rcp(rcp(x)) = x was folded away: the round-1 numbers of
+    // this entry were impossible); the FADD runs on the FMA pipe, not the MUFU unit
+    for (int i = 0; i < 8; ++i) { float y; asm volatile("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(a[i])); a[i] = y + 1.f; }
   }
   float s = 0; for (int i = 0; i < 8; ++i) s += a[i];
 K_END(s)
