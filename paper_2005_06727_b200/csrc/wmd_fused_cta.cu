@@ -102,6 +102,7 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W, TW>()) sinkhorn_
   constexpr int EPT = (ROWS + NT - 1) / NT;    // entries each thread prefetches
   static_assert(Q >= 1 && Q <= 4, "1 to 4 column quads per lane (LD <= 128)");
   static_assert(TW == 0 || TW == 2 || TW == 4, "tail width");
+  static_assert(RW % 2 == 0 && RW >= 4, "row slots in pairs (FFMA2)");
   extern __shared__ __align__(16) float csm[];
   float* colpart = csm;                                    // [2][W][CP]
   float* betal = colpart + 2 * W * CP;                     // [LD] column shifts beta (log2 units)
@@ -137,8 +138,9 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W, TW>()) sinkhorn_
   int64_t pos = pos0 + blockIdx.x;
   int pj = -1, pb = 0, pn = 0;
   int2 pe[EPT];
-  // (unconditional loads of clamped, always valid indices, then selects: the guarded-load form
-  // faulted in some optimised builds of this kernel)
+  // (unconditional loads of clamped, always valid indices, then selects. The round-1 guarded
+  // form is kept under WMD_CTA_GUARDED_LOADS; the faults once blamed on it came from load_D's
+  // select, see there and DESIGN.md §5)
   auto stage1 = [&](int64_t p) {
     const bool ok = p < pos1;
 #if WMD_CTA_GUARDED_LOADS  // the round-1 form (sanitizer study only, tools/cta_fault_study.py)
@@ -197,7 +199,12 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W, TW>()) sinkhorn_
     for (int s = 0; s < RW; ++s) {
       const int e = row0 + row_of<1, TW>(s, a, b);
       const bool ok = e < n;
-      const float* row = Mx + (size_t)(ok ? ents[e] : 0) * P;
+      // ents[e] is 0 for the rows past n (the prefetch zero-fills them), so no select: the form
+      // (ok ? ents[e] : 0) compiled to CS2R Rx, SRZ + a predicated IMAD.WIDE Rx + a read of Rx
+      // 5 cycles after the CS2R, which on rows past n read Rx's previous contents (a float) as
+      // the row offset — the illegal-address / misaligned / invalid-address-space fault of
+      // DESIGN.md §5, located with cuda-gdb (tools/sass_hazard_scan.py lists such sites)
+      const float* row = Mx + (size_t)ents[e] * P;
       float x[CW];
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
@@ -313,18 +320,23 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W, TW>()) sinkhorn_
         u4[0] = uo[g];
 #pragma unroll
         for (int t = 1; t < 4; ++t) u4[t] = shx(uo[g], 8 * t);
+        // rows in pairs (s, s + 1) (RW is even), one FFMA2 per column with uh broadcast
 #pragma unroll
-        for (int s = 0; s < RW; ++s) {
-          float acc = g == 0 ? K[s][0] * u4[0] : fmaf(K[s][4 * g], u4[0], p[s]);
+        for (int s = 0; s < RW; s += 2) {
+          float a0, a1;
+          if (g == 0) fmul2(a0, a1, K[s][0], K[s + 1][0], u4[0], u4[0]);
+          else ffma2(a0, a1, K[s][4 * g], K[s + 1][4 * g], u4[0], u4[0], p[s], p[s + 1]);
 #pragma unroll
-          for (int t = 1; t < 4; ++t) acc = fmaf(K[s][4 * g + t], u4[t], acc);
-          p[s] = acc;
+          for (int t = 1; t < 4; ++t) ffma2(a0, a1, K[s][4 * g + t], K[s + 1][4 * g + t], u4[t], u4[t], a0, a1);
+          p[s] = a0;
+          p[s + 1] = a1;
         }
       }
 #pragma unroll
       for (int r = 0; r < R; ++r) {
 #pragma unroll
-        for (int s = 0; s < RW; ++s) p[s] = fmaf(K[s][4 * Q + r], ur[r], p[s]);
+        for (int s = 0; s < RW; s += 2)
+          ffma2(p[s], p[s + 1], K[s][4 * Q + r], K[s + 1][4 * Q + r], ur[r], ur[r], p[s], p[s + 1]);
       }
       reduce_rows<1, TW>(p);
       bool sfail = false;
@@ -343,6 +355,9 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W, TW>()) sinkhorn_
         // SpMM: this warp's column partials, one quad at a time, then its transpose-reduce
         float vs[RW];
         rows_to_slots(v_own, vs);
+        uint64_t vp[RW / 2];  // the row pairs' v, packed once
+#pragma unroll
+        for (int s = 0; s < RW; s += 2) vp[s / 2] = pack2(vs[s], vs[s + 1]);
         float qo[4];
 #pragma unroll
         for (int g = 0; g < 4; ++g) qo[g] = 0.f;
@@ -350,11 +365,13 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W, TW>()) sinkhorn_
         for (int g = 0; g < Q; ++g) {
           float q[4];
 #pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            float q0 = K[0][4 * g + t] * vs[0];
+          for (int t = 0; t < 4; ++t) {  // even- and odd-row partial sums in one FFMA2, added
+            float e0, e1;
+            fmul2p(e0, e1, K[2][4 * g + t], K[3][4 * g + t], vp[1]);
 #pragma unroll
-            for (int s = 1; s < RW; ++s) q0 = fmaf(K[s][4 * g + t], vs[s], q0);
-            q[t] = q0;
+            for (int pp = 0; pp < RW / 2; ++pp)
+              if (pp != 1) ffma2p(e0, e1, K[2 * pp][4 * g + t], K[2 * pp + 1][4 * g + t], vp[pp], e0, e1);
+            q[t] = e0 + e1;
           }
           reduce_cols<4>(q);
           qo[g] = q[0];
@@ -363,9 +380,12 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W, TW>()) sinkhorn_
         *reinterpret_cast<float4*>(cp + warp * CP + 4 * lane) = make_float4(qo[0], qo[1], qo[2], qo[3]);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          float q0 = K[0][4 * Q + r] * vs[0];
+          float e0, e1;
+          fmul2p(e0, e1, K[2][4 * Q + r], K[3][4 * Q + r], vp[1]);
 #pragma unroll
-          for (int s = 1; s < RW; ++s) q0 = fmaf(K[s][4 * Q + r], vs[s], q0);
+          for (int pp = 0; pp < RW / 2; ++pp)
+            if (pp != 1) ffma2p(e0, e1, K[2 * pp][4 * Q + r], K[2 * pp + 1][4 * Q + r], vp[pp], e0, e1);
+          float q0 = e0 + e1;
           q0 += shx(q0, 16);
           q0 += shx(q0, 8);
           if (a == 0) cp[warp * CP + S::CREM + R * b + r] = q0;
@@ -522,10 +542,12 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W, TW>()) sinkhorn_
         const float uc = c < 4 * Q ? ((c & 3) == 0 ? uo[c >> 2] : shx(uo[c >> 2], 8 * (c & 3))) : ur[c - 4 * Q];
         const float ub = uc * (-ia * betal[col_of<CW>(c, a, b)]);
 #pragma unroll
-        for (int s = 0; s < RW; ++s) {
-          const float k = K[s][c];   // 0 or normal (ex2.approx.ftz): k log2 k = 0 for k = 0
-          const float kl = k * lg2_ftz(fmaxf(k, FLT_MIN));
-          p[s] = fmaf(k, ub, fmaf(kl * ia, uc, p[s]));
+        for (int s = 0; s < RW; s += 2) {  // row pairs; k = 0 or normal (ex2.approx.ftz): k log2 k = 0 for k = 0
+          const float k0 = K[s][c], k1 = K[s + 1][c];
+          float l0, l1, t0, t1;
+          fmul2(l0, l1, k0, k1, lg2_ftz(fmaxf(k0, FLT_MIN)), lg2_ftz(fmaxf(k1, FLT_MIN)));
+          ffma2(t0, t1, l0, l1, ia * uc, ia * uc, p[s], p[s + 1]);
+          ffma2(p[s], p[s + 1], k0, k1, ub, ub, t0, t1);
         }
       }
       reduce_rows<1, TW>(p);

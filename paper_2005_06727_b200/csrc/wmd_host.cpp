@@ -23,11 +23,14 @@
 
 using wmd::Entry;
 
+// Zeroed slack entries after ent / sdoc. 0: the slack (1,024 entries in rounds 1-2) contained the
+// one-CTA kernel's illegal-address fault before its cause was found (a ptxas wait-count hazard on
+// a CS2R-zeroed register); no kernel reads past the arrays' ends.
 #ifndef WMD_GUARD_ENTRIES
-#define WMD_GUARD_ENTRIES 1024
+#define WMD_GUARD_ENTRIES 0
 #endif
 namespace {
-constexpr int64_t kGuard = WMD_GUARD_ENTRIES;  // zeroed slack entries after ent / sdoc (see set_targets)
+constexpr int64_t kGuard = WMD_GUARD_ENTRIES;
 }  // namespace
 
 namespace {
@@ -626,8 +629,7 @@ wmd_status wmd_set_targets(wmd_handle* h, const int64_t* col_ptr, const int32_t*
   std::vector<Entry> en(nnz);
   for (int64_t q = 0; q < nnz; ++q) en[q] = Entry{row_idx[q], val[q]};
   CK(h, h->doc_ptr.ensure(N + 1));
-  // + kGuard zeroed entries past the end: the fused kernels' guarded prefetch loads clamp their
-  // index, and the slack keeps any speculated read of the next row inside the allocation
+  // (+ kGuard zeroed slack entries past the end, WMD_GUARD_ENTRIES, 0 by default)
   CK(h, h->ent.ensure(nnz + kGuard));
   if (kGuard) CK(h, cudaMemsetAsync(h->ent.p + nnz, 0, kGuard * sizeof(Entry), h->stream));
   CK(h, h->order.ensure(N));
