@@ -405,8 +405,8 @@ __global__ void __launch_bounds__(32 * W, cta_min_blocks<CW, W, TW>()) sinkhorn_
         for (int g = 0; g < 4; ++g) acc[g] = 0.f;
 #pragma unroll
         for (int r = 0; r < R; ++r) accr[r] = 0.f;
-#pragma unroll 2
-        for (int w = 0; w < W; ++w) {  // (not fully unrolled: bounds the loads in flight)
+#pragma unroll
+        for (int w = 0; w < W; ++w) {  // (fully unrolled: Long 16.55 -> 16.32 ms)
           const float4 t = *reinterpret_cast<const float4*>(cp + w * CP + 4 * lane);
           acc[0] += t.x; acc[1] += t.y; acc[2] += t.z; acc[3] += t.w;
 #pragma unroll
