@@ -1,7 +1,8 @@
 // wmd_fused_half.cu — NEXT-1 for short documents: the one-warp fused kernel's
 // algorithm (wmd_fused.cu: all Sinkhorn iterations and the final step of a document in one
-// launch, doc-local two-sided rescale, power-of-two gauge, FP32 range certificate)
-// with HALF a warp per document: each 16-lane half-warp solves its own (document, query) item.
+// launch, doc-local two-sided rescale, FP32 range certificate) with HALF a warp per
+// document (each 16-lane half-warp solves its own (document, query) item) and, unlike it, no
+// per-iteration gauge of uh (R39).
 //
 // Why: the one-warp kernel is bound by its warp shuffles (one SHFL per SM-cycle against ~3.5
 // FFMA, profiles/r01_issue_bench.jsonl; L1/TEX pipe 60-71 % busy, r02_full_scaling_fused_
@@ -344,7 +345,8 @@ __global__ void __launch_bounds__(kThreads, hmin_blocks<CW, NT, TW>()) sinkhorn_
     int it = 0;
     auto iterate = [&](auto und_tag) {
       constexpr bool UND = decltype(und_tag)::value;
-      // FIRST: the first row step, the only one that checks s_e directly (uh0 is not gauged)
+      // FIRST: the first row step, the only one that checks s_e directly (uh0 is outside the
+      // running range of the column steps' uh)
       auto row_step = [&](auto first_tag) {
         constexpr bool FIRST = decltype(first_tag)::value;
         // rows in pairs (s, s + 1), one FFMA2 per column with uh broadcast
@@ -416,14 +418,11 @@ __global__ void __launch_bounds__(kThreads, hmin_blocks<CW, NT, TW>()) sinkhorn_
           uo[g] = r_own[g] * rcp_fast(acc);
           umax_b = max(umax_b, __float_as_uint(uo[g]));
         }
-        umax_b = half_max(umax_b, h);
+        // no per-iteration gauge (R39): the lane's running max / min of the real uh,
+        // reduced over the half once per document
         umax_all = max(umax_all, umax_b);
-        const float sc = __uint_as_float((254u - min(umax_b >> 23, 253u)) << 23);
 #pragma unroll
-        for (int g = 0; g < NCO; ++g) {
-          uo[g] *= sc;
-          umin = fminf(umin, oreal[g] ? uo[g] : 1.f);
-        }
+        for (int g = 0; g < NCO; ++g) umin = fminf(umin, oreal[g] ? uo[g] : FLT_MAX);
 #pragma unroll
         for (int g = 0; g < Q; ++g) {
           u[4 * g] = uo[g];
@@ -504,15 +503,16 @@ __global__ void __launch_bounds__(kThreads, hmin_blocks<CW, NT, TW>()) sinkhorn_
     }
 #pragma unroll
     for (int off = 8; off; off >>= 1) wsum += shx(wsum, off);
-    // range form of the certificate (blocks with flushed entries; R38): every real row
-    // and column of Kh holds a 1, so s_e >= min_i uh_i and acc_i >= min_e vh_e; after each gauge
-    // max uh is in [1, 2). Sufficient for every iteration t >= 1: min uh >= 2 v_r 2^-110, and for
-    // every t: min vh >= n 2^-110 max vh (min / max over all t; t = 0 checked directly above).
+    // range form of the certificate (blocks with flushed entries; R38, R39): every real
+    // row and column of Kh holds a 1, so s_e >= min_i uh_i and acc_i >= min_e vh_e. Sufficient
+    // for every iteration t >= 1: min uh >= v_r 2^-110 max uh, and for every t: min vh >=
+    // n 2^-110 max vh, with min / max taken over all t (t = 0 checked directly above)
+    const uint32_t umax_h = half_max(umax_all, h);
     if (__any_sync(kFull, und_mine)) {
       const float vcap = (float)n * kUnder * __uint_as_float(half_max(__float_as_uint(vhi), h));
-      bad |= und_mine && (umin < 2.f * kv_s || vlo < vcap);
+      bad |= und_mine && (umin < kv_s * __uint_as_float(umax_h) || vlo < vcap);
     }
-    const bool flag = half_any(bad || !(umin >= FLT_MIN), h) || umax_all > 0x7f7fffffu || !(fabsf(wsum) <= FLT_MAX);
+    const bool flag = half_any(bad || !(umin >= FLT_MIN), h) || umax_h > 0x7f7fffffu || !(fabsf(wsum) <= FLT_MAX);
     if (l16 == 0 && j >= 0) {
       const int64_t o = (int64_t)q * qs.N + j;
       qs.dist[out0 + j] = wsum;
