@@ -522,7 +522,10 @@ __global__ void __launch_bounds__(kThreads, hmin_blocks<CW, NT, TW>()) sinkhorn_
         f |= kFlagFp32Range;
         qs.flagged_list[(int64_t)q * qs.N + atomicAdd(qs.flagged_count + q, 1)] = j;
       }
-      if (f) qs.flags[o] |= f;
+      // a plain store, not |=: the flags are zeroed at the query's start and this kernel is the
+      // first writer of its documents' bytes (the read of the RMW exposed a global-load latency
+      // per item, 2.5 % of the Scaling fused phase)
+      if (f) qs.flags[o] = f;
     }
     if (q + 1 < nq) {
       ++q;
