@@ -15,7 +15,7 @@ ncu -f --set full --import-source on --clock-control none -k regex:"sinkhorn_hal
 ncu -f --set full --import-source on --clock-control none -k regex:"build_mx" --launch-skip 1 --launch-count 1 \
     -o $R/scaling_build $B > gpurun_out/prof/ncu_scaling_build.log 2>&1
 $B --config long > gpurun_out/prof/plain_long.log 2>&1 || exit 4
-ncu -f --set full --import-source on --clock-control none -k regex:"sinkhorn_cta" --launch-skip 5 --launch-count 5 \
+ncu -f --set full --import-source on --clock-control none -k regex:"sinkhorn_cta" --launch-skip 8 --launch-count 8 \
     -o $R/long_cta $B --config long > gpurun_out/prof/ncu_long_cta.log 2>&1
 ncu -f --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/prof/launches_scaling.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-roofbench > gpurun_out/prof/ncu_launches.log 2>&1
