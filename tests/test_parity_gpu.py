@@ -294,6 +294,24 @@ def test_query_width_boundaries(W, path, v_r):
     assert_parity(g, o, f"v_r={v_r}")
 
 
+@pytest.mark.parametrize("iters", [14, 15, 16, 30])
+def test_cta_reanchor_single_document(W, iters):
+    """The deterministic repro of the one-CTA kernel's fault: Tiny document 24
+    alone against the v_r = 128 query of test_query_width_boundaries (2-warp instance at ld = 128,
+    warp 1 without valid rows). Its smallest row sum fails the s-side range check at pass 15, so
+    from 15 iterations on the re-anchor path runs and re-reads the block's rows (load_D) — where a
+    CS2R-zeroed row offset was read stale in the builds that faulted."""
+    wl = synth.make_workload("tiny")
+    rng = np.random.default_rng(128)
+    q = np.sort(rng.choice(wl.cfg.V, 128, replace=False)).astype(np.int32)
+    cnt = rng.geometric(0.5, 128).astype(np.float64)
+    w = (cnt / cnt.sum()).astype(np.float32)
+    cp, ri, va = synth.subset_docs(wl.col_ptr, wl.row_idx, wl.val, np.array([24]))
+    g = run_gpu(W, wl.E, cp, ri, va, q, w, 10.0, iters, path=2)
+    o = oracle.sinkhorn_wmd(wl.E, cp, ri, va, q, w, 10.0, iters)
+    assert_parity(g, o, f"document 24, {iters} iterations")
+
+
 @pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("iters", [0, 1, 2, 40, 100])
 def test_iteration_counts(W, path, iters):
